@@ -1,0 +1,166 @@
+/*
+ * kvmig.h — C ABI of the B200-native KV-migration data plane (libkvmig.so).
+ *
+ * Drop-in boundary for the data-plane hole in the reference simulator
+ * (kvpack, arXiv 2501.06709 "Mell"): the reference planner emits
+ * `MigrationPlan.executed` (/root/reference/pkg/src/kvpack/migration.py:119-121)
+ * and its only consumer, the slot loop, simply deletes the records
+ * (/root/reference/pkg/src/kvpack/sim.py:221-223).  Each entry point below is
+ * what a maintainer binds at that spot (ctypes stub in INTEGRATION.md):
+ *
+ *   kvm_migrate        executes PlannedMove(mode in {kv_transfer,
+ *                      forced_kv_transfer})            migration.py:155-158,164-167
+ *   kvm_reprefill      executes PlannedMove(mode == token_transfer): the
+ *                      re-prefill the cost model prices at
+ *                      tokens / prefill_tokens_per_s   migration.py:159-163
+ *   kvm_compact        1-GPU case: src pool == dst pool (defragmentation)
+ *   kvm_pool_register  the per-GPU KV capacity that ClusterState models as
+ *                      `capacity_bytes`                model.py:122-131
+ *
+ * Conventions
+ *   - Plain C types only; no C++ exceptions cross this ABI.
+ *   - Every call returns KVM_OK (0) or a negative KVM_ERR_* code; the text of
+ *     the last failure on the calling thread is kvm_last_error().  The Python
+ *     wrapper maps codes onto the reference's exception classes
+ *     (errors.py:4-32): KVM_ERR_CONFIG -> ConfigError, KVM_ERR_INVALID ->
+ *     ValueError, KVM_ERR_NOT_FOUND -> NotPlaced, KVM_ERR_CUDA -> KvmCudaError
+ *     (a KvPackError subclass).
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - The library never allocates or frees pool memory: pools are borrowed
+ *     device allocations (e.g. torch tensors) registered by pointer.
+ *   - KV layout (frozen, vLLM-style layer-major):
+ *         pool[layers][2 (K,V)][num_blocks][block_tokens][kv_heads][head_dim]
+ *     One (layer, K|V, block) "piece" is contiguous:
+ *         piece_bytes = block_tokens * kv_heads * head_dim * elem_bytes.
+ */
+#ifndef KVMIG_H
+#define KVMIG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVM_ABI_VERSION 1
+
+#define KVM_OK 0
+#define KVM_ERR_INVALID (-1)     /* bad argument              -> ValueError   */
+#define KVM_ERR_CONFIG (-2)      /* bad pool/topology config  -> ConfigError  */
+#define KVM_ERR_CUDA (-3)        /* CUDA runtime failure      -> KvmCudaError */
+#define KVM_ERR_NOT_FOUND (-4)   /* unknown pool id           -> NotPlaced    */
+#define KVM_ERR_UNSUPPORTED (-5) /* feature not built / device too old        */
+
+/* kvm_migrate flags */
+#define KVM_F_BLOCKS_ON_HOST 0x1 /* src_blocks/dst_blocks are host pointers; the
+                                    library stages them to the device inside the
+                                    call (pinned ring + async H2D on `stream`) */
+#define KVM_F_ENGINE_BULK 0x2    /* copy engine: TMA bulk (cp.async.bulk) through
+                                    shared memory instead of LDG.128/STG.128  */
+
+/* Pool geometry. */
+typedef struct kvm_pool_desc {
+  int32_t layers;
+  int32_t kv_heads;
+  int32_t head_dim;
+  int32_t block_tokens;
+  int32_t num_blocks;
+  int32_t elem_bytes; /* 2 for fp16/bf16 */
+} kvm_pool_desc;
+
+/* One physical KV transfer: the executed form of a reference PendingMove
+ * (migration.py:94-102).  Block i of the request lives in src block
+ * src_blocks[i] and lands in dst block dst_blocks[i], for every layer and
+ * for both K and V.  Completion side effects, all optional (NULL = skip),
+ * are written by the kernel itself with system-scope release semantics so
+ * they become visible only after the KV bytes:
+ *   dst_table_row[i] = dst_blocks[i]   (the destination block-table rewrite)
+ *   layer_flags[l]   = done_value      (layer l of this move has landed)
+ *   *done_flag       = done_value      (whole move has landed)
+ * These pointers may point into a peer GPU (P2P / IPC-mapped) allocation. */
+typedef struct kvm_move {
+  int32_t src_pool;
+  int32_t dst_pool;
+  int32_t n_blocks;
+  uint32_t done_value;
+  const int32_t* src_blocks;
+  const int32_t* dst_blocks;
+  int32_t* dst_table_row;
+  uint32_t* done_flag;
+  uint32_t* layer_flags;
+} kvm_move;
+
+/* Re-prefill (token_transfer) of the suffix of a request on the destination:
+ * for every layer l,  [Q | K | V] = X[rows] @ W[l]^T  (bf16 in, fp32 accumulate,
+ * bf16 out), with K and V scattered straight into the destination pool blocks
+ * (token t goes to block dst_blocks[(tok0 + t) / block_tokens], slot
+ * (tok0 + t) % block_tokens) and Q optionally written densely to q_out.
+ * W[l] is row-major [n_out][d_model] (nn.Linear layout), n_out = q_cols +
+ * 2 * kv_heads * head_dim; q_cols may be 0 (KV-only projection). */
+typedef struct kvm_reprefill_args {
+  int32_t dst_pool;
+  int32_t rows;    /* s: tokens to recompute */
+  int32_t d_model; /* K of the contraction */
+  int32_t q_cols;  /* 0 or num_heads * head_dim */
+  int32_t tok0;    /* absolute index of the first recomputed token */
+  int32_t n_dst_blocks;
+  const void* x;          /* bf16 [rows][d_model], device */
+  const void* w;          /* bf16 [layers][n_out][d_model], device */
+  void* q_out;            /* bf16 [layers][rows][q_cols] or NULL */
+  const int32_t* dst_blocks; /* device, n_dst_blocks entries */
+  uint32_t* done_flag;    /* optional, set to done_value when all layers landed */
+  uint32_t done_value;
+  int32_t flags;          /* reserved, 0 */
+} kvm_reprefill_args;
+
+/* --- library / device ---------------------------------------------------- */
+int kvm_version(void);
+const char* kvm_last_error(void);
+int kvm_device_count(int* n_out);
+/* Enable all-pairs peer access between visible devices (single-process,
+ * multi-device mode).  Harmless when n_dev == 1. */
+int kvm_init(int enable_peer_access);
+int kvm_can_access_peer(int dev, int peer, int* out);
+
+/* --- pools ----------------------------------------------------------------- */
+/* Register a borrowed device allocation as a pool; returns pool id >= 0. */
+int kvm_pool_register(int device, void* base, const kvm_pool_desc* desc);
+int kvm_pool_unregister(int pool);
+int kvm_pool_piece_bytes(int pool, int64_t* out);
+int kvm_pool_bytes(const kvm_pool_desc* desc, int64_t* out);
+
+/* --- cross-process peer memory (one process per GPU) ----------------------- */
+/* Export the allocation containing `ptr` (64-byte opaque handle) and ptr's
+ * offset from the allocation base. */
+int kvm_ipc_export(const void* ptr, void* handle64, int64_t* offset_out);
+/* Map a peer process's exported allocation into this process (on `device`)
+ * and return base + offset. */
+int kvm_ipc_import(int device, const void* handle64, int64_t offset,
+                   void** ptr_out);
+int kvm_ipc_close(void* mapped_ptr, int64_t offset);
+
+/* --- data path -------------------------------------------------------------- */
+/* Launch one fused gather -> push -> block-table-rewrite kernel for up to
+ * KVM_MAX_MOVES moves (larger batches are split internally), on the device
+ * that owns the first move's source pool.  Asynchronous on `stream`. */
+#define KVM_MAX_MOVES 96
+int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream);
+/* src pool == dst pool: move n blocks of one request into fresh blocks. */
+int kvm_compact(int pool, const int32_t* src_blocks, const int32_t* dst_blocks,
+                int n_blocks, int32_t* table_row, int flags, void* stream);
+/* Device-side wait until *flag >= value (unsigned; system-scope acquire), on
+ * `stream`: makes a peer's completion flag a stream dependency of the
+ * destination.  Flags carry monotonically increasing sequence numbers. */
+int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream);
+/* tcgen05 re-prefill projection (see kvm_reprefill_args). */
+int kvm_reprefill(const kvm_reprefill_args* args, void* stream);
+
+/* --- instrumentation -------------------------------------------------------- */
+/* Number of data-path kernels this process has launched through the ABI. */
+int64_t kvm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVMIG_H */

@@ -1,0 +1,14 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+CPU restatements of the reference's migration path, used as the checker by
+tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+leg.  The product package (paper_2501_06709_b200) never imports this package.
+
+  planner.py          plan_hybrid & co. (migration.py), parity pinned against
+                      tests/golden/*.json generated from the reference itself.
+  kvmig_oracle.c      the byte path (migrate / allocate / re-prefill) in C;
+                      the reference moves no bytes, so the byte layout is frozen
+                      by this repo and pinned by identity / known-answer
+                      properties (see the C header).
+  kvmig_oracle.py     ctypes wrapper over liboracle_kvmig.so (built by Makefile).
+"""

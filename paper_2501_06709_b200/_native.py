@@ -1,0 +1,127 @@
+"""ctypes binding of libkvmig.so (include/kvmig.h).
+
+This is the only way the package reaches the GPU.  If the library is absent
+the import of any data-path object fails loudly (NativeLibraryMissing); there
+is no eager-PyTorch or CPU fallback for the copy or the re-prefill.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigError, KvmCudaError, KvmUnsupported, NativeLibraryMissing, NotPlaced
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libkvmig.so")
+
+KVM_OK = 0
+KVM_ERR_INVALID = -1
+KVM_ERR_CONFIG = -2
+KVM_ERR_CUDA = -3
+KVM_ERR_NOT_FOUND = -4
+KVM_ERR_UNSUPPORTED = -5
+
+KVM_F_BLOCKS_ON_HOST = 0x1
+KVM_F_ENGINE_BULK = 0x2
+KVM_MAX_MOVES = 96
+
+# Every symbol include/kvmig.h declares (checked by tests/test_native_abi.py).
+EXPORTS = (
+    "kvm_version", "kvm_last_error", "kvm_device_count", "kvm_init", "kvm_can_access_peer",
+    "kvm_pool_register", "kvm_pool_unregister", "kvm_pool_piece_bytes", "kvm_pool_bytes",
+    "kvm_ipc_export", "kvm_ipc_import", "kvm_ipc_close",
+    "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_launch_count",
+)
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [("layers", ctypes.c_int32), ("kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("block_tokens", ctypes.c_int32),
+                ("num_blocks", ctypes.c_int32), ("elem_bytes", ctypes.c_int32)]
+
+
+class Move(ctypes.Structure):
+    _fields_ = [("src_pool", ctypes.c_int32), ("dst_pool", ctypes.c_int32),
+                ("n_blocks", ctypes.c_int32), ("done_value", ctypes.c_uint32),
+                ("src_blocks", ctypes.c_void_p), ("dst_blocks", ctypes.c_void_p),
+                ("dst_table_row", ctypes.c_void_p), ("done_flag", ctypes.c_void_p),
+                ("layer_flags", ctypes.c_void_p)]
+
+
+class ReprefillArgs(ctypes.Structure):
+    _fields_ = [("dst_pool", ctypes.c_int32), ("rows", ctypes.c_int32),
+                ("d_model", ctypes.c_int32), ("q_cols", ctypes.c_int32),
+                ("tok0", ctypes.c_int32), ("n_dst_blocks", ctypes.c_int32),
+                ("x", ctypes.c_void_p), ("w", ctypes.c_void_p), ("q_out", ctypes.c_void_p),
+                ("dst_blocks", ctypes.c_void_p), ("done_flag", ctypes.c_void_p),
+                ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(L: ctypes.CDLL) -> None:
+    I, P, I64 = ctypes.c_int, ctypes.c_void_p, ctypes.c_int64
+    sig = {
+        "kvm_version": ([], I),
+        "kvm_last_error": ([], ctypes.c_char_p),
+        "kvm_device_count": ([ctypes.POINTER(I)], I),
+        "kvm_init": ([I], I),
+        "kvm_can_access_peer": ([I, I, ctypes.POINTER(I)], I),
+        "kvm_pool_register": ([I, P, ctypes.POINTER(PoolDesc)], I),
+        "kvm_pool_unregister": ([I], I),
+        "kvm_pool_piece_bytes": ([I, ctypes.POINTER(I64)], I),
+        "kvm_pool_bytes": ([ctypes.POINTER(PoolDesc), ctypes.POINTER(I64)], I),
+        "kvm_ipc_export": ([P, P, ctypes.POINTER(I64)], I),
+        "kvm_ipc_import": ([I, P, I64, ctypes.POINTER(P)], I),
+        "kvm_ipc_close": ([P, I64], I),
+        "kvm_migrate": ([ctypes.POINTER(Move), I, I, P], I),
+        "kvm_compact": ([I, P, P, I, P, I, P], I),
+        "kvm_wait_flag": ([P, ctypes.c_uint32, P], I),
+        "kvm_reprefill": ([ctypes.POINTER(ReprefillArgs), P], I),
+        "kvm_launch_count": ([], I64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib() -> ctypes.CDLL:
+    """Load libkvmig.so once; raise NativeLibraryMissing if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeLibraryMissing(
+                    f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                    " (there is no CPU fallback for the KV data path)")
+            L = ctypes.CDLL(LIB_PATH)
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = "") -> int:
+    """Map a KVM_ERR_* return code onto the reference's exception classes."""
+    if rc >= 0:
+        return rc
+    msg = lib().kvm_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == KVM_ERR_INVALID:
+        raise ValueError(text)
+    if rc == KVM_ERR_CONFIG:
+        raise ConfigError(text)
+    if rc == KVM_ERR_NOT_FOUND:
+        raise NotPlaced(text)
+    if rc == KVM_ERR_UNSUPPORTED:
+        raise KvmUnsupported(text)
+    raise KvmCudaError(text)
+
+
+def launch_count() -> int:
+    return int(lib().kvm_launch_count())

@@ -1,0 +1,821 @@
+// libkvmig.so — B200 (sm_100a) KV-migration data plane behind the C ABI in
+// include/kvmig.h.
+//
+// What the reference does at this spot: nothing moves.  plan_hybrid labels a
+// PendingMove kv_transfer / forced_kv_transfer (migration.py:155-158, 164-167)
+// and sim.run deletes the record (sim.py:221-223).  Here an executed move is a
+// real transfer of the request's paged KV cache:
+//
+//   for every layer l, for K and V, for every logical block i of the request:
+//       dst_pool[l][kv][dst_blocks[i]]  <-  src_pool[l][kv][src_blocks[i]]
+//   then  dst_table_row[i] = dst_blocks[i];  *done_flag = done_value
+//
+// One persistent launch covers a whole batch of moves (all moves of one slot
+// that leave the same source GPU).  Work unit = one 32 KiB "tile" of a piece;
+// tiles are enumerated move-major, then (layer, K|V) plane, then block, so the
+// grid-stride sweep finishes layer 0 of a move before layer 1 (layer-by-layer
+// pipelining: layer_flags[l] is published as soon as every tile of layer l
+// has landed).  The kernel runs on the SOURCE GPU and pushes: local HBM loads,
+// stores straight to the destination pool, which may be a peer GPU's HBM
+// (UVA peer pointer or CUDA-IPC mapping) so the stores cross NVLink/NVSwitch.
+//
+// Two copy engines:
+//   * LDG engine  : 256 threads, each moving 8 x 16 B per tile with
+//                   ld.global.nc.L1::no_allocate / st.global (coalesced 128-bit).
+//   * bulk engine : one warp per CTA, lane 0 drives cp.async.bulk (the TMA
+//                   bulk-copy unit) global->smem->global through an S-stage
+//                   mbarrier ring; no register staging at all.
+//
+// Completion protocol (cross-GPU memory ordering): every CTA, when it leaves a
+// (move, layer) key, does bar.sync; fence.acq_rel.sys; atomicAdd(counter, k).
+// The CTA whose add completes a layer publishes layer_flags[l] with
+// st.release.sys; the CTA that completes the last layer rewrites the
+// destination block-table row, fences, and st.release.sys's done_flag.  The
+// counters self-reset so a staging slot can be reused without a memset.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kvmig_common.cuh"
+
+namespace kvm {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string t_last_error;
+
+int fail(int code, const std::string& msg) {
+  t_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  t_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                 cudaGetErrorString(e) + ")";
+  return KVM_ERR_CUDA;
+}
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int64_t n) { g_launches.fetch_add(n); }
+
+// ---------------------------------------------------------------------------
+// pool registry
+// ---------------------------------------------------------------------------
+static std::mutex g_mu;
+static std::vector<Pool> g_pools;
+
+const Pool* get_pool(int id) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (id < 0 || id >= (int)g_pools.size() || !g_pools[id].live) {
+    fail(KVM_ERR_NOT_FOUND, "unknown pool id " + std::to_string(id));
+    return nullptr;
+  }
+  return &g_pools[id];  // entries are never erased, only marked dead
+}
+
+static int g_sm_count[64] = {0};
+int sm_count(int device) {
+  if (device < 0 || device >= 64) return 148;
+  if (g_sm_count[device] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0)
+      n = 148;
+    g_sm_count[device] = n;
+  }
+  return g_sm_count[device];
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+constexpr int kTileBytes = 32 * 1024;   // work unit
+constexpr int kLdgThreads = 256;
+constexpr int kLdgVecPerThread = kTileBytes / 16 / kLdgThreads;  // 8
+
+struct DevMove {
+  const uint8_t* src;        // src pool base
+  uint8_t* dst;              // dst pool base (may be a peer mapping)
+  const int32_t* src_blocks; // device
+  const int32_t* dst_blocks; // device
+  int32_t* table_row;        // nullable
+  uint32_t* done_flag;       // nullable
+  uint32_t* layer_flags;     // nullable
+  uint32_t* ctr;             // [layers + 1] self-resetting counters
+  int64_t src_plane;         // bytes per (layer, K|V) plane in src pool
+  int64_t dst_plane;
+  int64_t tile_begin;        // first global tile index of this move
+  int32_t piece;             // bytes per piece (same for src and dst)
+  int32_t tpp;               // tiles per piece
+  int32_t n_blocks;
+  int32_t layers;
+  uint32_t done_value;
+  int32_t _pad;
+};
+
+struct MigrateParams {
+  int32_t n_moves;
+  int32_t per_layer_flush;   // 1: flush at (move, layer) granularity
+  int64_t total_tiles;
+  DevMove m[KVM_MAX_MOVES];
+};
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+struct TileRef {
+  int move;
+  int layer;
+  const uint8_t* src;
+  uint8_t* dst;
+  int len;
+};
+
+__device__ __forceinline__ TileRef decode_tile(const MigrateParams& p, int64_t t, int& cur) {
+  while (cur + 1 < p.n_moves && t >= p.m[cur + 1].tile_begin) ++cur;
+  const DevMove& mv = p.m[cur];
+  const int32_t local = (int32_t)(t - mv.tile_begin);
+  const int32_t per_plane = mv.n_blocks * mv.tpp;
+  const int32_t plane = local / per_plane;
+  const int32_t r = local - plane * per_plane;
+  const int32_t bi = r / mv.tpp;
+  const int32_t ti = r - bi * mv.tpp;
+  const int64_t sb = __ldg(mv.src_blocks + bi);
+  const int64_t db = __ldg(mv.dst_blocks + bi);
+  const int64_t off = (int64_t)ti * kTileBytes;
+  TileRef tr;
+  tr.move = cur;
+  tr.layer = plane >> 1;
+  tr.src = mv.src + plane * mv.src_plane + sb * mv.piece + off;
+  tr.dst = mv.dst + plane * mv.dst_plane + db * mv.piece + off;
+  tr.len = min((int64_t)kTileBytes, (int64_t)mv.piece - off);
+  return tr;
+}
+
+// Called by ONE thread after the CTA's stores for `key` are ordered before it
+// (bar.sync / bulk wait_group + this fence).  Returns 1 if this call completed
+// the whole move (caller then runs finalize_move with the CTA / warp).
+__device__ __forceinline__ int account(const MigrateParams& p, int move, int layer, int ntiles) {
+  const DevMove& mv = p.m[move];
+  fence_acq_rel_sys();
+  const uint32_t per_layer = 2u * (uint32_t)mv.n_blocks * (uint32_t)mv.tpp;
+  if (p.per_layer_flush) {
+    uint32_t old = atomicAdd(mv.ctr + layer, (uint32_t)ntiles);
+    if (old + (uint32_t)ntiles == per_layer) {
+      mv.ctr[layer] = 0;  // self-reset: nobody else touches it this launch
+      fence_acq_rel_sys();
+      if (mv.layer_flags) st_release_sys_u32(mv.layer_flags + layer, mv.done_value);
+      uint32_t o2 = atomicAdd(mv.ctr + mv.layers, 1u);
+      if (o2 + 1 == (uint32_t)mv.layers) {
+        mv.ctr[mv.layers] = 0;
+        fence_acq_rel_sys();
+        return 1;
+      }
+    }
+  } else {
+    const uint32_t total = per_layer * (uint32_t)mv.layers;
+    uint32_t old = atomicAdd(mv.ctr + mv.layers, (uint32_t)ntiles);
+    if (old + (uint32_t)ntiles == total) {
+      mv.ctr[mv.layers] = 0;
+      fence_acq_rel_sys();
+      return 1;
+    }
+  }
+  return 0;
+}
+
+// Block-table rewrite + done flag; executed by `nthr` cooperating threads,
+// `tid` in [0, nthr).  sync() must order all threads' table stores before the
+// single release store of the flag.
+template <bool kCta>
+__device__ __forceinline__ void finalize_move(const DevMove& mv, int tid, int nthr) {
+  if (mv.table_row) {
+    for (int i = tid; i < mv.n_blocks; i += nthr) mv.table_row[i] = __ldg(mv.dst_blocks + i);
+  }
+  if (kCta) __syncthreads(); else __syncwarp();
+  if (tid == 0) {
+    fence_acq_rel_sys();
+    if (mv.done_flag) st_release_sys_u32(mv.done_flag, mv.done_value);
+  }
+}
+
+// ------------------------- LDG/STG engine ----------------------------------
+__global__ void __launch_bounds__(kLdgThreads)
+    migrate_ldg_kernel(const __grid_constant__ MigrateParams p) {
+  __shared__ int s_done;
+  int cur = 0;
+  int key_move = -1, key_layer = -1, key_n = 0;
+  const int tid = threadIdx.x;
+  for (int64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    TileRef tr = decode_tile(p, t, cur);
+    const int lay = p.per_layer_flush ? tr.layer : 0;
+    if (tr.move != key_move || lay != key_layer) {
+      if (key_move >= 0) {
+        __syncthreads();
+        if (tid == 0) s_done = account(p, key_move, key_layer, key_n);
+        __syncthreads();
+        if (s_done) finalize_move<true>(p.m[key_move], tid, kLdgThreads);
+      }
+      key_move = tr.move;
+      key_layer = lay;
+      key_n = 0;
+    }
+    const int4* s = reinterpret_cast<const int4*>(tr.src);
+    int4* d = reinterpret_cast<int4*>(tr.dst);
+    const int nvec = tr.len >> 4;
+    if (nvec == kLdgThreads * kLdgVecPerThread) {
+      int4 v[kLdgVecPerThread];
+#pragma unroll
+      for (int k = 0; k < kLdgVecPerThread; ++k) v[k] = ld_stream(s + tid + k * kLdgThreads);
+#pragma unroll
+      for (int k = 0; k < kLdgVecPerThread; ++k) st_stream(d + tid + k * kLdgThreads, v[k]);
+    } else {
+      int4 v[kLdgVecPerThread];
+#pragma unroll
+      for (int k = 0; k < kLdgVecPerThread; ++k) {
+        int i = tid + k * kLdgThreads;
+        if (i < nvec) v[k] = ld_stream(s + i);
+      }
+#pragma unroll
+      for (int k = 0; k < kLdgVecPerThread; ++k) {
+        int i = tid + k * kLdgThreads;
+        if (i < nvec) st_stream(d + i, v[k]);
+      }
+    }
+    ++key_n;
+  }
+  if (key_move >= 0) {
+    __syncthreads();
+    if (tid == 0) s_done = account(p, key_move, key_layer, key_n);
+    __syncthreads();
+    if (s_done) finalize_move<true>(p.m[key_move], tid, kLdgThreads);
+  }
+}
+
+// ------------------------- bulk-copy (TMA unit) engine ---------------------
+constexpr int kBulkStages = 4;
+constexpr int kBulkLag = 2;   // loads in flight; stages - lag stores in flight
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// One warp per CTA; lane 0 drives the bulk unit, the warp cooperates on the
+// block-table rewrite.  Dynamic smem: kBulkStages * kTileBytes + barriers.
+__global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant__ MigrateParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * kTileBytes);
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t first = blockIdx.x;
+  const int64_t stride = gridDim.x;
+  const int64_t my_tiles = first < p.total_tiles ? (p.total_tiles - 1 - first) / stride + 1 : 0;
+
+  int cur_ld = 0;
+  int key_move = -1, key_layer = -1, key_n = 0;
+  // Stored-tile metadata ring (lane 0 only): dst pointer, len, move, layer.
+  uint8_t* st_dst[kBulkStages];
+  int st_len[kBulkStages], st_move[kBulkStages], st_layer[kBulkStages];
+
+  for (int64_t i = 0; i < my_tiles + kBulkLag; ++i) {
+    // ---- store side: tile j = i - lag ----
+    const int64_t j = i - kBulkLag;
+    if (j >= 0) {
+      const int sj = (int)(j % kBulkStages);
+      int mv = 0, ly = 0;
+      if (lane == 0) { mv = st_move[sj]; ly = st_layer[sj]; }
+      mv = __shfl_sync(0xffffffffu, mv, 0);
+      ly = __shfl_sync(0xffffffffu, ly, 0);
+      if (mv != key_move || ly != key_layer) {
+        if (key_move >= 0) {
+          int done = 0;
+          if (lane == 0) {
+            bulk_wait_all();
+            done = account(p, key_move, key_layer, key_n);
+          }
+          done = __shfl_sync(0xffffffffu, done, 0);
+          if (done) finalize_move<false>(p.m[key_move], lane, 32);
+        }
+        key_move = mv;
+        key_layer = ly;
+        key_n = 0;
+      }
+      if (lane == 0) {
+        mbar_wait(full + sj, (uint32_t)((j / kBulkStages) & 1));
+        bulk_s2g(st_dst[sj], smem + sj * kTileBytes, (uint32_t)st_len[sj]);
+      }
+      ++key_n;
+    }
+    // ---- load side: tile i ----
+    if (i < my_tiles) {
+      if (lane == 0) {
+        const int si = (int)(i % kBulkStages);
+        // slot si last held tile i - stages; its store must have finished reading smem.
+        bulk_wait_read<kBulkStages - kBulkLag>();
+        TileRef tr = decode_tile(p, first + i * stride, cur_ld);
+        st_dst[si] = tr.dst;
+        st_len[si] = tr.len;
+        st_move[si] = tr.move;
+        st_layer[si] = p.per_layer_flush ? tr.layer : 0;
+        mbar_expect_tx(full + si, (uint32_t)tr.len);
+        bulk_g2s(smem + si * kTileBytes, tr.src, (uint32_t)tr.len, full + si);
+      }
+    }
+  }
+  if (key_move >= 0) {
+    int done = 0;
+    if (lane == 0) {
+      bulk_wait_all();
+      done = account(p, key_move, key_layer, key_n);
+    }
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (done) finalize_move<false>(p.m[key_move], lane, 32);
+  }
+}
+
+// Moves with zero blocks: publish their (empty) completion without a copy.
+__global__ void finalize_empty_kernel(const __grid_constant__ MigrateParams p) {
+  for (int m = 0; m < p.n_moves; ++m) {
+    const DevMove& mv = p.m[m];
+    if (mv.n_blocks != 0) continue;
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      if (mv.layer_flags)
+        for (int l = 0; l < mv.layers; ++l) st_release_sys_u32(mv.layer_flags + l, mv.done_value);
+      if (mv.done_flag) st_release_sys_u32(mv.done_flag, mv.done_value);
+    }
+  }
+}
+
+__global__ void wait_flag_kernel(const uint32_t* flag, uint32_t value) {
+  if (threadIdx.x == 0) {
+    unsigned ns = 32;
+    while (ld_acquire_sys_u32(flag) < value) {
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-device staging ring (pinned host -> device block lists + counters)
+// ---------------------------------------------------------------------------
+struct Slot {
+  void* host = nullptr;        // pinned
+  uint8_t* dev = nullptr;      // device: block lists
+  size_t cap = 0;
+  uint32_t* ctr = nullptr;     // device counters (zeroed once, self-resetting)
+  size_t ctr_cap = 0;          // in uint32
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+constexpr int kSlots = 16;
+struct DevState {
+  bool init = false;
+  Slot slots[kSlots];
+  int next = 0;
+  int ldg_grid = 0;
+  int bulk_grid = 0;
+};
+static DevState g_dev[64];
+static std::mutex g_dev_mu[64];
+
+static int dev_init(int device, DevState& ds) {
+  if (ds.init) return KVM_OK;
+  for (int i = 0; i < kSlots; ++i)
+    KVM_CUDA_TRY(cudaEventCreateWithFlags(&ds.slots[i].ev, cudaEventDisableTiming));
+  int occ = 0;
+  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, migrate_ldg_kernel, kLdgThreads, 0));
+  ds.ldg_grid = sm_count(device) * std::max(occ, 1);
+  const size_t bulk_smem = kBulkStages * kTileBytes + 64;
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bulk_smem));
+  int occb = 0;
+  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occb, migrate_bulk_kernel, 32, bulk_smem));
+  ds.bulk_grid = sm_count(device) * std::max(occb, 1);
+  ds.init = true;
+  return KVM_OK;
+}
+
+static int slot_acquire(DevState& ds, size_t bytes, size_t ctrs, Slot** out) {
+  Slot& s = ds.slots[ds.next];
+  ds.next = (ds.next + 1) % kSlots;
+  if (s.pending) {
+    KVM_CUDA_TRY(cudaEventSynchronize(s.ev));
+    s.pending = false;
+  }
+  if (bytes > s.cap) {
+    size_t cap = std::max<size_t>(bytes, 64 * 1024);
+    if (s.host) cudaFreeHost(s.host);
+    if (s.dev) cudaFree(s.dev);
+    s.host = nullptr;
+    s.dev = nullptr;
+    s.cap = 0;
+    KVM_CUDA_TRY(cudaMallocHost(&s.host, cap));
+    KVM_CUDA_TRY(cudaMalloc(&s.dev, cap));
+    s.cap = cap;
+  }
+  if (ctrs > s.ctr_cap) {
+    size_t cap = std::max<size_t>(ctrs, 4096);
+    if (s.ctr) cudaFree(s.ctr);
+    s.ctr = nullptr;
+    KVM_CUDA_TRY(cudaMalloc(&s.ctr, cap * sizeof(uint32_t)));
+    KVM_CUDA_TRY(cudaMemset(s.ctr, 0, cap * sizeof(uint32_t)));
+    s.ctr_cap = cap;
+  }
+  *out = &s;
+  return KVM_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static int validate_blocks_host(const int32_t* b, int n, int nb, const char* what) {
+  for (int i = 0; i < n; ++i)
+    if (b[i] < 0 || b[i] >= nb)
+      return fail(KVM_ERR_INVALID, std::string(what) + "[" + std::to_string(i) + "] = " +
+                                       std::to_string(b[i]) + " out of range [0, " +
+                                       std::to_string(nb) + ")");
+  return KVM_OK;
+}
+
+static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t stream) {
+  const Pool* sp0 = get_pool(moves[0].src_pool);
+  if (!sp0) return KVM_ERR_NOT_FOUND;
+  const int device = sp0->device;
+  std::lock_guard<std::mutex> lk(g_dev_mu[device]);
+  DeviceGuard dg(device);
+  DevState& ds = g_dev[device];
+  int rc = dev_init(device, ds);
+  if (rc) return rc;
+
+  static MigrateParams p;  // large; guarded by g_dev_mu[device] (one device at a time per call)
+  static std::mutex p_mu;
+  std::lock_guard<std::mutex> lkp(p_mu);
+  memset(&p, 0, sizeof(p));
+  p.n_moves = n;
+  bool any_layer_flags = false;
+  size_t host_bytes = 0, ctrs = 0;
+  int64_t tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const kvm_move& mv = moves[i];
+    const Pool* sp = get_pool(mv.src_pool);
+    const Pool* dp = get_pool(mv.dst_pool);
+    if (!sp || !dp) return KVM_ERR_NOT_FOUND;
+    if (sp->device != device)
+      return fail(KVM_ERR_INVALID, "all moves of one kvm_migrate batch must leave the same device");
+    const kvm_pool_desc& a = sp->desc;
+    const kvm_pool_desc& b = dp->desc;
+    if (a.layers != b.layers || a.kv_heads != b.kv_heads || a.head_dim != b.head_dim ||
+        a.block_tokens != b.block_tokens || a.elem_bytes != b.elem_bytes)
+      return fail(KVM_ERR_CONFIG, "move " + std::to_string(i) + ": src and dst pools differ in KV shape");
+    if (mv.n_blocks < 0) return fail(KVM_ERR_INVALID, "n_blocks < 0");
+    if (mv.n_blocks > 0 && (!mv.src_blocks || !mv.dst_blocks))
+      return fail(KVM_ERR_INVALID, "NULL block list");
+    if (flags & KVM_F_BLOCKS_ON_HOST) {
+      if ((rc = validate_blocks_host(mv.src_blocks, mv.n_blocks, a.num_blocks, "src_blocks"))) return rc;
+      if ((rc = validate_blocks_host(mv.dst_blocks, mv.n_blocks, b.num_blocks, "dst_blocks"))) return rc;
+      host_bytes += 2 * sizeof(int32_t) * (size_t)mv.n_blocks;
+      host_bytes = (host_bytes + 15) & ~size_t(15);
+    }
+    if (mv.layer_flags) any_layer_flags = true;
+    ctrs += (size_t)a.layers + 1;
+    DevMove& d = p.m[i];
+    d.src = sp->base;
+    d.dst = dp->base;
+    d.table_row = mv.dst_table_row;
+    d.done_flag = mv.done_flag;
+    d.layer_flags = mv.layer_flags;
+    d.src_plane = sp->plane_bytes;
+    d.dst_plane = dp->plane_bytes;
+    d.piece = (int32_t)sp->piece_bytes;
+    d.tpp = (int32_t)((sp->piece_bytes + kTileBytes - 1) / kTileBytes);
+    d.n_blocks = mv.n_blocks;
+    d.layers = a.layers;
+    d.done_value = mv.done_value;
+    d.tile_begin = tiles;
+    tiles += (int64_t)mv.n_blocks * d.tpp * 2 * a.layers;
+  }
+  p.total_tiles = tiles;
+  p.per_layer_flush = any_layer_flags ? 1 : 0;
+
+  Slot* slot = nullptr;
+  if ((rc = slot_acquire(ds, host_bytes, ctrs, &slot))) return rc;
+  // stage host block lists and counters
+  size_t off = 0, coff = 0;
+  for (int i = 0; i < n; ++i) {
+    DevMove& d = p.m[i];
+    const kvm_move& mv = moves[i];
+    d.ctr = slot->ctr + coff;
+    coff += (size_t)d.layers + 1;
+    if (flags & KVM_F_BLOCKS_ON_HOST) {
+      uint8_t* h = static_cast<uint8_t*>(slot->host) + off;
+      memcpy(h, mv.src_blocks, sizeof(int32_t) * mv.n_blocks);
+      memcpy(h + sizeof(int32_t) * mv.n_blocks, mv.dst_blocks, sizeof(int32_t) * mv.n_blocks);
+      d.src_blocks = reinterpret_cast<const int32_t*>(slot->dev + off);
+      d.dst_blocks = reinterpret_cast<const int32_t*>(slot->dev + off + sizeof(int32_t) * mv.n_blocks);
+      off += 2 * sizeof(int32_t) * (size_t)mv.n_blocks;
+      off = (off + 15) & ~size_t(15);
+    } else {
+      d.src_blocks = mv.src_blocks;
+      d.dst_blocks = mv.dst_blocks;
+    }
+  }
+  if ((flags & KVM_F_BLOCKS_ON_HOST) && off > 0)
+    KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
+
+  bool any_empty = false;
+  for (int i = 0; i < n; ++i) any_empty |= (moves[i].n_blocks == 0);
+  if (tiles > 0) {
+    if (flags & KVM_F_ENGINE_BULK) {
+      int grid = (int)std::min<int64_t>(tiles, ds.bulk_grid);
+      migrate_bulk_kernel<<<grid, 32, kBulkStages * kTileBytes + 64, stream>>>(p);
+    } else {
+      int grid = (int)std::min<int64_t>(tiles, ds.ldg_grid);
+      migrate_ldg_kernel<<<grid, kLdgThreads, 0, stream>>>(p);
+    }
+    KVM_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  }
+  if (any_empty) {
+    finalize_empty_kernel<<<1, 32, 0, stream>>>(p);
+    KVM_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  }
+  KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
+  slot->pending = true;
+  return KVM_OK;
+}
+
+}  // namespace kvm
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace kvm;
+
+extern "C" {
+
+int kvm_version(void) { return KVM_ABI_VERSION; }
+const char* kvm_last_error(void) { return t_last_error.c_str(); }
+int64_t kvm_launch_count(void) { return g_launches.load(); }
+
+int kvm_device_count(int* n_out) {
+  if (!n_out) return fail(KVM_ERR_INVALID, "n_out is NULL");
+  KVM_CUDA_TRY(cudaGetDeviceCount(n_out));
+  return KVM_OK;
+}
+
+int kvm_can_access_peer(int dev, int peer, int* out) {
+  if (!out) return fail(KVM_ERR_INVALID, "out is NULL");
+  if (dev == peer) {
+    *out = 1;
+    return KVM_OK;
+  }
+  KVM_CUDA_TRY(cudaDeviceCanAccessPeer(out, dev, peer));
+  return KVM_OK;
+}
+
+int kvm_init(int enable_peer_access) {
+  int n = 0;
+  KVM_CUDA_TRY(cudaGetDeviceCount(&n));
+  if (!enable_peer_access || n < 2) return KVM_OK;
+  int prev = 0;
+  KVM_CUDA_TRY(cudaGetDevice(&prev));
+  for (int a = 0; a < n; ++a) {
+    KVM_CUDA_TRY(cudaSetDevice(a));
+    for (int b = 0; b < n; ++b) {
+      if (a == b) continue;
+      int can = 0;
+      KVM_CUDA_TRY(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) continue;
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        continue;
+      }
+      if (e != cudaSuccess) {
+        cudaSetDevice(prev);
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  }
+  KVM_CUDA_TRY(cudaSetDevice(prev));
+  return KVM_OK;
+}
+
+int kvm_pool_bytes(const kvm_pool_desc* d, int64_t* out) {
+  if (!d || !out) return fail(KVM_ERR_INVALID, "NULL argument");
+  if (d->layers <= 0 || d->kv_heads <= 0 || d->head_dim <= 0 || d->block_tokens <= 0 ||
+      d->num_blocks <= 0 || d->elem_bytes <= 0)
+    return fail(KVM_ERR_CONFIG, "pool geometry fields must all be > 0");
+  *out = (int64_t)d->layers * 2 * d->num_blocks * d->block_tokens * d->kv_heads * d->head_dim *
+         d->elem_bytes;
+  return KVM_OK;
+}
+
+int kvm_pool_register(int device, void* base, const kvm_pool_desc* desc) {
+  int64_t total = 0;
+  int rc = kvm_pool_bytes(desc, &total);
+  if (rc) return rc;
+  if (!base) return fail(KVM_ERR_INVALID, "pool base is NULL");
+  if (reinterpret_cast<uintptr_t>(base) % 16)
+    return fail(KVM_ERR_INVALID, "pool base must be 16-byte aligned");
+  const int64_t piece = (int64_t)desc->block_tokens * desc->kv_heads * desc->head_dim * desc->elem_bytes;
+  if (piece % 16) return fail(KVM_ERR_CONFIG, "piece bytes must be a multiple of 16");
+  if (piece > (int64_t)1 << 30) return fail(KVM_ERR_CONFIG, "piece too large");
+  int ndev = 0;
+  KVM_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(KVM_ERR_INVALID, "bad device " + std::to_string(device));
+  Pool p;
+  p.live = true;
+  p.device = device;
+  p.base = static_cast<uint8_t*>(base);
+  p.desc = *desc;
+  p.piece_bytes = piece;
+  p.plane_bytes = piece * desc->num_blocks;
+  p.token_bytes = (int64_t)desc->kv_heads * desc->head_dim * desc->elem_bytes;
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_pools.push_back(p);
+  return (int)g_pools.size() - 1;
+}
+
+int kvm_pool_unregister(int pool) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (pool < 0 || pool >= (int)g_pools.size() || !g_pools[pool].live)
+    return fail(KVM_ERR_NOT_FOUND, "unknown pool id " + std::to_string(pool));
+  g_pools[pool].live = false;
+  return KVM_OK;
+}
+
+int kvm_pool_piece_bytes(int pool, int64_t* out) {
+  if (!out) return fail(KVM_ERR_INVALID, "out is NULL");
+  const Pool* p = get_pool(pool);
+  if (!p) return KVM_ERR_NOT_FOUND;
+  *out = p->piece_bytes;
+  return KVM_OK;
+}
+
+int kvm_ipc_export(const void* ptr, void* handle64, int64_t* offset_out) {
+  if (!ptr || !handle64 || !offset_out) return fail(KVM_ERR_INVALID, "NULL argument");
+  // Find the allocation base with the driver API (no -lcuda link dependency).
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    KVM_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn) return fail(KVM_ERR_UNSUPPORTED, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult r = get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr));
+  if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuMemGetAddressRange failed: " + std::to_string((int)r));
+  cudaIpcMemHandle_t h;
+  KVM_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  memcpy(handle64, &h, 64);
+  *offset_out = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - (uintptr_t)base);
+  return KVM_OK;
+}
+
+int kvm_ipc_import(int device, const void* handle64, int64_t offset, void** ptr_out) {
+  if (!handle64 || !ptr_out) return fail(KVM_ERR_INVALID, "NULL argument");
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  void* base = nullptr;
+  KVM_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr_out = static_cast<uint8_t*>(base) + offset;
+  return KVM_OK;
+}
+
+int kvm_ipc_close(void* mapped_ptr, int64_t offset) {
+  if (!mapped_ptr) return fail(KVM_ERR_INVALID, "NULL argument");
+  KVM_CUDA_TRY(cudaIpcCloseMemHandle(static_cast<uint8_t*>(mapped_ptr) - offset));
+  return KVM_OK;
+}
+
+int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream) {
+  if (n_moves < 0) return fail(KVM_ERR_INVALID, "n_moves < 0");
+  if (n_moves == 0) return KVM_OK;
+  if (!moves) return fail(KVM_ERR_INVALID, "moves is NULL");
+  if (flags & ~(KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK))
+    return fail(KVM_ERR_INVALID, "unknown flags");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < n_moves; i += KVM_MAX_MOVES) {
+    int rc = migrate_batch(moves + i, std::min(KVM_MAX_MOVES, n_moves - i), flags, s);
+    if (rc) return rc;
+  }
+  return KVM_OK;
+}
+
+int kvm_compact(int pool, const int32_t* src_blocks, const int32_t* dst_blocks, int n_blocks,
+                int32_t* table_row, int flags, void* stream) {
+  const Pool* p = get_pool(pool);
+  if (!p) return KVM_ERR_NOT_FOUND;
+  if (flags & KVM_F_BLOCKS_ON_HOST) {
+    // In-place defragmentation is only well defined for disjoint block sets.
+    std::vector<char> seen(p->desc.num_blocks, 0);
+    for (int i = 0; i < n_blocks; ++i) {
+      int b = src_blocks[i];
+      if (b >= 0 && b < p->desc.num_blocks) seen[b] |= 1;
+    }
+    for (int i = 0; i < n_blocks; ++i) {
+      int b = dst_blocks[i];
+      if (b >= 0 && b < p->desc.num_blocks) {
+        if (seen[b] & 1) return fail(KVM_ERR_INVALID, "compaction dst block overlaps a src block");
+        if (seen[b] & 2) return fail(KVM_ERR_INVALID, "duplicate dst block " + std::to_string(b));
+        seen[b] |= 2;
+      }
+    }
+  }
+  kvm_move mv;
+  memset(&mv, 0, sizeof(mv));
+  mv.src_pool = pool;
+  mv.dst_pool = pool;
+  mv.n_blocks = n_blocks;
+  mv.src_blocks = src_blocks;
+  mv.dst_blocks = dst_blocks;
+  mv.dst_table_row = table_row;
+  return kvm_migrate(&mv, 1, flags, stream);
+}
+
+int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream) {
+  if (!flag) return fail(KVM_ERR_INVALID, "flag is NULL");
+  wait_flag_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flag, value);
+  KVM_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  return KVM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+// Shared internals of libkvmig.so (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/kvmig.h"
+
+namespace kvm {
+
+// Thread-local last-error text + code helpers (defined in kvmig.cu).
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define KVM_CUDA_TRY(expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return ::kvm::cuda_fail(_e, #expr); \
+  } while (0)
+
+struct Pool {
+  bool live = false;
+  int device = -1;
+  uint8_t* base = nullptr;
+  kvm_pool_desc desc{};
+  int64_t piece_bytes = 0;  // block_tokens * kv_heads * head_dim * elem_bytes
+  int64_t plane_bytes = 0;  // num_blocks * piece_bytes  (one (layer, K|V) plane)
+  int64_t token_bytes = 0;  // kv_heads * head_dim * elem_bytes (one token row)
+};
+
+// Look up a registered pool; returns nullptr (and sets the error) if unknown.
+const Pool* get_pool(int id);
+void count_launch(int64_t n = 1);
+int sm_count(int device);
+
+// ---- PTX helpers ---------------------------------------------------------
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+}  // namespace kvm

@@ -1,0 +1,285 @@
+"""The data plane the reference leaves out: execute a MigrationPlan on GPUs.
+
+Insertion point: /root/reference/pkg/src/kvpack/sim.py:218-227, where the
+reference takes `plan.executed` (migration.py:119-121) and simply deletes the
+records.  `MigrationExecutor.execute(plan)` is called at exactly that spot,
+once per slot, from the single scheduler thread (model.py:119);
+it is asynchronous on per-device CUDA streams and, by default, awaited before
+returning so the slot's metrics row (sim.py:229-238) stays truthful.
+
+Physical vs logical placement.  The scheduler moves items logically at once,
+but a deferred move's bytes stay where they were for epochs (sim.py:207-227),
+and a group item's members drift while its move is pending.  The executor
+therefore keeps its own physical location map per *request* and, for a move
+of item I from GPU s to GPU d, migrates exactly the members of I that are
+physically on s (SURVEY.md §7 hard part 5).  Source blocks are released only
+after the copy has completed.
+
+Modes (migration.py:19-22):
+  kv_transfer, forced_kv_transfer -> kvm_migrate (gather -> push -> table rewrite)
+  token_transfer                  -> kvm_reprefill on the destination
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Callable, Dict, Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, NotPlaced
+from .kvcache import BlockTable, KVPool
+from .planner import FORCED_KV_TRANSFER, KV_TRANSFER, TOKEN_TRANSFER, MigrationPlan, PlannedMove
+
+ENGINES = {"ldg": 0, "bulk": _native.KVM_F_ENGINE_BULK}
+
+
+@dataclass
+class Residency:
+    """Where a request's KV physically lives right now."""
+
+    gpu: int
+    blocks: np.ndarray  # int32, logical block i -> pool block id
+    tokens: int
+
+
+@dataclass
+class ExecRecord:
+    item: int
+    src: int
+    dst: int
+    mode: str
+    requests: List[int]
+    blocks: int
+    bytes_moved: int      # KV bytes physically copied (members found at src)
+    tokens_recomputed: int
+
+
+@dataclass
+class ExecReport:
+    records: List[ExecRecord] = field(default_factory=list)
+    launches: int = 0
+
+    @property
+    def bytes_moved(self) -> int:
+        return sum(r.bytes_moved for r in self.records)
+
+
+class MigrationExecutor:
+    """Executes planned moves over registered per-GPU pools.
+
+    pools:  logical GPU id -> KVPool (several logical GPUs may share one
+            physical device, e.g. replaying an 8-GPU trace on one B200).
+    tables: logical GPU id -> BlockTable (optional; when present the kernel
+            rewrites the destination row in place).
+    reprefill: callable(executor, request_id, dst_gpu, dst_blocks, tokens,
+            stream) that recomputes KV on the destination (token_transfer);
+            see reprefill.ReprefillEngine.  Without it, token_transfer raises.
+    """
+
+    def __init__(self, pools: Dict[int, KVPool], tables: Optional[Dict[int, BlockTable]] = None,
+                 engine: str = "ldg", reprefill: Optional[Callable] = None):
+        import torch
+
+        if engine not in ENGINES:
+            raise ConfigError(f"engine must be one of {sorted(ENGINES)}")
+        if not pools:
+            raise ConfigError("executor needs at least one pool")
+        shapes = {p.shape for p in pools.values()}
+        self.pools = dict(pools)
+        self.tables = dict(tables or {})
+        self.engine_flag = ENGINES[engine]
+        self.reprefill = reprefill
+        self.loc: Dict[int, Residency] = {}
+        self._streams: Dict[int, "torch.cuda.Stream"] = {}
+        self._multi_shape = len(shapes) > 1
+        _native.lib()  # fail loudly now if the native library is missing
+
+    # -- streams ---------------------------------------------------------------
+    def stream(self, device: int):
+        import torch
+
+        s = self._streams.get(device)
+        if s is None:
+            s = torch.cuda.Stream(device=device)
+            self._streams[device] = s
+        return s
+
+    def synchronize(self) -> None:
+        for s in self._streams.values():
+            s.synchronize()
+
+    # -- residency ---------------------------------------------------------------
+    def admit(self, rid: int, gpu: int, tokens: int) -> np.ndarray:
+        """Allocate blocks for a new request on `gpu` (prefill happens elsewhere)."""
+        if rid in self.loc:
+            raise ValueError(f"request {rid} already resident")
+        pool = self._pool(gpu)
+        blocks = pool.allocator.alloc(pool.shape.blocks_for(tokens))
+        self.loc[rid] = Residency(gpu, blocks, tokens)
+        self._table_set(gpu, rid, blocks)
+        return blocks
+
+    def grow(self, rid: int, tokens: int) -> None:
+        """Decode appended tokens: extend the block table when a block fills."""
+        r = self._res(rid)
+        pool = self._pool(r.gpu)
+        need = pool.shape.blocks_for(tokens) - len(r.blocks)
+        if need > 0:
+            r.blocks = np.concatenate([r.blocks, pool.allocator.alloc(need)])
+            self._table_set(r.gpu, rid, r.blocks)
+        r.tokens = tokens
+
+    def release(self, rid: int) -> None:
+        r = self.loc.pop(rid, None)
+        if r is None:
+            return
+        self._pool(r.gpu).allocator.free(r.blocks)
+        t = self.tables.get(r.gpu)
+        if t is not None:
+            t.drop(rid)
+
+    def where(self, rid: int) -> Residency:
+        return self._res(rid)
+
+    # -- execution ---------------------------------------------------------------
+    def execute(self, plan, members_of: Optional[Callable[[int], Sequence[int]]] = None,
+                wait: bool = True) -> ExecReport:
+        """Carry out `plan.executed` (or a list of PlannedMove) in plan order.
+
+        members_of(item) -> request ids of a group item (negative id); the
+        default treats every item as a single request.
+        """
+        executed: List[PlannedMove] = plan.executed if isinstance(plan, MigrationPlan) else [
+            p for p in plan if p.mode != "deferred"]
+        report = ExecReport()
+        by_dev: Dict[int, List[Tuple[_native.Move, int, int, np.ndarray, np.ndarray]]] = {}
+        keep = []  # host arrays must outlive the kvm_migrate call
+        post: List[Tuple[int, int, int, np.ndarray]] = []  # (rid, dst, tokens, dst_blocks)
+        for pm in executed:
+            mv = pm.move
+            rids = list(members_of(mv.item)) if (members_of and mv.item < 0) else [mv.item]
+            here = [r for r in rids if r in self.loc and self.loc[r].gpu == mv.src]
+            rec = ExecRecord(mv.item, mv.src, mv.dst, pm.mode, here, 0, 0, 0)
+            if mv.src == mv.dst:
+                report.records.append(rec)
+                continue
+            src_pool, dst_pool = self._pool(mv.src), self._pool(mv.dst)
+            for rid in here:
+                res = self.loc[rid]
+                nb = len(res.blocks)
+                dst_blocks = dst_pool.allocator.alloc(nb)
+                if pm.mode in (KV_TRANSFER, FORCED_KV_TRANSFER):
+                    m = _native.Move()
+                    m.src_pool, m.dst_pool, m.n_blocks = src_pool.pool_id, dst_pool.pool_id, nb
+                    m.done_value = 1
+                    sb = np.ascontiguousarray(res.blocks, dtype=np.int32)
+                    db = np.ascontiguousarray(dst_blocks, dtype=np.int32)
+                    keep += [sb, db]
+                    m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
+                    table = self.tables.get(mv.dst)
+                    if table is not None:
+                        table.set_host(rid, db)
+                        m.dst_table_row = table.row_ptr(rid)
+                    by_dev.setdefault(src_pool.device, []).append(m)
+                    rec.bytes_moved += nb * src_pool.shape.piece_bytes * 2 * src_pool.shape.layers
+                elif pm.mode == TOKEN_TRANSFER:
+                    if self.reprefill is None:
+                        raise ConfigError("token_transfer planned but executor has no re-prefill engine")
+                    self.reprefill(self, rid, mv.dst, dst_blocks, res.tokens,
+                                   self.stream(dst_pool.device))
+                    table = self.tables.get(mv.dst)
+                    if table is not None:
+                        table.set_host(rid, dst_blocks)
+                        table.rows[table.slot(rid), :len(dst_blocks)].copy_(
+                            _as_i32_tensor(dst_blocks, dst_pool.device), non_blocking=False)
+                    rec.tokens_recomputed += res.tokens
+                    report.launches += 1
+                else:
+                    raise ValueError(f"cannot execute mode {pm.mode!r}")
+                rec.blocks += nb
+                post.append((rid, mv.dst, res.tokens, dst_blocks))
+            report.records.append(rec)
+        for dev, moves in by_dev.items():
+            arr = (_native.Move * len(moves))(*moves)
+            s = self.stream(dev)
+            _native.check(_native.lib().kvm_migrate(arr, len(moves),
+                                                    _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag,
+                                                    ctypes.c_void_p(s.cuda_stream)), "kvm_migrate")
+            report.launches += 1
+        if wait:
+            self.synchronize()
+            self._commit(post)
+        else:
+            self._pending_commit = post
+        return report
+
+    def compact(self, rid: int, wait: bool = True) -> ExecRecord:
+        """1-GPU case: move a request into the lowest free blocks of its own
+        pool (defragmentation; kvm_compact = migrate with src pool == dst pool)."""
+        res = self._res(rid)
+        pool = self._pool(res.gpu)
+        nb = len(res.blocks)
+        dst = pool.allocator.alloc(nb)
+        sb = np.ascontiguousarray(res.blocks, dtype=np.int32)
+        table = self.tables.get(res.gpu)
+        row = 0
+        if table is not None:
+            table.set_host(rid, dst)
+            row = table.row_ptr(rid)
+        s = self.stream(pool.device)
+        _native.check(_native.lib().kvm_compact(
+            pool.pool_id, sb.ctypes.data, dst.ctypes.data, nb, ctypes.c_void_p(row),
+            _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag, ctypes.c_void_p(s.cuda_stream)),
+            "kvm_compact")
+        rec = ExecRecord(rid, res.gpu, res.gpu, "compact", [rid], nb,
+                         nb * pool.shape.piece_bytes * 2 * pool.shape.layers, 0)
+        post = [(rid, res.gpu, res.tokens, dst)]
+        if wait:
+            s.synchronize()
+            self._commit(post, keep_table=True)
+        else:
+            self._pending_commit = post
+        return rec
+
+    def commit(self) -> None:
+        """Finish a wait=False execute(): await streams, then free sources."""
+        self.synchronize()
+        self._commit(getattr(self, "_pending_commit", []))
+        self._pending_commit = []
+
+    # -- internals ---------------------------------------------------------------
+    def _commit(self, post, keep_table: bool = False) -> None:
+        for rid, dst, tokens, dst_blocks in post:
+            old = self.loc[rid]
+            self._pool(old.gpu).allocator.free(old.blocks)
+            t = self.tables.get(old.gpu)
+            if t is not None and not keep_table:
+                t.drop(rid)
+            self.loc[rid] = Residency(dst, np.asarray(dst_blocks, dtype=np.int32), tokens)
+
+    def _pool(self, gpu: int) -> KVPool:
+        try:
+            return self.pools[gpu]
+        except KeyError:
+            raise NotPlaced(f"no KV pool registered for GPU {gpu}") from None
+
+    def _res(self, rid: int) -> Residency:
+        try:
+            return self.loc[rid]
+        except KeyError:
+            raise NotPlaced(f"request {rid} is not resident") from None
+
+    def _table_set(self, gpu: int, rid: int, blocks: np.ndarray) -> None:
+        t = self.tables.get(gpu)
+        if t is None:
+            return
+        t.set_host(rid, blocks)
+        t.rows[t.slot(rid), :len(blocks)].copy_(_as_i32_tensor(blocks, t.device))
+
+
+def _as_i32_tensor(a: np.ndarray, device: int):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(f"cuda:{device}")

@@ -1,0 +1,245 @@
+"""GPU parity of the migration kernels (through the C ABI) against the oracle.
+
+Small seeded cases are compared with the C oracle byte-for-byte over the WHOLE
+destination pool (so any stray write outside the target blocks fails);
+full-size configs use size-independent properties (gathered src == gathered
+dst, everything else unchanged, via per-piece checksums on the device).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kvmig_oracle as orc
+from paper_2501_06709_b200 import ConfigError, NotPlaced, _native
+from paper_2501_06709_b200.kvcache import (LLAMA2_7B, LLAMA2_13B, LLAMA3_70B, BlockTable, KVPool,
+                                           ModelShape)
+
+pytestmark = pytest.mark.gpu
+ENGINES = {"ldg": 0, "bulk": _native.KVM_F_ENGINE_BULK}
+
+
+def _fill(pool, seed):
+    g = torch.Generator(device=f"cuda:{pool.device}").manual_seed(seed)
+    t = pool.tensor.view(torch.int16)
+    t.copy_(torch.randint(-2 ** 15, 2 ** 15, t.shape, generator=g, device=t.device, dtype=torch.int16))
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _move(src, dst, sb, db, row=0, flag=0, layer_flags=0, value=1):
+    m = _native.Move()
+    m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, len(sb), value
+    m.src_blocks, m.dst_blocks = sb.ctypes.data if isinstance(sb, np.ndarray) else sb, \
+        db.ctypes.data if isinstance(db, np.ndarray) else db
+    m.dst_table_row, m.done_flag, m.layer_flags = row, flag, layer_flags
+    return m
+
+
+def _run(moves, flags):
+    arr = (_native.Move * len(moves))(*moves)
+    _native.check(_native.lib().kvm_migrate(arr, len(moves), flags, _stream()))
+    torch.cuda.synchronize()
+
+
+def _desc(pool):
+    s = pool.shape
+    return orc.desc(s.layers, s.kv_heads, s.head_dim, s.block_tokens, pool.num_blocks, s.elem_bytes)
+
+
+SMALL = ModelShape("t", layers=3, kv_heads=4, head_dim=64, q_heads=4, d_model=256)   # 8 KiB pieces
+ODD = ModelShape("odd", layers=2, kv_heads=5, head_dim=40, q_heads=5, d_model=200)   # 6400 B pieces
+BIG = ModelShape("b", layers=2, kv_heads=40, head_dim=128, q_heads=40, d_model=5120)  # 160 KiB pieces
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+@pytest.mark.parametrize("shape", [SMALL, ODD, BIG], ids=lambda s: s.name)
+@pytest.mark.parametrize("host_blocks", [True, False])
+def test_migrate_bit_exact_vs_oracle(engine, shape, host_blocks):
+    nb = 48
+    src, dst = KVPool(shape, nb), KVPool(shape, nb)
+    _fill(src, 1)
+    _fill(dst, 2)
+    rng = np.random.default_rng(7)
+    sb = rng.permutation(nb)[:17].astype(np.int32)
+    dst.allocator.take(rng.permutation(nb)[:20])
+    db = dst.allocator.alloc(17)
+    exp = dst.tensor.view(torch.int16).cpu().numpy()
+    row_exp = orc.migrate(src.tensor.view(torch.int16).cpu().numpy(), _desc(src), exp, _desc(dst), sb, db)
+    table = BlockTable(2, 32)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if host_blocks:
+        m = _move(src, dst, sb, db, table.row_ptr(5), flag.data_ptr(), value=9)
+        _run([m], _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine])
+    else:
+        sbd = torch.from_numpy(sb).cuda()
+        dbd = torch.from_numpy(db).cuda()
+        m = _move(src, dst, sbd.data_ptr(), dbd.data_ptr(), table.row_ptr(5), flag.data_ptr(), value=9)
+        m.n_blocks = 17
+        _run([m], ENGINES[engine])
+    assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
+    assert np.array_equal(table.rows[table.slot(5), :17].cpu().numpy(), row_exp)
+    assert (table.rows[table.slot(5), 17:] == -1).all()
+    assert flag.item() == 9
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+def test_batch_of_many_moves_and_layer_flags(engine):
+    """130 moves (> KVM_MAX_MOVES, so the batch is split) with ragged sizes,
+    including empty moves, every one with layer flags and a done flag."""
+    nb = 400
+    src, dst = KVPool(SMALL, nb), KVPool(SMALL, nb)
+    _fill(src, 3)
+    _fill(dst, 4)
+    rng = np.random.default_rng(11)
+    perm = rng.permutation(nb).astype(np.int32)
+    sizes = [int(rng.integers(0, 6)) for _ in range(130)]
+    sizes[0] = 0
+    moves, keep, exp_rows = [], [], []
+    flags = torch.zeros(130, dtype=torch.int32, device="cuda")
+    lflags = torch.zeros(130, SMALL.layers, dtype=torch.int32, device="cuda")
+    table = BlockTable(130, 8)
+    exp = dst.tensor.view(torch.int16).cpu().numpy()
+    src_np = src.tensor.view(torch.int16).cpu().numpy()
+    off = 0
+    for i, n in enumerate(sizes):
+        sb = perm[off:off + n].copy()
+        off += n
+        db = dst.allocator.alloc(n)
+        keep += [sb, db]
+        exp_rows.append(orc.migrate(src_np, _desc(src), exp, _desc(dst), sb, db))
+        moves.append(_move(src, dst, sb, db, table.row_ptr(i), flags[i:].data_ptr(),
+                           lflags[i].data_ptr(), value=100 + i))
+    _run(moves, _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine])
+    assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
+    assert flags.cpu().tolist() == [100 + i for i in range(130)]
+    assert (lflags.cpu() == torch.arange(100, 230, dtype=torch.int32)[:, None]).all()
+    for i, n in enumerate(sizes):
+        assert np.array_equal(table.rows[table.slot(i), :n].cpu().numpy(), exp_rows[i])
+
+
+def test_compaction_and_overlap_rejected():
+    nb = 64
+    pool = KVPool(SMALL, nb)
+    _fill(pool, 5)
+    before = pool.tensor.view(torch.int16).cpu().numpy()
+    sb = np.array([60, 3, 41, 17], dtype=np.int32)
+    pool.allocator.take(sb)
+    db = pool.allocator.alloc(4)
+    exp = before.copy()
+    orc.migrate(before, _desc(pool), exp, _desc(pool), sb, db)
+    table = BlockTable(1, 8)
+    _native.check(_native.lib().kvm_compact(pool.pool_id, sb.ctypes.data, db.ctypes.data, 4,
+                                            ctypes.c_void_p(table.row_ptr(0)),
+                                            _native.KVM_F_BLOCKS_ON_HOST, _stream()))
+    torch.cuda.synchronize()
+    assert np.array_equal(pool.tensor.view(torch.int16).cpu().numpy(), exp)
+    bad = np.array([3, 5, 6, 7], dtype=np.int32)
+    with pytest.raises(ValueError):
+        _native.check(_native.lib().kvm_compact(pool.pool_id, sb.ctypes.data, bad.ctypes.data, 4,
+                                                None, _native.KVM_F_BLOCKS_ON_HOST, _stream()))
+
+
+def test_errors_map_to_reference_exceptions():
+    pool = KVPool(SMALL, 8)
+    other = KVPool(ODD, 8)
+    sb = np.array([0], dtype=np.int32)
+    db = np.array([9], dtype=np.int32)
+    with pytest.raises(ValueError):  # dst block out of range
+        _run([_move(pool, pool, sb, db)], _native.KVM_F_BLOCKS_ON_HOST)
+    with pytest.raises(ConfigError):  # shape mismatch
+        _run([_move(pool, other, sb, sb)], _native.KVM_F_BLOCKS_ON_HOST)
+    m = _move(pool, pool, sb, sb)
+    m.dst_pool = 10 ** 6
+    with pytest.raises(NotPlaced):
+        _run([m], _native.KVM_F_BLOCKS_ON_HOST)
+
+
+@pytest.mark.parametrize("shape,tokens", [(LLAMA2_7B, 4096), (LLAMA2_13B, 8192), (LLAMA3_70B, 16384)],
+                         ids=["7b-4k", "13b-8k", "70b-16k"])
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+def test_full_size_property(shape, tokens, engine):
+    """BASELINE configs 2-4 at full size: moved pieces identical, nothing else
+    touched (checksums of all pieces before/after), table row exact."""
+    n = tokens // 16
+    nb = 2 * n + 64
+    pool_src, pool_dst = KVPool(shape, nb), KVPool(shape, nb)
+    _fill(pool_src, 1)
+    _fill(pool_dst, 2)
+    g = torch.Generator().manual_seed(1)
+    sb = torch.randperm(nb, generator=g)[:n].to(torch.int32).numpy()
+    occ = torch.randperm(nb, generator=torch.Generator().manual_seed(2))[: nb // 2].numpy()
+    pool_dst.allocator.take(occ)
+    db = pool_dst.allocator.alloc(n)
+
+    def piece_sums(pool):  # [L, 2, nb] int64 position-weighted checksum per piece
+        t = pool.tensor.view(torch.int16).view(shape.layers, 2, nb, -1)
+        w = torch.arange(1, t.shape[-1] + 1, device=t.device, dtype=torch.int64)
+        return torch.stack([(t[l].to(torch.int64) * w).sum(-1) for l in range(shape.layers)])
+
+    src_sums = piece_sums(pool_src)
+    before = piece_sums(pool_dst)
+    table = BlockTable(1, n)
+    _run([_move(pool_src, pool_dst, sb, db, table.row_ptr(0))],
+         _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine])
+    after = piece_sums(pool_dst)
+    sbt, dbt = torch.from_numpy(sb).long().cuda(), torch.from_numpy(db).long().cuda()
+    assert torch.equal(after[:, :, dbt], src_sums[:, :, sbt])
+    mask = torch.ones(nb, dtype=torch.bool, device="cuda")
+    mask[dbt] = False
+    assert torch.equal(after[:, :, mask], before[:, :, mask])
+    # exact bytes on a sample of pieces (first/last layer, K and V)
+    for l in (0, shape.layers - 1):
+        for kv in (0, 1):
+            assert torch.equal(pool_dst.tensor[l, kv, dbt[:8]].view(torch.int16),
+                               pool_src.tensor[l, kv, sbt[:8]].view(torch.int16))
+    assert np.array_equal(table.rows[0].cpu().numpy(), db)
+
+
+def test_wait_flag_kernel():
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pool = KVPool(SMALL, 8)
+    sb = np.array([1, 2], dtype=np.int32)
+    db = np.array([5, 6], dtype=np.int32)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        _native.check(_native.lib().kvm_wait_flag(ctypes.c_void_p(flag.data_ptr()), 3,
+                                                  ctypes.c_void_p(side.cuda_stream)))
+    m = _move(pool, pool, sb, db, flag=flag.data_ptr(), value=3)
+    _run([m], _native.KVM_F_BLOCKS_ON_HOST)
+    side.synchronize()
+    assert flag.item() == 3
+
+
+def test_executor_plan_roundtrip():
+    """Planner -> executor on two logical GPUs of one device; bytes follow."""
+    from paper_2501_06709_b200 import PendingMove, Topology, load_boundaries, plan_hybrid
+    from paper_2501_06709_b200.executor import MigrationExecutor
+
+    pools = {0: KVPool(SMALL, 64), 1: KVPool(SMALL, 64)}
+    tables = {0: BlockTable(8, 16), 1: BlockTable(8, 16)}
+    ex = MigrationExecutor(pools, tables)
+    _fill(pools[0], 8)
+    ex.admit(10, 0, 50)
+    ex.admit(11, 0, 17)
+    b10, b11 = ex.where(10).blocks.copy(), ex.where(11).blocks.copy()
+    src_np = pools[0].tensor.view(torch.int16).cpu().numpy()
+    topo = Topology(gpus_per_machine=8, intra_bandwidth_bytes_per_s=900e9)
+    bounds = load_boundaries(topo, 1.0, 1.0)
+    bpt = SMALL.kv_bytes_per_token
+    plan = plan_hybrid([PendingMove(10, 0, 1, 50 * bpt, 50), PendingMove(11, 0, 1, 17 * bpt, 17)],
+                       bounds, topo)
+    rep = ex.execute(plan)
+    assert rep.bytes_moved == (4 + 2) * 16 * bpt
+    dst_np = pools[1].tensor.view(torch.int16).cpu().numpy()
+    for rid, sb in ((10, b10), (11, b11)):
+        r = ex.where(rid)
+        assert r.gpu == 1
+        assert np.array_equal(dst_np[:, :, r.blocks], src_np[:, :, sb])
+        assert np.array_equal(tables[1].rows[tables[1].slot(rid), :len(sb)].cpu().numpy(), r.blocks)
+    assert pools[0].allocator.n_free == 64
+    rec = ex.compact(10)
+    assert rec.bytes_moved == 4 * 16 * bpt

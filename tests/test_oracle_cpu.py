@@ -1,0 +1,162 @@
+"""CPU-only: the byte-path oracle's known answers, the host objects, and the
+C ABI surface of libkvmig.so (load + exported symbols; no compute calls)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import kvmig_oracle as orc
+from paper_2501_06709_b200 import kvcache
+from paper_2501_06709_b200.kvcache import (LLAMA2_7B, LLAMA2_13B, LLAMA3_70B, BlockAllocator,
+                                           blocks_for_bytes)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _pool(rng, L, H, D, nb):
+    return rng.integers(-2 ** 15, 2 ** 15, size=(L, 2, nb, 16, H, D), dtype=np.int16)
+
+
+def test_shapes_match_survey():
+    assert LLAMA2_7B.kv_bytes_per_token == 524_288
+    assert LLAMA2_13B.kv_bytes_per_token == 819_200
+    assert LLAMA3_70B.kv_bytes_per_token == 327_680
+    assert LLAMA2_7B.piece_bytes == 128 * 1024
+    assert LLAMA2_13B.piece_bytes == 160 * 1024
+    assert LLAMA3_70B.piece_bytes == 32 * 1024
+    assert 4096 * LLAMA2_7B.kv_bytes_per_token == 2 ** 31
+    assert blocks_for_bytes(4096 * LLAMA2_7B.kv_bytes_per_token, LLAMA2_7B) == 256
+    with pytest.raises(ValueError):
+        blocks_for_bytes(LLAMA2_7B.kv_bytes_per_token + 1, LLAMA2_7B)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_oracle_migrate_identity(threads):
+    rng = np.random.default_rng(0)
+    L, H, D, nb = 3, 4, 32, 40
+    src, dst = _pool(rng, L, H, D, nb), _pool(rng, L, H, D, nb)
+    before = dst.copy()
+    sb = rng.permutation(nb)[:13].astype(np.int32)
+    free = np.ones(nb, dtype=np.uint8)
+    free[rng.permutation(nb)[:20]] = 0
+    db = orc.alloc_ascending(free, 13)
+    assert list(db) == sorted(db)
+    sd = dd = orc.desc(L, H, D, 16, nb)
+    row = orc.migrate(src, sd, dst, dd, sb, db, threads=threads)
+    assert list(row) == list(db)
+    for i in range(13):
+        assert np.array_equal(dst[:, :, db[i]], src[:, :, sb[i]])
+    untouched = np.setdiff1d(np.arange(nb), db)
+    assert np.array_equal(dst[:, :, untouched], before[:, :, untouched])
+
+
+def test_oracle_nan_payloads_bit_exact():
+    L, H, D, nb = 1, 1, 8, 4
+    src = np.full((L, 2, nb, 16, H, D), 0x7E01, dtype=np.uint16)  # fp16 NaN with payload
+    src[..., 1] = 0xFC00  # -inf
+    dst = np.zeros_like(src)
+    d = orc.desc(L, H, D, 16, nb)
+    orc.migrate(src, d, dst, d, [3, 0], [1, 2])
+    assert np.array_equal(dst[:, :, 1], src[:, :, 3]) and np.array_equal(dst[:, :, 2], src[:, :, 0])
+
+
+def test_oracle_rejects_out_of_range():
+    d = orc.desc(1, 1, 8, 16, 4)
+    a = np.zeros((1, 2, 4, 16, 1, 8), dtype=np.int16)
+    with pytest.raises(ValueError):
+        orc.migrate(a, d, a.copy(), d, [4], [0])
+
+
+def test_allocator_matches_oracle():
+    rng = np.random.default_rng(3)
+    nb = 300
+    a = BlockAllocator(nb)
+    taken = rng.permutation(nb)[:150]
+    a.take(taken)
+    mask = np.ones(nb, dtype=np.uint8)
+    mask[taken] = 0
+    for n in (7, 1, 40, 0, 33):
+        got = a.alloc(n)
+        exp = orc.alloc_ascending(mask, n)
+        assert np.array_equal(got, exp)
+    a.free(got)
+    with pytest.raises(ValueError):
+        a.free(got)
+    with pytest.raises(kvcache.RequestTooLarge):
+        a.alloc(10 ** 6)
+
+
+def test_oracle_reprefill_matches_numpy():
+    rng = np.random.default_rng(5)
+    L, H, D, nb, dm, qc, rows, tok0 = 2, 2, 16, 6, 64, 32, 21, 5
+    kvd = H * D
+    n_out = qc + 2 * kvd
+
+    def bf16_bits(a):
+        u = a.astype(np.float32).view(np.uint32)
+        return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+    def bits_to_f32(b):
+        return (b.astype(np.uint32) << 16).view(np.float32)
+
+    x = bf16_bits(rng.standard_normal((rows, dm)))
+    w = bf16_bits(rng.standard_normal((L, n_out, dm)) / 8)
+    pool = np.zeros((L, 2, nb, 16, H, D), dtype=np.uint16)
+    blocks = np.array([4, 0, 2], dtype=np.int32)  # tokens 0..47
+    q = np.zeros((L, rows, qc), dtype=np.uint16)
+    orc.reprefill(orc.desc(L, H, D, 16, nb), pool, blocks, x, w, rows, dm, qc, tok0, q)
+    ref = np.einsum("tk,lnk->ltn", bits_to_f32(x).astype(np.float64), bits_to_f32(w).astype(np.float64))
+    for l in range(L):
+        np.testing.assert_allclose(bits_to_f32(q[l]), ref[l, :, :qc], rtol=1e-2, atol=1e-2)
+        for t in range(rows):
+            tok = tok0 + t
+            blk, slot = blocks[tok // 16], tok % 16
+            k = bits_to_f32(pool[l, 0, blk, slot].reshape(-1))
+            v = bits_to_f32(pool[l, 1, blk, slot].reshape(-1))
+            np.testing.assert_allclose(k, ref[l, t, qc:qc + kvd], rtol=1e-2, atol=1e-2)
+            np.testing.assert_allclose(v, ref[l, t, qc + kvd:], rtol=1e-2, atol=1e-2)
+
+
+# --- C ABI surface ----------------------------------------------------------------
+
+def _header_symbols():
+    with open(os.path.join(ROOT, "include", "kvmig.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(kvm_\w+)\(", text, re.M)))
+
+
+def test_abi_library_exports_every_header_symbol():
+    from paper_2501_06709_b200 import _native
+
+    L = _native.lib()
+    syms = _header_symbols()
+    assert len(syms) >= 15
+    assert set(syms) == set(_native.EXPORTS)
+    for s in syms:
+        assert hasattr(L, s), s
+    assert L.kvm_version() == 1
+
+
+def test_abi_error_mapping_without_gpu():
+    from paper_2501_06709_b200 import ConfigError, _native
+
+    d = _native.PoolDesc(0, 1, 1, 16, 1, 2)
+    out = ctypes.c_int64()
+    with pytest.raises(ConfigError):
+        _native.check(_native.lib().kvm_pool_bytes(ctypes.byref(d), ctypes.byref(out)))
+    d = _native.PoolDesc(32, 32, 128, 16, 256, 2)
+    _native.check(_native.lib().kvm_pool_bytes(ctypes.byref(d), ctypes.byref(out)))
+    assert out.value == 256 * 16 * LLAMA2_7B.kv_bytes_per_token
+    with pytest.raises(ValueError):
+        _native.check(_native.lib().kvm_migrate(None, -1, 0, None))
+    assert _native.lib().kvm_migrate(None, 0, 0, None) == 0
+
+
+def test_abi_struct_layout():
+    from paper_2501_06709_b200 import _native
+
+    assert ctypes.sizeof(_native.PoolDesc) == 24
+    assert ctypes.sizeof(_native.Move) == 56
+    assert _native.Move.src_blocks.offset == 16
