@@ -331,9 +331,9 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
 
   int cur_ld = 0;
   int key_move = -1, key_layer = -1, key_n = 0;
-  // Stored-tile metadata ring (lane 0 only): dst pointer, len, move, layer.
-  uint8_t* st_dst[kBulkStages];
-  int st_len[kBulkStages], st_move[kBulkStages], st_layer[kBulkStages];
+  // Stored-tile metadata ring (written/read by lane 0 only): dst, len, move, layer.
+  __shared__ uint8_t* st_dst[kBulkStages];
+  __shared__ int st_len[kBulkStages], st_move[kBulkStages], st_layer[kBulkStages];
 
   for (int64_t i = 0; i < my_tiles + kBulkLag; ++i) {
     // ---- store side: tile j = i - lag ----

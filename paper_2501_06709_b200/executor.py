@@ -79,7 +79,7 @@ class MigrationExecutor:
     """
 
     def __init__(self, pools: Dict[int, KVPool], tables: Optional[Dict[int, BlockTable]] = None,
-                 engine: str = "ldg", reprefill: Optional[Callable] = None):
+                 engine: str = "bulk", reprefill: Optional[Callable] = None):
         import torch
 
         if engine not in ENGINES:

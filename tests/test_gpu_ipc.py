@@ -1,0 +1,121 @@
+"""One process per GPU, exercised on ONE B200: two ranks (gloo for the control
+plane) each own a pool; rank 0 maps rank 1's pool, block table and flag
+words through CUDA IPC and pushes a request into it with the migration
+kernel.  This is the exact multi-GPU code path (peer-mapped stores, fused
+table rewrite, system-scope flags, kvm_wait_flag on the receiver) minus the
+NVLink hop, which needs a second GPU."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, engine_flag, result_q):
+    import ctypes
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import kvmig_oracle as orc
+    from paper_2501_06709_b200 import _native
+    from paper_2501_06709_b200.dist import exchange_objects
+    from paper_2501_06709_b200.kvcache import BlockTable, KVPool, ModelShape
+
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        torch.cuda.set_device(0)
+        shape = ModelShape("ipc", layers=3, kv_heads=8, head_dim=64, q_heads=8, d_model=512)
+        nb = 40
+        pool = KVPool(shape, nb, device=0)
+        g = torch.Generator(device="cuda:0").manual_seed(100 + rank)
+        pool.tensor.view(torch.int16).copy_(torch.randint(-2 ** 15, 2 ** 15, pool.view_shape, generator=g,
+                                                          device="cuda:0", dtype=torch.int16))
+        table = BlockTable(2, 16, device=0)
+        words = torch.zeros(8, dtype=torch.int32, device="cuda:0")  # [0]=done, [1..3]=layer flags
+        lib = _native.lib()
+
+        def export(ptr):
+            h = (ctypes.c_ubyte * 64)()
+            off = ctypes.c_int64()
+            _native.check(lib.kvm_ipc_export(ctypes.c_void_p(ptr), h, ctypes.byref(off)))
+            return bytes(h), off.value
+
+        rng = np.random.default_rng(5)
+        sb = rng.permutation(nb)[:9].astype(np.int32)
+        pool.allocator.take(rng.permutation(nb)[:15])
+        db = pool.allocator.alloc(9)
+        before = pool.tensor.view(torch.int16).cpu().numpy()
+        info = exchange_objects((pool.ipc_handle(), export(table.rows.data_ptr()), export(words.data_ptr()),
+                                 db.tolist(), before if rank == 0 else None))
+        torch.cuda.synchronize()
+        if rank == 0:
+            (ph, po), (th, to), (wh, wo), peer_db, _ = info[1]
+            peer = KVPool.from_ipc(shape, nb, 0, ph, po)
+            tptr, wptr = ctypes.c_void_p(), ctypes.c_void_p()
+            _native.check(lib.kvm_ipc_import(0, (ctypes.c_ubyte * 64).from_buffer_copy(th), to, ctypes.byref(tptr)))
+            _native.check(lib.kvm_ipc_import(0, (ctypes.c_ubyte * 64).from_buffer_copy(wh), wo, ctypes.byref(wptr)))
+            pdb = np.asarray(peer_db, dtype=np.int32)
+            m = _native.Move()
+            m.src_pool, m.dst_pool, m.n_blocks, m.done_value = pool.pool_id, peer.pool_id, 9, 5
+            m.src_blocks, m.dst_blocks = sb.ctypes.data, pdb.ctypes.data
+            m.dst_table_row = tptr.value  # rank 1's table row 0
+            m.done_flag = wptr.value
+            m.layer_flags = wptr.value + 4
+            s = torch.cuda.Stream()
+            _native.check(lib.kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | engine_flag,
+                                          ctypes.c_void_p(s.cuda_stream)))
+            s.synchronize()
+            dist.barrier()
+            ok = True
+        else:
+            s = torch.cuda.Stream()
+            _native.check(lib.kvm_wait_flag(ctypes.c_void_p(words.data_ptr()), 5, ctypes.c_void_p(s.cuda_stream)))
+            s.synchronize()   # returns only once rank 0's kernel published the flag
+            dist.barrier()
+            src0 = info[0][4]
+            exp = before.copy()
+            d = orc.desc(3, 8, 64, 16, nb)
+            sb0 = np.random.default_rng(5).permutation(nb)[:9].astype(np.int32)
+            row = orc.migrate(src0, d, exp, d, sb0, db)
+            got = pool.tensor.view(torch.int16).cpu().numpy()
+            ok = bool(np.array_equal(got, exp)) and bool(np.array_equal(table.rows[0, :9].cpu().numpy(), row)) \
+                and words[:4].cpu().tolist() == [5, 5, 5, 5]
+        result_q.put((rank, ok, ""))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        result_q.put((rank, False, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+def test_two_process_ipc_push(engine):
+    import torch.multiprocessing as mp
+
+    from paper_2501_06709_b200 import _native
+
+    flag = {"ldg": 0, "bulk": _native.KVM_F_ENGINE_BULK}[engine]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, flag, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, err in res:
+        assert ok, f"rank {rank} failed:\n{err}"

@@ -30,9 +30,10 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _move(src, dst, sb, db, row=0, flag=0, layer_flags=0, value=1):
+def _move(src, dst, sb, db, row=0, flag=0, layer_flags=0, value=1, n=None):
     m = _native.Move()
-    m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, len(sb), value
+    n = len(sb) if n is None else n
+    m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, n, value
     m.src_blocks, m.dst_blocks = sb.ctypes.data if isinstance(sb, np.ndarray) else sb, \
         db.ctypes.data if isinstance(db, np.ndarray) else db
     m.dst_table_row, m.done_flag, m.layer_flags = row, flag, layer_flags
@@ -77,8 +78,8 @@ def test_migrate_bit_exact_vs_oracle(engine, shape, host_blocks):
     else:
         sbd = torch.from_numpy(sb).cuda()
         dbd = torch.from_numpy(db).cuda()
-        m = _move(src, dst, sbd.data_ptr(), dbd.data_ptr(), table.row_ptr(5), flag.data_ptr(), value=9)
-        m.n_blocks = 17
+        m = _move(src, dst, sbd.data_ptr(), dbd.data_ptr(), table.row_ptr(5), flag.data_ptr(), value=9,
+                  n=17)
         _run([m], ENGINES[engine])
     assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
     assert np.array_equal(table.rows[table.slot(5), :17].cpu().numpy(), row_exp)
