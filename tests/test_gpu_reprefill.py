@@ -1,0 +1,114 @@
+"""tcgen05 re-prefill vs an fp32 reference (torch fp32 on the GPU for speed,
+and the C oracle on the smallest case).
+
+Tolerance (stated, bf16 output of an fp32-accumulated bf16 GEMM):
+    |got - ref| <= 1e-2 + 1.6e-2 * |ref|     (ref = fp32 product of the bf16 operands)
+Only the pool slots of the recomputed tokens may change.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import kvmig_oracle as orc
+from paper_2501_06709_b200.kvcache import LLAMA2_13B, KVPool, ModelShape
+from paper_2501_06709_b200.reprefill import reprefill, synthetic_hidden, synthetic_weights
+
+pytestmark = pytest.mark.gpu
+ATOL, RTOL = 1e-2, 1.6e-2
+
+
+def _ref(x, w):  # [L, rows, n_out] fp32
+    return torch.einsum("tk,lnk->ltn", x.float(), w.float())
+
+
+def _check(shape, pool, blocks, tok0, rows, ref, q_out, before):
+    kvd = shape.kv_cols
+    qc = ref.shape[2] - 2 * kvd
+    t = pool.tensor
+    for l in range(shape.layers):
+        toks = torch.arange(tok0, tok0 + rows, device="cuda")
+        blk = blocks.long()[toks // 16]
+        slot = toks % 16
+        k = t[l, 0, blk, slot].reshape(rows, kvd).float()
+        v = t[l, 1, blk, slot].reshape(rows, kvd).float()
+        torch.testing.assert_close(k, ref[l, :, qc:qc + kvd], atol=ATOL, rtol=RTOL)
+        torch.testing.assert_close(v, ref[l, :, qc + kvd:], atol=ATOL, rtol=RTOL)
+        if q_out is not None:
+            torch.testing.assert_close(q_out[l].float(), ref[l, :, :qc], atol=ATOL, rtol=RTOL)
+    # nothing outside the recomputed token slots changed
+    after = t.view(torch.int16).clone()
+    mask = torch.ones(t.shape[2], 16, dtype=torch.bool, device="cuda")
+    toks = torch.arange(tok0, tok0 + rows, device="cuda")
+    mask[blocks.long()[toks // 16], toks % 16] = False
+    assert torch.equal(after[:, :, mask], before[:, :, mask])
+
+
+@pytest.mark.parametrize("rows,tok0,with_q", [(1, 0, True), (77, 5, True), (128, 0, False),
+                                              (300, 21, True), (513, 16, False)])
+def test_reprefill_small_shapes(rows, tok0, with_q):
+    shape = ModelShape("rp", layers=3, kv_heads=4, head_dim=64, q_heads=8, d_model=256)
+    nblk = (tok0 + rows + 15) // 16
+    nb = nblk + 10
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    before = pool.tensor.view(torch.int16).clone()
+    blocks = torch.randperm(nb, generator=torch.Generator().manual_seed(rows))[:nblk].to(torch.int32).cuda()
+    x = synthetic_hidden(shape, rows, 0, seed=rows)
+    w = synthetic_weights(shape, 0, with_q=with_q, seed=rows + 1)
+    q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda") if with_q else None
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q)
+    torch.cuda.synchronize()
+    _check(shape, pool, blocks, tok0, rows, _ref(x, w), q, before)
+
+
+def test_reprefill_matches_c_oracle():
+    shape = ModelShape("rp", layers=2, kv_heads=2, head_dim=64, q_heads=2, d_model=128)
+    rows, tok0, nb = 40, 3, 6
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.zero_()
+    blocks = torch.tensor([4, 1, 5], dtype=torch.int32, device="cuda")
+    x = synthetic_hidden(shape, rows, 0, seed=9)
+    w = synthetic_weights(shape, 0, with_q=True, seed=10)
+    q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda")
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q)
+    torch.cuda.synchronize()
+    exp = np.zeros(pool.view_shape, dtype=np.uint16)
+    q_exp = np.zeros((shape.layers, rows, shape.q_cols), dtype=np.uint16)
+    orc.reprefill(orc.desc(2, 2, 64, 16, nb), exp, blocks.cpu().numpy(), x.view(torch.int16).cpu().numpy().view(np.uint16),
+                  w.view(torch.int16).cpu().numpy().view(np.uint16), rows, shape.d_model, shape.q_cols, tok0, q_exp)
+    to_f = lambda b: torch.from_numpy(b.astype(np.int32) << 16).view(torch.float32)  # noqa: E731
+    got = pool.tensor.float().cpu()
+    exp_f = to_f(exp.reshape(-1)).view(pool.view_shape)
+    torch.testing.assert_close(got, exp_f, atol=ATOL, rtol=RTOL)
+    torch.testing.assert_close(q.float().cpu(), to_f(q_exp.reshape(-1)).view(q_exp.shape), atol=ATOL, rtol=RTOL)
+
+
+def test_reprefill_13b_balanced_split():
+    """BASELINE configs[2]: 13B, suffix of s ~ 1.4k tokens of an 8k request."""
+    shape = LLAMA2_13B
+    rows, tok0 = 1360, 8192 - 1360
+    nblk = 8192 // 16
+    nb = nblk + 8
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    blocks = torch.randperm(nb, generator=torch.Generator().manual_seed(0))[:nblk].to(torch.int32).cuda()
+    x = synthetic_hidden(shape, rows, 0, seed=2)
+    w = synthetic_weights(shape, 0, with_q=True, seed=3)
+    before = pool.tensor.view(torch.int16).clone()
+    reprefill(pool, x, w, blocks, tok0=tok0)
+    torch.cuda.synchronize()
+    # check a sample of layers against fp32 (full einsum over 40 layers is 8.6 TFLOP)
+    kvd, qc = shape.kv_cols, shape.q_cols
+    for l in (0, 17, 39):
+        ref = x.float() @ w[l].float().t()
+        toks = torch.arange(tok0, tok0 + rows, device="cuda")
+        blk, slot = blocks.long()[toks // 16], toks % 16
+        torch.testing.assert_close(pool.tensor[l, 0, blk, slot].reshape(rows, kvd).float(), ref[:, qc:qc + kvd],
+                                   atol=ATOL, rtol=RTOL)
+        torch.testing.assert_close(pool.tensor[l, 1, blk, slot].reshape(rows, kvd).float(), ref[:, qc + kvd:],
+                                   atol=ATOL, rtol=RTOL)
+    after = pool.tensor.view(torch.int16)
+    toks = torch.arange(tok0, tok0 + rows, device="cuda")
+    mask = torch.ones(nb, 16, dtype=torch.bool, device="cuda")
+    mask[blocks.long()[toks // 16], toks % 16] = False
+    assert torch.equal(after[:, :, mask], before[:, :, mask])
