@@ -52,8 +52,9 @@ class ExecRecord:
     mode: str
     requests: List[int]
     blocks: int
-    bytes_moved: int      # KV bytes physically copied (members found at src)
+    bytes_moved: int      # KV bytes physically copied (members found at src), whole blocks
     tokens_recomputed: int
+    tokens_moved: int = 0  # tokens of the members copied: algorithmic bytes = tokens_moved * bpt
 
 
 @dataclass
@@ -64,6 +65,10 @@ class ExecReport:
     @property
     def bytes_moved(self) -> int:
         return sum(r.bytes_moved for r in self.records)
+
+    @property
+    def tokens_moved(self) -> int:
+        return sum(r.tokens_moved for r in self.records)
 
 
 class MigrationExecutor:
@@ -184,6 +189,7 @@ class MigrationExecutor:
                         m.dst_table_row = table.row_ptr(rid)
                     by_dev.setdefault(src_pool.device, []).append(m)
                     rec.bytes_moved += nb * src_pool.shape.piece_bytes * 2 * src_pool.shape.layers
+                    rec.tokens_moved += res.tokens
                 elif pm.mode == TOKEN_TRANSFER:
                     if self.reprefill is None:
                         raise ConfigError("token_transfer planned but executor has no re-prefill engine")
@@ -202,11 +208,7 @@ class MigrationExecutor:
                 post.append((rid, mv.dst, res.tokens, dst_blocks))
             report.records.append(rec)
         for dev, moves in by_dev.items():
-            arr = (_native.Move * len(moves))(*moves)
-            s = self.stream(dev)
-            _native.check(_native.lib().kvm_migrate(arr, len(moves),
-                                                    _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag,
-                                                    ctypes.c_void_p(s.cuda_stream)), "kvm_migrate")
+            self._launch_migrate(dev, moves)
             report.launches += 1
         if wait:
             self.synchronize()
@@ -250,6 +252,14 @@ class MigrationExecutor:
         self._pending_commit = []
 
     # -- internals ---------------------------------------------------------------
+    def _launch_migrate(self, dev: int, moves: List[_native.Move]) -> None:
+        """One fused kvm_migrate launch for every move leaving `dev` this slot."""
+        arr = (_native.Move * len(moves))(*moves)
+        s = self.stream(dev)
+        _native.check(_native.lib().kvm_migrate(arr, len(moves),
+                                                _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag,
+                                                ctypes.c_void_p(s.cuda_stream)), "kvm_migrate")
+
     def _commit(self, post, keep_table: bool = False) -> None:
         for rid, dst, tokens, dst_blocks in post:
             old = self.loc[rid]

@@ -1,0 +1,216 @@
+"""Trace-replay executor: the reference's slot loop with the bytes moved.
+
+Input is a recorded run of the reference simulator (tests/golden/trace_*.json,
+written by tests/golden/make_golden.py from `kvpack.sim.run`): per slot, the
+arrivals and the GPU the scheduler placed each on, completions / rejections /
+aborts, and every plan row (item, src, dst, kv_bytes, tokens, mode) with the
+group members at plan time.  The replay reproduces sim.py:151-227 physically:
+
+  1. completions / rejected / aborted requests release their blocks;
+  2. decode growth: every resident request's KV grows to
+     prompt + min(response, tokens_per_slot * (slot - arrival)) tokens
+     (model.py:58-69), allocating blocks on the GPU that *physically* holds it;
+  3. arrivals are admitted on the GPU the scheduler placed them on;
+  4. the slot's executed plan rows (plan.executed, migration.py:119-121) run on
+     the GPUs: kv_transfer / forced_kv_transfer -> kvm_migrate,
+     token_transfer -> kvm_reprefill.  Group items move the members that are
+     physically on the row's src (SURVEY.md §7 hard part 5).
+
+Each logical GPU of the trace gets its own KV pool; several logical GPUs may
+share one physical device (the whole 8-GPU trace replays on one B200 with a
+down-scaled KV shape; token counts and therefore every decision are unchanged,
+bytes scale by shape.kv_bytes_per_token / reference bpt).
+
+Correctness: every block a request owns carries a fingerprint that depends on
+(request, logical block, layer, K|V); `verify()` checks every resident request
+still reads back its own fingerprint wherever it now lives.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from .planner import DEFERRED, TOKEN_TRANSFER, PendingMove, PlannedMove
+
+
+@dataclass
+class SlotStats:
+    slot: int
+    rows: int
+    executed: int
+    kv_moves: int
+    token_moves: int
+    bytes_moved: int          # bytes physically copied by kvm_migrate (whole blocks)
+    tokens_moved: int         # tokens of the requests copied (algorithmic bytes = x bpt)
+    ref_kv_bytes: int         # sum of the reference's kv_bytes over executed kv rows (at its bpt)
+    seconds: float
+
+
+@dataclass
+class ReplayReport:
+    slots: List[SlotStats] = field(default_factory=list)
+    verified_requests: int = 0
+    recomputed_requests: int = 0
+
+    @property
+    def bytes_moved(self) -> int:
+        return sum(s.bytes_moved for s in self.slots)
+
+    @property
+    def executed(self) -> int:
+        return sum(s.executed for s in self.slots)
+
+    @property
+    def tokens_moved(self) -> int:
+        return sum(s.tokens_moved for s in self.slots)
+
+    @property
+    def migrate_seconds(self) -> float:
+        return sum(s.seconds for s in self.slots)
+
+
+def tokens_at(rec, slot: int, tokens_per_slot: int) -> int:
+    """model.py:58-69 in tokens."""
+    _, arrival, prompt, response = rec
+    return prompt + min(response, tokens_per_slot * max(0, slot - arrival))
+
+
+class TraceReplay:
+    """Drive a MigrationExecutor with a recorded reference run."""
+
+    def __init__(self, fixture: dict, executor, ref_bpt: Optional[int] = None, fingerprint: bool = True):
+        self.fx = fixture
+        self.ex = executor
+        self.ref_bpt = ref_bpt or fixture["config"]["workload"]["kv_bytes_per_token"]
+        self.tps = fixture["config"]["sim"].get("tokens_per_slot", 10)
+        self.trace = {r[0]: tuple(r) for r in fixture["trace"]}
+        self.rows_by_slot: Dict[int, list] = {}
+        for row in fixture["plan_rows"]:
+            self.rows_by_slot.setdefault(row[0], []).append(row)
+        self.fingerprint = fingerprint
+        self.recomputed: set = set()
+        self._stamped: Dict[int, int] = {}   # rid -> number of blocks stamped
+        self.reports: list = []              # per-slot ExecReport (None if nothing executed)
+
+    # -- fingerprints ------------------------------------------------------------
+    def _stamp(self, rid: int) -> None:
+        """Write the fingerprint into blocks the request gained since last time."""
+        if not self.fingerprint or rid in self.recomputed:
+            return
+        import torch
+
+        r = self.ex.where(rid)
+        start = self._stamped.get(rid, 0)
+        if start >= len(r.blocks):
+            return
+        pool = self.ex.pools[r.gpu]
+        idx = torch.from_numpy(r.blocks[start:].astype(np.int64)).to(pool.tensor.device)
+        vals = self._values(rid, start, len(r.blocks), pool)
+        pool.tensor.view(torch.int16)[:, :, idx] = vals
+        self._stamped[rid] = len(r.blocks)
+
+    @staticmethod
+    def _values(rid, lo, hi, pool):
+        import torch
+
+        L = pool.shape.layers
+        dev = pool.tensor.device
+        i = torch.arange(lo, hi, device=dev, dtype=torch.int32)
+        base = (rid * 7919 + i * 104729) % 16381
+        lay = torch.arange(L, device=dev, dtype=torch.int32)[:, None, None] * 2
+        kv = torch.arange(2, device=dev, dtype=torch.int32)[None, :, None]
+        v = (base[None, None, :] * 2 + lay * 3 + kv) % 32749 - 16374
+        return v.to(torch.int16)[..., None, None, None].expand(L, 2, hi - lo, *pool.view_shape[3:])
+
+    def verify(self) -> int:
+        """Every resident (not re-prefilled) request reads back its fingerprint."""
+        import torch
+
+        n = 0
+        for rid, r in self.ex.loc.items():
+            if rid in self.recomputed or not self.fingerprint:
+                continue
+            pool = self.ex.pools[r.gpu]
+            got = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(r.blocks.astype(np.int64)).to(
+                pool.tensor.device)]
+            exp = self._values(rid, 0, len(r.blocks), pool)
+            if not torch.equal(got, exp):
+                raise AssertionError(f"request {rid} on GPU {r.gpu}: KV bytes differ from its fingerprint")
+            n += 1
+        return n
+
+    # -- the slot loop -------------------------------------------------------------
+    def run(self, max_slots: Optional[int] = None, verify_every: int = 0) -> ReplayReport:
+        if self.fingerprint:
+            import torch
+
+        rep = ReplayReport()
+        ex = self.ex
+        slots = self.fx["slots"]
+        n_slots = len(slots) if max_slots is None else min(max_slots, len(slots))
+        for s in range(n_slots):
+            ev = slots[s]
+            # 1. departures (completed, rejected, aborted)
+            for rid in list(ev["done"]) + list(ev["gone"]):
+                if rid in ex.loc:
+                    ex.release(rid)
+                    self._stamped.pop(rid, None)
+                    self.recomputed.discard(rid)
+            # 2. decode growth of resident requests on their physical GPU
+            for rid in list(ex.loc):
+                if rid in self.trace:
+                    tok = tokens_at(self.trace[rid], s, self.tps)
+                    if tok > ex.loc[rid].tokens:
+                        ex.grow(rid, tok)
+                        self._stamp(rid)
+            # 3. arrivals at the scheduler's placement
+            for rid, gpu, size in ev["arr"]:
+                if gpu < 0 or rid in ex.loc:
+                    continue
+                ex.admit(rid, gpu, size // self.ref_bpt)
+                self._stamp(rid)
+            # 4. the slot's executed plan rows
+            rows = self.rows_by_slot.get(s, [])
+            planned, members = [], {}
+            ref_bytes = 0
+            for (_slot, item, src, dst, kvb, tok, mode, mem, _sizes) in rows:
+                if mode == DEFERRED:
+                    continue
+                planned.append(PlannedMove(PendingMove(item, src, dst, kvb, tok), mode))
+                members[item] = mem
+                if mode != TOKEN_TRANSFER:
+                    ref_bytes += kvb
+            t0 = time.perf_counter()
+            report = ex.execute(planned, members_of=lambda it: members.get(it, [it])) if planned else None
+            dt = time.perf_counter() - t0
+            if report is not None:
+                for rec in report.records:
+                    if rec.mode == TOKEN_TRANSFER:
+                        self.recomputed.update(rec.requests)
+            rep.slots.append(SlotStats(
+                s, len(rows), len(planned),
+                sum(1 for p in planned if p.mode != TOKEN_TRANSFER),
+                sum(1 for p in planned if p.mode == TOKEN_TRANSFER),
+                report.bytes_moved if report else 0, report.tokens_moved if report else 0,
+                ref_bytes, dt))
+            self.reports.append(report)
+            if self.fingerprint and verify_every and (s + 1) % verify_every == 0:
+                torch.cuda.synchronize()
+                self.verify()
+        if self.fingerprint:
+            torch.cuda.synchronize()
+            rep.verified_requests = self.verify()
+        rep.recomputed_requests = len(self.recomputed)
+        return rep
+
+
+def pool_blocks_for(fixture: dict, shape_block_tokens: int = 16, headroom: float = 1.5) -> int:
+    """Blocks per logical GPU: capacity in tokens (capacity_bytes / bpt) with
+    headroom for the physical-vs-logical skew of deferred moves (the physical
+    source can hold ~1.2 C, SURVEY.md §7 hard part 4)."""
+    cap_tokens = fixture["config"]["cluster"]["capacity_bytes"] // fixture["config"]["workload"]["kv_bytes_per_token"]
+    return int(math.ceil(headroom * cap_tokens / shape_block_tokens))

@@ -164,8 +164,15 @@ B200_7B_DOC = {
 }
 
 
-def trace_fixture(seed: int) -> dict:
-    doc = json.loads(json.dumps(B200_7B_DOC))
+# Same trace with tighter link budgets and a faster prefill so the planner
+# also picks token_transfer (re-prefill) and defers more: exercises every mode.
+MIXED_DOC = json.loads(json.dumps(B200_7B_DOC))
+MIXED_DOC["cluster"]["intra_bandwidth_bytes_per_s"] = 200e9
+MIXED_DOC["cluster"]["prefill_tokens_per_s"] = 500_000.0
+
+
+def trace_fixture(seed: int, base: dict = B200_7B_DOC) -> dict:
+    doc = json.loads(json.dumps(base))
     doc["sim"]["seed"] = seed
     cfg = config_from_dict(doc)
     w = cfg.workload
@@ -196,19 +203,36 @@ def trace_fixture(seed: int) -> dict:
                          members, member_sizes])
         return plan
 
+    slots = []
+    orig_step = refsim.MellScheduler.step_epoch
+
+    def spy_step(self, arrivals, completions, growths=None):
+        res = orig_step(self, arrivals, completions, growths=growths)
+        cl = state["cluster"]
+        gone = [int(ev[1]) for ev in res.events if ev and ev[0] in ("rejected", "aborted")]
+        arr = []
+        for rid, size in arrivals:
+            item = cl.item_of_request(rid)
+            arr.append([rid, cl.placement.get(item, -1), size])
+        slots.append({"arr": arr, "done": list(completions), "gone": gone})
+        return res
+
     refsim.plan_hybrid = spy_plan
     refsim.ClusterState = SpyCluster
+    refsim.MellScheduler.step_epoch = spy_step
     try:
         res = refsim.run(cfg, trace)
     finally:
         refsim.plan_hybrid = orig_plan
         refsim.ClusterState = orig_cluster
+        refsim.MellScheduler.step_epoch = orig_step
     fp = hashlib.sha256(json.dumps([r[:7] for r in rows]).encode()).hexdigest()[:16]
     return {
         "config": doc,
         "trace": [[r.request_id, r.arrival_slot, r.prompt_tokens, r.response_tokens]
                   for r in trace.records],
         "plan_rows": rows,
+        "slots": slots,
         "plan_rows_sha256_16": fp,
         "active_gpus": res.metrics.active_gpus,
         "migrations": res.metrics.migrations,
@@ -229,6 +253,11 @@ def main() -> int:
             json.dump(fx, fh, separators=(",", ":"))
         print(f"seed {seed}: {len(fx['trace'])} requests, {len(fx['plan_rows'])} plan rows, "
               f"peak {fx['summary']['peak_gpus']}, sha {fx['plan_rows_sha256_16']}")
+    fx = trace_fixture(0, MIXED_DOC)
+    with open(os.path.join(HERE, "trace_7b_mixed_seed0.json"), "w") as fh:
+        json.dump(fx, fh, separators=(",", ":"))
+    print(f"mixed seed 0: {len(fx['plan_rows'])} plan rows, modes "
+          f"{sorted(set(r[6] for r in fx['plan_rows']))}, sha {fx['plan_rows_sha256_16']}")
     print("kvpack from", os.path.dirname(kvpack.__file__))
     return 0
 

@@ -1,0 +1,71 @@
+"""Replay a recorded reference run (tests/golden/trace_*.json) on GPU pools.
+
+    python tools/replay_trace.py [--fixture tests/golden/trace_7b_c48g_seed0.json]
+                                 [--shape mini|full] [--max-slots N] [--engine bulk|ldg]
+
+Logical GPU g of the trace maps to physical device g % device_count.  With
+--shape mini (default) the KV shape is Llama-2-7B's layer count with 2 KV
+heads (32 KiB/token, 1/16 of 7B) so all 8 logical pools fit one B200; token
+counts, and therefore every scheduler/planner decision, are the reference's.
+Prints one JSON line with the totals.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2501_06709_b200.executor import MigrationExecutor  # noqa: E402
+from paper_2501_06709_b200.kvcache import LLAMA2_7B, BlockTable, KVPool, ModelShape  # noqa: E402
+from paper_2501_06709_b200.replay import TraceReplay, pool_blocks_for  # noqa: E402
+from paper_2501_06709_b200.reprefill import ReprefillEngine  # noqa: E402
+
+MINI_7B = ModelShape("llama2-7b-mini", layers=32, kv_heads=2, head_dim=128, q_heads=2, d_model=512)
+
+
+def build(fx, shape, engine, devices):
+    n_gpus = fx["summary"]["peak_gpus"]
+    nb = pool_blocks_for(fx, shape.block_tokens)
+    pools, tables = {}, {}
+    for g in range(n_gpus):
+        dev = devices[g % len(devices)]
+        pools[g] = KVPool(shape, nb, device=dev, dtype=torch.bfloat16)
+        tables[g] = BlockTable(512, 1024, device=dev)
+    rp = ReprefillEngine(shape, sorted({p.device for p in pools.values()}), with_q=False)
+    return MigrationExecutor(pools, tables, engine=engine, reprefill=rp), nb
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--fixture", default=os.path.join("tests", "golden", "trace_7b_c48g_seed0.json"))
+    ap.add_argument("--shape", choices=["mini", "full"], default="mini")
+    ap.add_argument("--max-slots", type=int, default=None)
+    ap.add_argument("--engine", choices=["bulk", "ldg"], default="bulk")
+    ap.add_argument("--verify-every", type=int, default=0)
+    a = ap.parse_args()
+    with open(a.fixture) as fh:
+        fx = json.load(fh)
+    shape = MINI_7B if a.shape == "mini" else LLAMA2_7B
+    devices = list(range(torch.cuda.device_count()))
+    ex, nb = build(fx, shape, a.engine, devices)
+    rep = TraceReplay(fx, ex).run(max_slots=a.max_slots, verify_every=a.verify_every)
+    scale = shape.kv_bytes_per_token / fx["config"]["workload"]["kv_bytes_per_token"]
+    ref_bytes = sum(s.ref_kv_bytes for s in rep.slots)
+    out = {
+        "fixture": os.path.basename(a.fixture), "shape": shape.name, "devices": len(devices),
+        "logical_gpus": len(ex.pools), "pool_blocks": nb, "slots": len(rep.slots),
+        "executed_rows": rep.executed,
+        "kv_moves": sum(s.kv_moves for s in rep.slots), "token_moves": sum(s.token_moves for s in rep.slots),
+        "bytes_moved": rep.bytes_moved, "ref_kv_bytes_scaled": int(ref_bytes * scale),
+        "execute_seconds": round(rep.migrate_seconds, 4),
+        "verified_requests": rep.verified_requests, "recomputed_requests": rep.recomputed_requests,
+        "fixture_sha": fx["plan_rows_sha256_16"],
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
