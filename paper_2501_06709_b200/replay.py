@@ -53,7 +53,7 @@ class SlotStats:
 @dataclass
 class ReplayReport:
     slots: List[SlotStats] = field(default_factory=list)
-    verified_requests: int = 0
+    verified_requests: int = 0     # request fingerprints checked (summed over checks)
     recomputed_requests: int = 0
 
     @property
@@ -200,10 +200,10 @@ class TraceReplay:
             self.reports.append(report)
             if self.fingerprint and verify_every and (s + 1) % verify_every == 0:
                 torch.cuda.synchronize()
-                self.verify()
+                rep.verified_requests += self.verify()
         if self.fingerprint:
             torch.cuda.synchronize()
-            rep.verified_requests = self.verify()
+            rep.verified_requests += self.verify()
         rep.recomputed_requests = len(self.recomputed)
         return rep
 

@@ -33,7 +33,7 @@ def build(fx, shape, engine, devices):
     for g in range(n_gpus):
         dev = devices[g % len(devices)]
         pools[g] = KVPool(shape, nb, device=dev, dtype=torch.bfloat16)
-        tables[g] = BlockTable(512, 1024, device=dev)
+        tables[g] = BlockTable(512, nb, device=dev)
     rp = ReprefillEngine(shape, sorted({p.device for p in pools.values()}), with_q=False)
     return MigrationExecutor(pools, tables, engine=engine, reprefill=rp), nb
 
@@ -44,7 +44,7 @@ def main():
     ap.add_argument("--shape", choices=["mini", "full"], default="mini")
     ap.add_argument("--max-slots", type=int, default=None)
     ap.add_argument("--engine", choices=["bulk", "ldg"], default="bulk")
-    ap.add_argument("--verify-every", type=int, default=0)
+    ap.add_argument("--verify-every", type=int, default=50)
     a = ap.parse_args()
     with open(a.fixture) as fh:
         fx = json.load(fh)
