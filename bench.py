@@ -251,7 +251,7 @@ def run_ours(args) -> int:
     shape = SHAPES[shape_name]
     kv_bytes = tokens * shape.kv_bytes_per_token
     n, nb, sb_np, used = _layout(shape, tokens, seed=1 + ri.rank)
-    eng = ENGINES[args.engine]
+    eng = ENGINES[args.engine] | (_native.KVM_F_L2_EVICT_FIRST if args.l2_evict_first else 0)
     lib = _native.lib()
 
     pool = KVPool(shape, nb, device=device)
@@ -463,7 +463,7 @@ def run_ours(args) -> int:
                                     f"same pool)" if world == 1 else
                                     f"{args.workload} ring push i->(i+1) mod {world} over NVLink (CUDA IPC)"),
                        "baseline_config": cfg_desc, "kv_bytes_per_rank_per_step": kv_bytes, "blocks": n,
-                       "pool_blocks": nb, "engine": args.engine,
+                       "pool_blocks": nb, "engine": args.engine, "l2_evict_first": bool(args.l2_evict_first),
                        "l2": "inputs larger than L2 (%.1f GiB per step per rank)" % (kv_bytes / 2 ** 30),
                        "parallelism": f"{world} ranks, one process per GPU" if world > 1 else "1 GPU"},
             "latency_ms": {"p50": round(p50, 4), "p99": round(p99, 4),
@@ -493,6 +493,8 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="7b-4k")
     ap.add_argument("--engine", choices=["ldg", "bulk"], default="bulk")
+    ap.add_argument("--l2-evict-first", type=int, choices=[0, 1], default=0,
+                    help="stream KV through L2 with an evict-first policy (KVM_F_L2_EVICT_FIRST)")
     ap.add_argument("--cpu-budget-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)

@@ -58,6 +58,13 @@ extern "C" {
                                     call (pinned ring + async H2D on `stream`) */
 #define KVM_F_ENGINE_BULK 0x2    /* copy engine: TMA bulk (cp.async.bulk) through
                                     shared memory instead of LDG.128/STG.128  */
+#define KVM_F_L2_EVICT_FIRST 0x4 /* stream the KV through L2 with an evict-first
+                                    cache policy (keeps a co-running kernel's
+                                    working set, e.g. re-prefill weights, in L2) */
+/* Cap the copy kernel at n CTAs per SM (bits 8..15; 0 = occupancy maximum), so
+ * it can share SMs with a concurrently running persistent kernel (e.g. the
+ * re-prefill GEMM of a split move on the same GPU). */
+#define KVM_F_CTAS_PER_SM(n) (((n)&0xff) << 8)
 
 /* Pool geometry. */
 typedef struct kvm_pool_desc {

@@ -24,7 +24,12 @@ KVM_ERR_UNSUPPORTED = -5
 
 KVM_F_BLOCKS_ON_HOST = 0x1
 KVM_F_ENGINE_BULK = 0x2
+KVM_F_L2_EVICT_FIRST = 0x4
 KVM_MAX_MOVES = 96
+
+
+def KVM_F_CTAS_PER_SM(n: int) -> int:
+    return (n & 0xFF) << 8
 
 # Every symbol include/kvmig.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (

@@ -127,17 +127,34 @@ struct MigrateParams {
   DevMove m[KVM_MAX_MOVES];
 };
 
-__device__ __forceinline__ int4 ld_stream(const int4* p) {
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <bool kEvictFirst>
+__device__ __forceinline__ int4 ld_stream(const int4* p, uint64_t pol) {
   int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  if (kEvictFirst)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
   return r;
 }
-__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
-  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
-               "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
+template <bool kEvictFirst>
+__device__ __forceinline__ void st_stream(int4* p, const int4& v, uint64_t pol) {
+  if (kEvictFirst)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
+  else
+    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
 }
 
 struct TileRef {
@@ -217,9 +234,11 @@ __device__ __forceinline__ void finalize_move(const DevMove& mv, int tid, int nt
 }
 
 // ------------------------- LDG/STG engine ----------------------------------
+template <bool kEvictFirst>
 __global__ void __launch_bounds__(kLdgThreads)
     migrate_ldg_kernel(const __grid_constant__ MigrateParams p) {
   __shared__ int s_done;
+  const uint64_t pol = kEvictFirst ? l2_evict_first_policy() : 0;
   int cur = 0;
   int key_move = -1, key_layer = -1, key_n = 0;
   const int tid = threadIdx.x;
@@ -243,20 +262,20 @@ __global__ void __launch_bounds__(kLdgThreads)
     if (nvec == kLdgThreads * kLdgVecPerThread) {
       int4 v[kLdgVecPerThread];
 #pragma unroll
-      for (int k = 0; k < kLdgVecPerThread; ++k) v[k] = ld_stream(s + tid + k * kLdgThreads);
+      for (int k = 0; k < kLdgVecPerThread; ++k) v[k] = ld_stream<kEvictFirst>(s + tid + k * kLdgThreads, pol);
 #pragma unroll
-      for (int k = 0; k < kLdgVecPerThread; ++k) st_stream(d + tid + k * kLdgThreads, v[k]);
+      for (int k = 0; k < kLdgVecPerThread; ++k) st_stream<kEvictFirst>(d + tid + k * kLdgThreads, v[k], pol);
     } else {
       int4 v[kLdgVecPerThread];
 #pragma unroll
       for (int k = 0; k < kLdgVecPerThread; ++k) {
         int i = tid + k * kLdgThreads;
-        if (i < nvec) v[k] = ld_stream(s + i);
+        if (i < nvec) v[k] = ld_stream<kEvictFirst>(s + i, pol);
       }
 #pragma unroll
       for (int k = 0; k < kLdgVecPerThread; ++k) {
         int i = tid + k * kLdgThreads;
-        if (i < nvec) st_stream(d + i, v[k]);
+        if (i < nvec) st_stream<kEvictFirst>(d + i, v[k], pol);
       }
     }
     ++key_n;
@@ -293,17 +312,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+template <bool kEvictFirst>
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  if (kEvictFirst) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(smem)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+    return;
+  }
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(smem)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-               "r"(smem_u32(smem)), "r"(bytes)
-               : "memory");
+template <bool kEvictFirst>
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem, uint32_t bytes, uint64_t pol) {
+  if (kEvictFirst)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(smem)), "r"(bytes)
+                 : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 template <int N>
@@ -316,8 +351,10 @@ __device__ __forceinline__ void bulk_wait_all() {
 
 // One warp per CTA; lane 0 drives the bulk unit, the warp cooperates on the
 // block-table rewrite.  Dynamic smem: kBulkStages * kTileBytes + barriers.
+template <bool kEvictFirst>
 __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant__ MigrateParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+  const uint64_t pol = kEvictFirst ? l2_evict_first_policy() : 0;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * kTileBytes);
   const int lane = threadIdx.x;
   if (lane == 0) {
@@ -360,7 +397,7 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
       }
       if (lane == 0) {
         mbar_wait(full + sj, (uint32_t)((j / kBulkStages) & 1));
-        bulk_s2g(st_dst[sj], smem + sj * kTileBytes, (uint32_t)st_len[sj]);
+        bulk_s2g<kEvictFirst>(st_dst[sj], smem + sj * kTileBytes, (uint32_t)st_len[sj], pol);
       }
       ++key_n;
     }
@@ -376,7 +413,7 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
         st_move[si] = tr.move;
         st_layer[si] = p.per_layer_flush ? tr.layer : 0;
         mbar_expect_tx(full + si, (uint32_t)tr.len);
-        bulk_g2s(smem + si * kTileBytes, tr.src, (uint32_t)tr.len, full + si);
+        bulk_g2s<kEvictFirst>(smem + si * kTileBytes, tr.src, (uint32_t)tr.len, full + si, pol);
       }
     }
   }
@@ -443,13 +480,15 @@ static int dev_init(int device, DevState& ds) {
   for (int i = 0; i < kSlots; ++i)
     KVM_CUDA_TRY(cudaEventCreateWithFlags(&ds.slots[i].ev, cudaEventDisableTiming));
   int occ = 0;
-  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, migrate_ldg_kernel, kLdgThreads, 0));
+  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, migrate_ldg_kernel<false>, kLdgThreads, 0));
   ds.ldg_grid = sm_count(device) * std::max(occ, 1);
   const size_t bulk_smem = kBulkStages * kTileBytes + 64;
-  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bulk_smem));
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)bulk_smem));
   int occb = 0;
-  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occb, migrate_bulk_kernel, 32, bulk_smem));
+  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occb, migrate_bulk_kernel<false>, 32, bulk_smem));
   ds.bulk_grid = sm_count(device) * std::max(occb, 1);
   ds.init = true;
   return KVM_OK;
@@ -595,12 +634,20 @@ static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t s
   bool any_empty = false;
   for (int i = 0; i < n; ++i) any_empty |= (moves[i].n_blocks == 0);
   if (tiles > 0) {
+    const int cap = (flags >> 8) & 0xff;
+    const int nsm = sm_count(device);
     if (flags & KVM_F_ENGINE_BULK) {
-      int grid = (int)std::min<int64_t>(tiles, ds.bulk_grid);
-      migrate_bulk_kernel<<<grid, 32, kBulkStages * kTileBytes + 64, stream>>>(p);
+      int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.bulk_grid, cap * nsm) : ds.bulk_grid);
+      if (flags & KVM_F_L2_EVICT_FIRST)
+        migrate_bulk_kernel<true><<<grid, 32, kBulkStages * kTileBytes + 64, stream>>>(p);
+      else
+        migrate_bulk_kernel<false><<<grid, 32, kBulkStages * kTileBytes + 64, stream>>>(p);
     } else {
-      int grid = (int)std::min<int64_t>(tiles, ds.ldg_grid);
-      migrate_ldg_kernel<<<grid, kLdgThreads, 0, stream>>>(p);
+      int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.ldg_grid, cap * nsm) : ds.ldg_grid);
+      if (flags & KVM_F_L2_EVICT_FIRST)
+        migrate_ldg_kernel<true><<<grid, kLdgThreads, 0, stream>>>(p);
+      else
+        migrate_ldg_kernel<false><<<grid, kLdgThreads, 0, stream>>>(p);
     }
     KVM_CUDA_TRY(cudaGetLastError());
     count_launch();
@@ -769,7 +816,7 @@ int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream) {
   if (n_moves < 0) return fail(KVM_ERR_INVALID, "n_moves < 0");
   if (n_moves == 0) return KVM_OK;
   if (!moves) return fail(KVM_ERR_INVALID, "moves is NULL");
-  if (flags & ~(KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK))
+  if (flags & ~(KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK | KVM_F_L2_EVICT_FIRST | KVM_F_CTAS_PER_SM(0xff)))
     return fail(KVM_ERR_INVALID, "unknown flags");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < n_moves; i += KVM_MAX_MOVES) {

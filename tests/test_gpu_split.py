@@ -1,0 +1,53 @@
+"""configs[2] split migration on one B200: the transferred prefix is bit-exact
+and the re-prefilled suffix is within the stated bf16 tolerance, with the two
+halves running concurrently on two streams (GEMM first, copy in the SM slots
+it leaves)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2501_06709_b200 import _native
+from paper_2501_06709_b200.kvcache import BlockTable, KVPool, ModelShape
+from paper_2501_06709_b200.reprefill import split_point, synthetic_hidden, synthetic_weights
+from paper_2501_06709_b200.split import flops_per_token, make_split, split_migrate, wait_split
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("tokens,suffix", [(1024, 240), (1000, 232), (512, 0), (512, 512), (16 * 40, None)])
+def test_split_migration(tokens, suffix):
+    shape = ModelShape("sp", layers=6, kv_heads=4, head_dim=128, q_heads=8, d_model=512)
+    if suffix is None:
+        suffix = split_point(tokens, shape.kv_bytes_per_token, 770e9, flops_per_token(shape), 1.2e15)
+    plan = make_split(tokens, suffix)
+    nb = plan.total_blocks + 20
+    src, dst = KVPool(shape, nb, dtype=torch.bfloat16), KVPool(shape, nb, dtype=torch.bfloat16)
+    src.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    dst.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(3))[:plan.total_blocks].to(torch.int32).numpy()
+    db = torch.from_numpy(dst.allocator.alloc(plan.total_blocks)).cuda()
+    x = synthetic_hidden(shape, max(suffix, 1), 0, seed=4)[:suffix].contiguous()
+    w = synthetic_weights(shape, 0, with_q=True, seed=5)
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    table = BlockTable(1, plan.total_blocks)
+    sa, sb_ = torch.cuda.Stream(), torch.cuda.Stream()
+    split_migrate(src, dst, sb, db, plan, x, w, xfer_stream=sa, rp_stream=sb_, flags_dev=flags, seq=7,
+                  table_row=table.row_ptr(0), engine_flags=_native.KVM_F_CTAS_PER_SM(3))
+    wait_split(flags, plan, 7, sb_)
+    sb_.synchronize()
+    sa.synchronize()
+    pre = plan.prefix_blocks
+    assert torch.equal(dst.tensor[:, :, db[:pre].long()].view(torch.int16),
+                       src.tensor[:, :, torch.from_numpy(sb[:pre]).long().cuda()].view(torch.int16))
+    assert np.array_equal(table.rows[0, :pre].cpu().numpy(), db[:pre].cpu().numpy())
+    if suffix:
+        kvd, qc = shape.kv_cols, shape.q_cols
+        toks = torch.arange(plan.prefix_tokens, tokens, device="cuda")
+        blk, slot = db.long()[toks // 16], toks % 16
+        for l in range(shape.layers):
+            ref = x.float() @ w[l].float().t()
+            torch.testing.assert_close(dst.tensor[l, 0, blk, slot].reshape(suffix, kvd).float(),
+                                       ref[:, qc:qc + kvd], atol=1e-2, rtol=1.6e-2)
+            torch.testing.assert_close(dst.tensor[l, 1, blk, slot].reshape(suffix, kvd).float(),
+                                       ref[:, qc + kvd:], atol=1e-2, rtol=1.6e-2)
+    assert flags.cpu().tolist() == [7 if pre else 0, 7 if suffix else 0]
