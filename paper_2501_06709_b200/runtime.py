@@ -1,0 +1,163 @@
+"""Live slot loop: any `step_epoch` scheduler -> planner -> GPU executor.
+
+This is the reference's slot loop (sim.py:151-227) with the data plane filled
+in.  The scheduler is the caller of the hot path and is used through the
+reference's duck-typed plugin API:
+
+    scheduler.step_epoch(arrivals: [(rid, size_bytes)], completions: [rid],
+                         growths={rid: size_bytes}) -> EpochResult
+                                                         (scheduler.py:979-981)
+    result.logs[i].moves  -> Move(item, src|None, dst, reason)   (scheduler.py:24-45)
+    result.logs[i].events -> ("rejected"|"aborted"|..., detail)
+
+and the cluster object it mutates is read through `placement`, `item_size`,
+`groups[gid].members` and `gpus[g].residents` (model.py:122-146).  So the
+reference's own MellScheduler/ClusterState plug in unchanged; the physical
+side (pools, blocks, bytes) is the executor's.
+
+Reference line map for the loop body:
+    growth / completions            sim.py:153-171
+    step_epoch                      sim.py:177
+    backlog + chain collapse        sim.py:179-187
+    departures / arrivals           sim.py:196-205
+    backlog refresh                 sim.py:207-217
+    plan + execute + retire/defer   sim.py:218-227   (executor.execute is the new part)
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
+
+from .planner import PendingMove, plan_hybrid
+
+
+@dataclass
+class LoopResult:
+    plan_rows: List[list] = field(default_factory=list)   # (slot, item, src, dst, kv_bytes, tokens, mode)
+    active_gpus: List[int] = field(default_factory=list)
+    logical_moves: List[int] = field(default_factory=list)
+    deferred: List[int] = field(default_factory=list)
+    forced: List[int] = field(default_factory=list)
+    bytes_moved: int = 0
+    completed: int = 0
+    rejected: int = 0
+    aborted: int = 0
+
+
+def _completion_slot(arrival: int, response: int, tps: int) -> int:
+    return arrival + math.ceil(response / tps)
+
+
+def _size_at(rec, slot, tps, bpt) -> int:
+    _, arrival, prompt, response = rec
+    return (prompt + min(response, tps * (slot - arrival))) * bpt
+
+
+def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, topology, boundaries, *,
+              bpt: int, tokens_per_slot: int = 10, epoch_slots: int = 1, max_defer: int = 3,
+              duration_slots: int = 0, executor=None, reserve_final: bool = False,
+              on_slot: Optional[Callable[[int, list], None]] = None) -> LoopResult:
+    """Run the slot loop; `records` are (request_id, arrival_slot, prompt, response).
+
+    With an executor, placements become executor.admit, growth executor.grow,
+    departures executor.release and executed plan rows executor.execute.
+    """
+    tps = tokens_per_slot
+    recs = {r[0]: tuple(r) for r in records}
+    by_slot: Dict[int, List[int]] = {}
+    for rid, (_, arrival, _p, _r) in recs.items():
+        by_slot.setdefault(arrival, []).append(rid)
+    last_arrival = max((r[1] for r in recs.values()), default=-1)
+    horizon = max(duration_slots, last_arrival + 1)
+    running: Dict[int, tuple] = {}
+    buffered: List[Tuple[int, int]] = []
+    pending: Dict[int, PendingMove] = {}
+    defer_counts: Dict[int, int] = {}
+    out = LoopResult()
+    slot = 0
+    while slot < horizon or running or buffered:
+        growths, completions = {}, []
+        for rid, rec in running.items():
+            if _completion_slot(rec[1], rec[3], tps) <= slot:
+                completions.append(rid)
+            else:
+                growths[rid] = _size_at(rec, slot, tps, bpt)
+        for rid in by_slot.get(slot, []):
+            _, _a, prompt, response = recs[rid]
+            size = (prompt + response) * bpt if reserve_final else prompt * bpt
+            buffered.append((rid, size))
+        if slot % epoch_slots == 0:
+            arrivals, buffered = buffered, []
+        else:
+            arrivals = []
+        result = scheduler.step_epoch(arrivals, completions, growths=growths)
+        n_moves = 0
+        gone = set(completions)
+        for log in result.logs:
+            for mv in log.moves:
+                if mv.src is not None:
+                    n_moves += 1
+                    phys = pending[mv.item].src if mv.item in pending else mv.src
+                    pending[mv.item] = PendingMove(mv.item, phys, mv.dst, 0, 0)
+            for kind, *detail in log.events:
+                if kind == "rejected":
+                    out.rejected += 1
+                    gone.add(int(detail[0]))
+                elif kind == "aborted":
+                    out.aborted += 1
+                    gone.add(int(detail[0]))
+        for rid in completions:
+            running.pop(rid, None)
+            out.completed += 1
+        for rid in gone - set(completions):
+            running.pop(rid, None)
+        for rid, _size in arrivals:
+            if rid not in gone:
+                running[rid] = recs[rid]
+        if executor is not None:
+            for rid in gone:
+                executor.release(rid)
+            for rid in running:
+                if rid in executor.loc:
+                    tok = _size_at(recs[rid], slot, tps, bpt) // bpt
+                    if tok > executor.loc[rid].tokens:
+                        executor.grow(rid, tok)
+            for rid, size in arrivals:
+                if rid in running and rid not in executor.loc:
+                    gpu = cluster.placement.get(cluster.item_of_request(rid))
+                    if gpu is not None:
+                        executor.admit(rid, gpu, size // bpt)
+        # data plane: refresh backlog, plan, execute, retire
+        for item in list(pending):
+            loc = cluster.placement.get(item)
+            if loc is None or loc == pending[item].src:
+                del pending[item]
+                defer_counts.pop(item, None)
+                continue
+            size = cluster.item_size(item)
+            pending[item] = PendingMove(item, pending[item].src, loc, size, size // bpt)
+        plan = plan_hybrid(list(pending.values()), boundaries, topology, defer_counts=defer_counts,
+                           max_defer=max_defer)
+        rows = [[slot, p.move.item, p.move.src, p.move.dst, p.move.kv_bytes, p.move.tokens, p.mode]
+                for p in plan.assignments]
+        out.plan_rows.extend(rows)
+        if executor is not None and plan.executed:
+            rep = executor.execute(plan, members_of=lambda gid: sorted(cluster.groups[gid].members)
+                                   if gid in cluster.groups else [])
+            out.bytes_moved += rep.bytes_moved
+        for planned in plan.executed:
+            del pending[planned.move.item]
+            defer_counts.pop(planned.move.item, None)
+        for mv in plan.deferred:
+            defer_counts[mv.item] = defer_counts.get(mv.item, 0) + 1
+        out.active_gpus.append(sum(1 for g in cluster.gpus.values() if g.residents))
+        out.logical_moves.append(n_moves)
+        out.deferred.append(len(plan.deferred))
+        out.forced.append(len(plan.forced))
+        if on_slot is not None:
+            on_slot(slot, rows)
+        slot += 1
+        if slot > horizon + 10 ** 6:
+            raise RuntimeError("slot loop failed to drain")
+    return out
