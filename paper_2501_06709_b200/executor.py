@@ -42,6 +42,7 @@ class Residency:
     gpu: int
     blocks: np.ndarray  # int32, logical block i -> pool block id
     tokens: int
+    model: str = ""     # ModelShape.name of the pool it lives in (multi-LLM)
 
 
 @dataclass
@@ -55,6 +56,7 @@ class ExecRecord:
     bytes_moved: int      # KV bytes physically copied (members found at src), whole blocks
     tokens_recomputed: int
     tokens_moved: int = 0  # tokens of the members copied: algorithmic bytes = tokens_moved * bpt
+    request_tokens: Dict[int, int] = field(default_factory=dict)  # per moved request: its tokens
 
 
 @dataclass
@@ -74,9 +76,11 @@ class ExecReport:
 class MigrationExecutor:
     """Executes planned moves over registered per-GPU pools.
 
-    pools:  logical GPU id -> KVPool (several logical GPUs may share one
-            physical device, e.g. replaying an 8-GPU trace on one B200).
-    tables: logical GPU id -> BlockTable (optional; when present the kernel
+    pools:  logical GPU id -> KVPool, or -> {model name: KVPool} when the GPU
+            serves several LLMs (multi-LLM: a request lives in the pool of its
+            model's shape).  Several logical GPUs may share one physical
+            device (e.g. replaying an 8-GPU trace on one B200).
+    tables: same keys -> BlockTable (optional; when present the kernel
             rewrites the destination row in place).
     reprefill: callable(executor, request_id, dst_gpu, dst_blocks, tokens,
             stream) that recomputes KV on the destination (token_transfer);
@@ -91,14 +95,19 @@ class MigrationExecutor:
             raise ConfigError(f"engine must be one of {sorted(ENGINES)}")
         if not pools:
             raise ConfigError("executor needs at least one pool")
-        shapes = {p.shape for p in pools.values()}
-        self.pools = dict(pools)
-        self.tables = dict(tables or {})
+        self.pools: Dict[int, Dict[str, KVPool]] = {g: _by_model(p) for g, p in pools.items()}
+        self.tables: Dict[int, Dict[str, BlockTable]] = {}
+        for g, t in (tables or {}).items():
+            if isinstance(t, dict):
+                self.tables[g] = dict(t)
+            else:  # one table per GPU: shared by the GPU's (single) model
+                self.tables[g] = {m: t for m in self.pools[g]}
+        models = {m for per in self.pools.values() for m in per}
+        self.default_model = next(iter(models)) if len(models) == 1 else None
         self.engine_flag = ENGINES[engine]
         self.reprefill = reprefill
         self.loc: Dict[int, Residency] = {}
         self._streams: Dict[int, "torch.cuda.Stream"] = {}
-        self._multi_shape = len(shapes) > 1
         _native.lib()  # fail loudly now if the native library is missing
 
     # -- streams ---------------------------------------------------------------
@@ -116,32 +125,50 @@ class MigrationExecutor:
             s.synchronize()
 
     # -- residency ---------------------------------------------------------------
-    def admit(self, rid: int, gpu: int, tokens: int) -> np.ndarray:
+    def pool(self, gpu: int, model: Optional[str] = None) -> KVPool:
+        """The pool of `model` on logical GPU `gpu` (model may be omitted when
+        the executor serves a single model)."""
+        per = self.pools.get(gpu)
+        if per is None:
+            raise NotPlaced(f"no KV pool registered for GPU {gpu}")
+        key = model or self.default_model
+        if key is None:
+            raise ValueError("several models are served: pass model=")
+        try:
+            return per[key]
+        except KeyError:
+            raise NotPlaced(f"GPU {gpu} has no pool for model {key!r}") from None
+
+    def pool_of(self, rid: int) -> KVPool:
+        r = self._res(rid)
+        return self.pool(r.gpu, r.model)
+
+    def admit(self, rid: int, gpu: int, tokens: int, model: Optional[str] = None) -> np.ndarray:
         """Allocate blocks for a new request on `gpu` (prefill happens elsewhere)."""
         if rid in self.loc:
             raise ValueError(f"request {rid} already resident")
-        pool = self._pool(gpu)
+        pool = self.pool(gpu, model)
         blocks = pool.allocator.alloc(pool.shape.blocks_for(tokens))
-        self.loc[rid] = Residency(gpu, blocks, tokens)
-        self._table_set(gpu, rid, blocks)
+        self.loc[rid] = Residency(gpu, blocks, tokens, pool.shape.name)
+        self._table_set(gpu, pool.shape.name, rid, blocks)
         return blocks
 
     def grow(self, rid: int, tokens: int) -> None:
         """Decode appended tokens: extend the block table when a block fills."""
         r = self._res(rid)
-        pool = self._pool(r.gpu)
+        pool = self.pool(r.gpu, r.model)
         need = pool.shape.blocks_for(tokens) - len(r.blocks)
         if need > 0:
             r.blocks = np.concatenate([r.blocks, pool.allocator.alloc(need)])
-            self._table_set(r.gpu, rid, r.blocks)
+            self._table_set(r.gpu, r.model, rid, r.blocks)
         r.tokens = tokens
 
     def release(self, rid: int) -> None:
         r = self.loc.pop(rid, None)
         if r is None:
             return
-        self._pool(r.gpu).allocator.free(r.blocks)
-        t = self.tables.get(r.gpu)
+        self.pool(r.gpu, r.model).allocator.free(r.blocks)
+        t = self._table(r.gpu, r.model)
         if t is not None:
             t.drop(rid)
 
@@ -170,9 +197,9 @@ class MigrationExecutor:
             if mv.src == mv.dst:
                 report.records.append(rec)
                 continue
-            src_pool, dst_pool = self._pool(mv.src), self._pool(mv.dst)
             for rid in here:
                 res = self.loc[rid]
+                src_pool, dst_pool = self.pool(mv.src, res.model), self.pool(mv.dst, res.model)
                 nb = len(res.blocks)
                 dst_blocks = dst_pool.allocator.alloc(nb)
                 if pm.mode in (KV_TRANSFER, FORCED_KV_TRANSFER):
@@ -183,7 +210,7 @@ class MigrationExecutor:
                     db = np.ascontiguousarray(dst_blocks, dtype=np.int32)
                     keep += [sb, db]
                     m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
-                    table = self.tables.get(mv.dst)
+                    table = self._table(mv.dst, res.model)
                     if table is not None:
                         table.set_host(rid, db)
                         m.dst_table_row = table.row_ptr(rid)
@@ -195,7 +222,7 @@ class MigrationExecutor:
                         raise ConfigError("token_transfer planned but executor has no re-prefill engine")
                     self.reprefill(self, rid, mv.dst, dst_blocks, res.tokens,
                                    self.stream(dst_pool.device))
-                    table = self.tables.get(mv.dst)
+                    table = self._table(mv.dst, res.model)
                     if table is not None:
                         table.set_host(rid, dst_blocks)
                         table.rows[table.slot(rid), :len(dst_blocks)].copy_(
@@ -205,6 +232,7 @@ class MigrationExecutor:
                 else:
                     raise ValueError(f"cannot execute mode {pm.mode!r}")
                 rec.blocks += nb
+                rec.request_tokens[rid] = res.tokens
                 post.append((rid, mv.dst, res.tokens, dst_blocks))
             report.records.append(rec)
         for dev, moves in by_dev.items():
@@ -221,11 +249,11 @@ class MigrationExecutor:
         """1-GPU case: move a request into the lowest free blocks of its own
         pool (defragmentation; kvm_compact = migrate with src pool == dst pool)."""
         res = self._res(rid)
-        pool = self._pool(res.gpu)
+        pool = self.pool(res.gpu, res.model)
         nb = len(res.blocks)
         dst = pool.allocator.alloc(nb)
         sb = np.ascontiguousarray(res.blocks, dtype=np.int32)
-        table = self.tables.get(res.gpu)
+        table = self._table(res.gpu, res.model)
         row = 0
         if table is not None:
             table.set_host(rid, dst)
@@ -263,17 +291,14 @@ class MigrationExecutor:
     def _commit(self, post, keep_table: bool = False) -> None:
         for rid, dst, tokens, dst_blocks in post:
             old = self.loc[rid]
-            self._pool(old.gpu).allocator.free(old.blocks)
-            t = self.tables.get(old.gpu)
+            self.pool(old.gpu, old.model).allocator.free(old.blocks)
+            t = self._table(old.gpu, old.model)
             if t is not None and not keep_table:
                 t.drop(rid)
-            self.loc[rid] = Residency(dst, np.asarray(dst_blocks, dtype=np.int32), tokens)
+            self.loc[rid] = Residency(dst, np.asarray(dst_blocks, dtype=np.int32), tokens, old.model)
 
-    def _pool(self, gpu: int) -> KVPool:
-        try:
-            return self.pools[gpu]
-        except KeyError:
-            raise NotPlaced(f"no KV pool registered for GPU {gpu}") from None
+    def _table(self, gpu: int, model: str) -> Optional[BlockTable]:
+        return self.tables.get(gpu, {}).get(model)
 
     def _res(self, rid: int) -> Residency:
         try:
@@ -281,12 +306,21 @@ class MigrationExecutor:
         except KeyError:
             raise NotPlaced(f"request {rid} is not resident") from None
 
-    def _table_set(self, gpu: int, rid: int, blocks: np.ndarray) -> None:
-        t = self.tables.get(gpu)
+    def _table_set(self, gpu: int, model: str, rid: int, blocks: np.ndarray) -> None:
+        t = self._table(gpu, model)
         if t is None:
             return
         t.set_host(rid, blocks)
         t.rows[t.slot(rid), :len(blocks)].copy_(_as_i32_tensor(blocks, t.device))
+
+
+def _by_model(p) -> Dict[str, KVPool]:
+    if isinstance(p, dict):
+        for name, pool in p.items():
+            if pool.shape.name != name:
+                raise ConfigError(f"pool keyed {name!r} has shape {pool.shape.name!r}")
+        return dict(p)
+    return {p.shape.name: p}
 
 
 def _as_i32_tensor(a: np.ndarray, device: int):

@@ -82,19 +82,30 @@ def tokens_at(rec, slot: int, tokens_per_slot: int) -> int:
 class TraceReplay:
     """Drive a MigrationExecutor with a recorded reference run."""
 
-    def __init__(self, fixture: dict, executor, ref_bpt: Optional[int] = None, fingerprint: bool = True):
+    def __init__(self, fixture: dict, executor, ref_bpt: Optional[int] = None, fingerprint: bool = True,
+                 model_map: Optional[Dict[str, str]] = None):
         self.fx = fixture
         self.ex = executor
-        self.ref_bpt = ref_bpt or fixture["config"]["workload"]["kv_bytes_per_token"]
+        wl_bpt = fixture["config"]["workload"]["kv_bytes_per_token"]
+        self.ref_bpt = ref_bpt or (wl_bpt if isinstance(wl_bpt, int) else None)
         self.tps = fixture["config"]["sim"].get("tokens_per_slot", 10)
         self.trace = {r[0]: tuple(r) for r in fixture["trace"]}
         self.rows_by_slot: Dict[int, list] = {}
         for row in fixture["plan_rows"]:
             self.rows_by_slot.setdefault(row[0], []).append(row)
         self.fingerprint = fingerprint
+        # multi-LLM fixtures carry the model of every request and its bytes/token
+        self.models: Dict[int, str] = {int(k): v for k, v in fixture.get("models", {}).items()}
+        self.model_bpt: Dict[str, int] = dict(fixture.get("model_bpt", {}))
+        # fixture model name -> executor pool key (e.g. a down-scaled shape's name)
+        self.model_map: Dict[str, str] = dict(model_map or {})
         self.recomputed: set = set()
         self._stamped: Dict[int, int] = {}   # rid -> number of blocks stamped
         self.reports: list = []              # per-slot ExecReport (None if nothing executed)
+
+    def bpt_of(self, rid: int) -> int:
+        m = self.models.get(rid)
+        return self.model_bpt[m] if m is not None else self.ref_bpt
 
     # -- fingerprints ------------------------------------------------------------
     def _stamp(self, rid: int) -> None:
@@ -107,7 +118,7 @@ class TraceReplay:
         start = self._stamped.get(rid, 0)
         if start >= len(r.blocks):
             return
-        pool = self.ex.pools[r.gpu]
+        pool = self.ex.pool(r.gpu, r.model)
         idx = torch.from_numpy(r.blocks[start:].astype(np.int64)).to(pool.tensor.device)
         vals = self._values(rid, start, len(r.blocks), pool)
         pool.tensor.view(torch.int16)[:, :, idx] = vals
@@ -134,7 +145,7 @@ class TraceReplay:
         for rid, r in self.ex.loc.items():
             if rid in self.recomputed or not self.fingerprint:
                 continue
-            pool = self.ex.pools[r.gpu]
+            pool = self.ex.pool(r.gpu, r.model)
             got = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(r.blocks.astype(np.int64)).to(
                 pool.tensor.device)]
             exp = self._values(rid, 0, len(r.blocks), pool)
@@ -171,7 +182,9 @@ class TraceReplay:
             for rid, gpu, size in ev["arr"]:
                 if gpu < 0 or rid in ex.loc:
                     continue
-                ex.admit(rid, gpu, size // self.ref_bpt)
+                model = self.models.get(rid)
+                ex.admit(rid, gpu, size // self.bpt_of(rid),
+                         model=self.model_map.get(model, model) if model else None)
                 self._stamp(rid)
             # 4. the slot's executed plan rows
             rows = self.rows_by_slot.get(s, [])
@@ -208,9 +221,11 @@ class TraceReplay:
         return rep
 
 
-def pool_blocks_for(fixture: dict, shape_block_tokens: int = 16, headroom: float = 1.5) -> int:
-    """Blocks per logical GPU: capacity in tokens (capacity_bytes / bpt) with
-    headroom for the physical-vs-logical skew of deferred moves (the physical
-    source can hold ~1.2 C, SURVEY.md §7 hard part 4)."""
-    cap_tokens = fixture["config"]["cluster"]["capacity_bytes"] // fixture["config"]["workload"]["kv_bytes_per_token"]
+def pool_blocks_for(fixture: dict, shape_block_tokens: int = 16, headroom: float = 1.5,
+                    model: Optional[str] = None) -> int:
+    """Blocks per logical GPU (per model): capacity in tokens
+    (capacity_bytes / bpt) with headroom for the physical-vs-logical skew of
+    deferred moves (the physical source can hold ~1.2 C)."""
+    bpt = fixture["model_bpt"][model] if model else fixture["config"]["workload"]["kv_bytes_per_token"]
+    cap_tokens = fixture["config"]["cluster"]["capacity_bytes"] // bpt
     return int(math.ceil(headroom * cap_tokens / shape_block_tokens))

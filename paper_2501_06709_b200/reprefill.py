@@ -85,26 +85,29 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
 
 class ReprefillEngine:
     """Executor plug-in for token_transfer moves: recompute a request's KV on
-    the destination from its (synthetic, seeded) hidden states."""
+    the destination from its (synthetic, seeded) hidden states.  One set of
+    synthetic weights per (device, model shape)."""
 
-    def __init__(self, shape: ModelShape, devices, with_q: bool = False, seed: int = 3):
-        self.shape = shape
+    def __init__(self, shapes, devices, with_q: bool = False, seed: int = 3):
+        shapes = [shapes] if isinstance(shapes, ModelShape) else list(shapes)
+        self.shapes = {s.name: s for s in shapes}
         self.with_q = with_q
-        self.weights = {d: synthetic_weights(shape, d, with_q=with_q, seed=seed) for d in set(devices)}
+        self.weights = {(d, s.name): synthetic_weights(s, d, with_q=with_q, seed=seed)
+                        for d in set(devices) for s in shapes}
 
-    def hidden(self, rid: int, tokens: int, device: int):
-        return synthetic_hidden(self.shape, tokens, device, seed=10_000 + rid)
+    def hidden(self, shape: ModelShape, rid: int, tokens: int, device: int):
+        return synthetic_hidden(shape, tokens, device, seed=10_000 + rid)
 
     def __call__(self, executor, rid: int, dst_gpu: int, dst_blocks: np.ndarray, tokens: int, stream):
         import torch
 
-        pool = executor.pools[dst_gpu]
+        pool = executor.pool(dst_gpu, executor.loc[rid].model)
         dev = pool.device
         with torch.cuda.stream(stream):
-            x = self.hidden(rid, tokens, dev)
+            x = self.hidden(pool.shape, rid, tokens, dev)
             blocks = torch.from_numpy(np.ascontiguousarray(dst_blocks, dtype=np.int32)).to(f"cuda:{dev}",
                                                                                           non_blocking=False)
-            reprefill(pool, x, self.weights[dev], blocks, tok0=0, stream=stream)
+            reprefill(pool, x, self.weights[(dev, pool.shape.name)], blocks, tok0=0, stream=stream)
             # keep the temporaries alive until the stream has consumed them
             x.record_stream(stream)
             blocks.record_stream(stream)

@@ -55,16 +55,34 @@ def _size_at(rec, slot, tps, bpt) -> int:
 
 
 def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, topology, boundaries, *,
-              bpt: int, tokens_per_slot: int = 10, epoch_slots: int = 1, max_defer: int = 3,
+              bpt, tokens_per_slot: int = 10, epoch_slots: int = 1, max_defer: int = 3,
               duration_slots: int = 0, executor=None, reserve_final: bool = False,
+              models: Optional[Dict[int, str]] = None,
               on_slot: Optional[Callable[[int, list], None]] = None) -> LoopResult:
     """Run the slot loop; `records` are (request_id, arrival_slot, prompt, response).
 
-    With an executor, placements become executor.admit, growth executor.grow,
-    departures executor.release and executed plan rows executor.execute.
+    `bpt` is the reference's kv_bytes_per_token (config.py:92), or — multi-LLM
+    extension — a dict request id -> bytes/token of that request's model
+    (the reference Request already carries a per-request bpt, model.py:38;
+    sim.run just sets them all equal).  `models` names each request's model
+    for the executor's per-model pools.  With an executor, placements become
+    executor.admit, growth executor.grow, departures executor.release and
+    executed plan rows executor.execute.
     """
     tps = tokens_per_slot
     recs = {r[0]: tuple(r) for r in records}
+    per_req = isinstance(bpt, dict)
+    bpt_of = (lambda rid: bpt[rid]) if per_req else (lambda rid: bpt)
+    models = models or {}
+
+    def item_tokens(item: int, size: int) -> int:
+        """sim.py:217 (size // bpt); per member for a mixed-model group."""
+        if not per_req:
+            return size // bpt
+        if item < 0:
+            return sum(cluster.sizes[m] // bpt[m] for m in cluster.groups[item].members)
+        return size // bpt[item]
+
     by_slot: Dict[int, List[int]] = {}
     for rid, (_, arrival, _p, _r) in recs.items():
         by_slot.setdefault(arrival, []).append(rid)
@@ -82,10 +100,10 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
             if _completion_slot(rec[1], rec[3], tps) <= slot:
                 completions.append(rid)
             else:
-                growths[rid] = _size_at(rec, slot, tps, bpt)
+                growths[rid] = _size_at(rec, slot, tps, bpt_of(rid))
         for rid in by_slot.get(slot, []):
             _, _a, prompt, response = recs[rid]
-            size = (prompt + response) * bpt if reserve_final else prompt * bpt
+            size = (prompt + response) * bpt_of(rid) if reserve_final else prompt * bpt_of(rid)
             buffered.append((rid, size))
         if slot % epoch_slots == 0:
             arrivals, buffered = buffered, []
@@ -120,14 +138,14 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
                 executor.release(rid)
             for rid in running:
                 if rid in executor.loc:
-                    tok = _size_at(recs[rid], slot, tps, bpt) // bpt
+                    tok = _size_at(recs[rid], slot, tps, bpt_of(rid)) // bpt_of(rid)
                     if tok > executor.loc[rid].tokens:
                         executor.grow(rid, tok)
             for rid, size in arrivals:
                 if rid in running and rid not in executor.loc:
                     gpu = cluster.placement.get(cluster.item_of_request(rid))
                     if gpu is not None:
-                        executor.admit(rid, gpu, size // bpt)
+                        executor.admit(rid, gpu, size // bpt_of(rid), model=models.get(rid))
         # data plane: refresh backlog, plan, execute, retire
         for item in list(pending):
             loc = cluster.placement.get(item)
@@ -136,7 +154,7 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
                 defer_counts.pop(item, None)
                 continue
             size = cluster.item_size(item)
-            pending[item] = PendingMove(item, pending[item].src, loc, size, size // bpt)
+            pending[item] = PendingMove(item, pending[item].src, loc, size, item_tokens(item, size))
         plan = plan_hybrid(list(pending.values()), boundaries, topology, defer_counts=defer_counts,
                            max_defer=max_defer)
         rows = [[slot, p.move.item, p.move.src, p.move.dst, p.move.kv_bytes, p.move.tokens, p.mode]

@@ -242,6 +242,69 @@ def trace_fixture(seed: int, base: dict = B200_7B_DOC) -> dict:
     }
 
 
+def multi_llm_fixture(seed: int = 0) -> dict:
+    """configs[4]: multi-LLM Poisson trace (7B + 13B mix).  The reference sim
+    has one kv_bytes_per_token (sim.py:105), so this run drives the REFERENCE
+    MellScheduler through this repo's slot loop (runtime.run_slots, proven
+    identical to sim.run on single-model traces by tests/test_runtime_cpu.py)
+    with per-request byte sizes; model per request ~ seeded Bernoulli(0.5)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    import numpy as np
+    from paper_2501_06709_b200.planner import Topology, load_boundaries
+    from paper_2501_06709_b200.runtime import run_slots
+
+    doc = json.loads(json.dumps(B200_7B_DOC))
+    doc["sim"]["seed"] = seed
+    w = doc["workload"]
+    dist = LengthDistribution(scale=w["scale"])
+    trace = gen_poisson(w["mean_interarrival_slots"], w["duration_slots"], dist, seed=seed)
+    rng = np.random.default_rng(1000 + seed)
+    model_bpt = {"llama2-7b": 524288, "llama2-13b": 819200}
+    models = {r.request_id: ("llama2-13b" if rng.random() < 0.5 else "llama2-7b") for r in trace.records}
+    bpt = {rid: model_bpt[m] for rid, m in models.items()}
+    cl = doc["cluster"]
+    cluster = kvpack.ClusterState(cl["capacity_bytes"], gpus_per_machine=cl["gpus_per_machine"])
+    sched = kvpack.MellScheduler(cluster, priority_cfg=kvpack.PriorityConfig(), batching=True)
+    topo = Topology(gpus_per_machine=cl["gpus_per_machine"],
+                    intra_bandwidth_bytes_per_s=cl["intra_bandwidth_bytes_per_s"],
+                    inter_bandwidth_bytes_per_s=cl["inter_bandwidth_bytes_per_s"],
+                    prefill_tokens_per_s=cl["prefill_tokens_per_s"])
+    bounds = load_boundaries(topo, doc["migration"]["epoch_seconds"], doc["migration"]["budget_fraction"])
+    slots, rows = [], []
+    orig_step = sched.step_epoch
+
+    def spy_step(arrivals, completions, growths=None):
+        res = orig_step(arrivals, completions, growths=growths)
+        gone = [int(ev[1]) for ev in res.events if ev and ev[0] in ("rejected", "aborted")]
+        arr = [[rid, cluster.placement.get(cluster.item_of_request(rid), -1), size] for rid, size in arrivals]
+        slots.append({"arr": arr, "done": list(completions), "gone": gone})
+        return res
+
+    sched.step_epoch = spy_step
+
+    def on_slot(slot, prow):
+        for r in prow:
+            item = r[1]
+            members = sorted(cluster.groups[item].members) if item < 0 and item in cluster.groups else [item]
+            rows.append(list(r) + [members, [cluster.sizes.get(m, 0) for m in members]])
+
+    out = run_slots([(r.request_id, r.arrival_slot, r.prompt_tokens, r.response_tokens) for r in trace.records],
+                    sched, cluster, topo, bounds, bpt=bpt, tokens_per_slot=doc["sim"]["tokens_per_slot"],
+                    max_defer=doc["migration"]["max_defer"], duration_slots=w["duration_slots"],
+                    on_slot=on_slot)
+    doc["workload"]["kv_bytes_per_token"] = "per-request (models / model_bpt)"
+    fp = hashlib.sha256(json.dumps([r[:7] for r in rows]).encode()).hexdigest()[:16]
+    return {
+        "config": doc, "models": {str(k): v for k, v in models.items()}, "model_bpt": model_bpt,
+        "trace": [[r.request_id, r.arrival_slot, r.prompt_tokens, r.response_tokens] for r in trace.records],
+        "plan_rows": rows, "slots": slots, "plan_rows_sha256_16": fp,
+        "active_gpus": out.active_gpus, "migrations": out.logical_moves, "deferred": out.deferred,
+        "forced": out.forced,
+        "summary": {"peak_gpus": max(out.active_gpus), "completed": out.completed, "rejected": out.rejected,
+                    "aborted": out.aborted, "total_migrations": sum(out.logical_moves)},
+    }
+
+
 def main() -> int:
     with open(os.path.join(HERE, "planner_cases.json"), "w") as fh:
         json.dump(planner_cases(), fh, separators=(",", ":"))
@@ -258,6 +321,11 @@ def main() -> int:
         json.dump(fx, fh, separators=(",", ":"))
     print(f"mixed seed 0: {len(fx['plan_rows'])} plan rows, modes "
           f"{sorted(set(r[6] for r in fx['plan_rows']))}, sha {fx['plan_rows_sha256_16']}")
+    fx = multi_llm_fixture(0)
+    with open(os.path.join(HERE, "trace_multillm_7b13b_seed0.json"), "w") as fh:
+        json.dump(fx, fh, separators=(",", ":"))
+    print(f"multi-LLM seed 0: {len(fx['trace'])} requests, {len(fx['plan_rows'])} plan rows, "
+          f"peak {fx['summary']['peak_gpus']}, sha {fx['plan_rows_sha256_16']}")
     print("kvpack from", os.path.dirname(kvpack.__file__))
     return 0
 

@@ -9,16 +9,18 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("name,max_slots", [("trace_7b_c48g_seed0.json", None),
-                                            ("trace_7b_mixed_seed0.json", 900)])
+                                            ("trace_7b_mixed_seed0.json", 900),
+                                            ("trace_multillm_7b13b_seed0.json", None)])
 def test_trace_replay_bit_exact(name, max_slots):
-    import sys, os
+    import os
+    import sys
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
-    from replay_trace import MINI_7B, build
+    from replay_trace import MINI, MINI_7B, build
     from paper_2501_06709_b200.replay import TraceReplay
 
     fx = load_golden(name)
-    ex, _ = build(fx, MINI_7B, "bulk", [0])
-    rp = TraceReplay(fx, ex)
+    ex, _ = build(fx, MINI_7B, "bulk", [0], MINI)
+    rp = TraceReplay(fx, ex, model_map={m: s.name for m, s in MINI.items()})
     rep = rp.run(max_slots=max_slots, verify_every=200)
     assert rep.executed > 0 and rep.verified_requests > 0
     if "mixed" in name:

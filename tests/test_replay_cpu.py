@@ -19,6 +19,8 @@ from paper_2501_06709_b200.planner import FORCED_KV_TRANSFER, KV_TRANSFER, TOKEN
 from paper_2501_06709_b200.replay import TraceReplay, pool_blocks_for
 
 MINI = ModelShape("mini", layers=32, kv_heads=2, head_dim=128, q_heads=2, d_model=512)
+MINI13 = ModelShape("mini13", layers=40, kv_heads=2, head_dim=128, q_heads=2, d_model=512)
+MODEL_MAP = {"llama2-7b": "mini", "llama2-13b": "mini13"}
 
 
 class HostPool:
@@ -59,11 +61,19 @@ FIXTURES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "t
 def test_replay_bookkeeping_matches_reference(name):
     fx = load_golden(name)
     n_gpus = fx["summary"]["peak_gpus"]
-    nb = pool_blocks_for(fx, 16)
-    ex = HostExecutor({g: HostPool(MINI, nb, g) for g in range(n_gpus)})
-    rp = TraceReplay(fx, ex, fingerprint=False)
+    models = fx.get("models")
+    if models:
+        nb = max(pool_blocks_for(fx, 16, model=m) for m in fx["model_bpt"])
+        ex = HostExecutor({g: {"mini": HostPool(MINI, nb, 2 * g), "mini13": HostPool(MINI13, nb, 2 * g + 1)}
+                           for g in range(n_gpus)})
+    else:
+        nb = pool_blocks_for(fx, 16)
+        ex = HostExecutor({g: HostPool(MINI, nb, g) for g in range(n_gpus)})
+    rp = TraceReplay(fx, ex, fingerprint=False, model_map=MODEL_MAP)
     rep = rp.run()
-    bpt = fx["config"]["workload"]["kv_bytes_per_token"]
+
+    def bpt_of(rid):
+        return fx["model_bpt"][models[str(rid)]] if models else fx["config"]["workload"]["kv_bytes_per_token"]
     rows = [r for r in fx["plan_rows"] if r[6] != "deferred"]
     assert rep.executed == len(rows)
     exact = partial = 0
@@ -79,11 +89,12 @@ def test_replay_bookkeeping_matches_reference(name):
             rec = recs[item]
             assert set(rec.requests) <= set(members)
             if mode in (KV_TRANSFER, FORCED_KV_TRANSFER):
-                assert rec.tokens_moved * bpt <= kvb
+                moved_bytes = sum(t * bpt_of(r) for r, t in rec.request_tokens.items())
+                assert moved_bytes <= kvb
                 if item >= 0 and rec.requests:
-                    assert rec.tokens_moved * bpt == kvb  # single request: exactly the reference bytes
+                    assert moved_bytes == kvb  # single request: exactly the reference bytes
                     exact += 1
-                if item < 0 and sum(sizes) == kvb and rec.tokens_moved * bpt < kvb:
+                if item < 0 and sum(sizes) == kvb and moved_bytes < kvb:
                     partial += 1
             else:
                 assert mode == TOKEN_TRANSFER
@@ -93,9 +104,10 @@ def test_replay_bookkeeping_matches_reference(name):
     assert exact > 0 or "mixed" in name
     # everyone still resident at the end is where its last executed move put it
     # or where it was admitted; pools' free counts add up
-    for g, pool in ex.pools.items():
-        held = sum(len(r.blocks) for r in ex.loc.values() if r.gpu == g)
-        assert pool.allocator.n_free + held == nb
+    for g, per in ex.pools.items():
+        for pool in per.values():
+            held = sum(len(r.blocks) for r in ex.loc.values() if r.gpu == g)
+            assert pool.allocator.n_free + held == nb
     kv_rows = sum(1 for r in rows if r[6] != TOKEN_TRANSFER)
     assert sum(len(b) for b in ex.launched) <= sum(len(r[7]) for r in rows if r[6] != TOKEN_TRANSFER)
     assert kv_rows == 0 or ex.launched

@@ -53,3 +53,26 @@ def test_live_loop_with_reference_scheduler(name):
     assert out.logical_moves == fx["migrations"]
     assert max(out.active_gpus) == fx["summary"]["peak_gpus"]
     assert out.completed == fx["summary"]["completed"]
+
+
+def test_multi_llm_loop_matches_fixture():
+    """configs[4] mixed 7B+13B: the reference scheduler with per-request byte
+    sizes through the live loop reproduces the committed multi-LLM fixture."""
+    kvpack = _kvpack()
+    fx = load_golden("trace_multillm_7b13b_seed0.json")
+    cfg = fx["config"]
+    cl = cfg["cluster"]
+    cluster = kvpack.ClusterState(cl["capacity_bytes"], gpus_per_machine=cl["gpus_per_machine"])
+    sched = kvpack.MellScheduler(cluster, priority_cfg=kvpack.PriorityConfig(), batching=True)
+    topo = Topology(gpus_per_machine=cl["gpus_per_machine"],
+                    intra_bandwidth_bytes_per_s=cl["intra_bandwidth_bytes_per_s"],
+                    inter_bandwidth_bytes_per_s=cl["inter_bandwidth_bytes_per_s"],
+                    prefill_tokens_per_s=cl["prefill_tokens_per_s"])
+    bounds = load_boundaries(topo, cfg["migration"]["epoch_seconds"], cfg["migration"]["budget_fraction"])
+    models = {int(k): v for k, v in fx["models"].items()}
+    bpt = {rid: fx["model_bpt"][m] for rid, m in models.items()}
+    out = run_slots([tuple(r) for r in fx["trace"]], sched, cluster, topo, bounds, bpt=bpt,
+                    tokens_per_slot=cfg["sim"]["tokens_per_slot"], max_defer=cfg["migration"]["max_defer"],
+                    duration_slots=cfg["workload"]["duration_slots"])
+    assert out.plan_rows == [r[:7] for r in fx["plan_rows"]]
+    assert out.active_gpus == fx["active_gpus"]

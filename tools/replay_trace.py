@@ -19,22 +19,38 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2501_06709_b200.executor import MigrationExecutor  # noqa: E402
-from paper_2501_06709_b200.kvcache import LLAMA2_7B, BlockTable, KVPool, ModelShape  # noqa: E402
+from paper_2501_06709_b200.kvcache import LLAMA2_7B, LLAMA2_13B, BlockTable, KVPool, ModelShape  # noqa: E402
 from paper_2501_06709_b200.replay import TraceReplay, pool_blocks_for  # noqa: E402
 from paper_2501_06709_b200.reprefill import ReprefillEngine  # noqa: E402
 
 MINI_7B = ModelShape("llama2-7b-mini", layers=32, kv_heads=2, head_dim=128, q_heads=2, d_model=512)
+MINI_13B = ModelShape("llama2-13b-mini", layers=40, kv_heads=2, head_dim=128, q_heads=2, d_model=512)
+MINI = {"llama2-7b": MINI_7B, "llama2-13b": MINI_13B}
+FULL = {"llama2-7b": LLAMA2_7B, "llama2-13b": LLAMA2_13B}
 
 
-def build(fx, shape, engine, devices):
+def build(fx, shape, engine, devices, shapes=None):
+    """One pool (per model, for multi-LLM fixtures) per logical GPU of the trace."""
     n_gpus = fx["summary"]["peak_gpus"]
-    nb = pool_blocks_for(fx, shape.block_tokens)
+    models = sorted(set(fx.get("models", {}).values()))
     pools, tables = {}, {}
+    nb = 0
     for g in range(n_gpus):
         dev = devices[g % len(devices)]
-        pools[g] = KVPool(shape, nb, device=dev, dtype=torch.bfloat16)
-        tables[g] = BlockTable(512, nb, device=dev)
-    rp = ReprefillEngine(shape, sorted({p.device for p in pools.values()}), with_q=False)
+        if models:
+            pools[g], tables[g] = {}, {}
+            for m in models:
+                sh = shapes[m]
+                nbm = pool_blocks_for(fx, sh.block_tokens, model=m)
+                nb = max(nb, nbm)
+                pools[g][sh.name] = KVPool(sh, nbm, device=dev, dtype=torch.bfloat16)
+                tables[g][sh.name] = BlockTable(512, nbm, device=dev)
+        else:
+            nb = pool_blocks_for(fx, shape.block_tokens)
+            pools[g] = KVPool(shape, nb, device=dev, dtype=torch.bfloat16)
+            tables[g] = BlockTable(512, nb, device=dev)
+    used = [shapes[m] for m in models] if models else [shape]
+    rp = ReprefillEngine(used, sorted(set(devices[g % len(devices)] for g in range(n_gpus))), with_q=False)
     return MigrationExecutor(pools, tables, engine=engine, reprefill=rp), nb
 
 
@@ -49,17 +65,22 @@ def main():
     with open(a.fixture) as fh:
         fx = json.load(fh)
     shape = MINI_7B if a.shape == "mini" else LLAMA2_7B
+    shapes = MINI if a.shape == "mini" else FULL
     devices = list(range(torch.cuda.device_count()))
-    ex, nb = build(fx, shape, a.engine, devices)
-    rep = TraceReplay(fx, ex).run(max_slots=a.max_slots, verify_every=a.verify_every)
-    scale = shape.kv_bytes_per_token / fx["config"]["workload"]["kv_bytes_per_token"]
+    ex, nb = build(fx, shape, a.engine, devices, shapes)
+    rp = TraceReplay(fx, ex, model_map={m: s.name for m, s in shapes.items()})
+    rep = rp.run(max_slots=a.max_slots, verify_every=a.verify_every)
+    wl = fx["config"]["workload"]["kv_bytes_per_token"]
+    scale = shape.kv_bytes_per_token / wl if isinstance(wl, int) else None
     ref_bytes = sum(s.ref_kv_bytes for s in rep.slots)
     out = {
         "fixture": os.path.basename(a.fixture), "shape": shape.name, "devices": len(devices),
-        "logical_gpus": len(ex.pools), "pool_blocks": nb, "slots": len(rep.slots),
+        "logical_gpus": len(ex.pools), "models": sorted({m for per in ex.pools.values() for m in per}),
+        "pool_blocks": nb, "slots": len(rep.slots),
         "executed_rows": rep.executed,
         "kv_moves": sum(s.kv_moves for s in rep.slots), "token_moves": sum(s.token_moves for s in rep.slots),
-        "bytes_moved": rep.bytes_moved, "ref_kv_bytes_scaled": int(ref_bytes * scale),
+        "bytes_moved": rep.bytes_moved, "tokens_moved": rep.tokens_moved,
+        "ref_kv_bytes": ref_bytes, "ref_kv_bytes_scaled": int(ref_bytes * scale) if scale else None,
         "execute_seconds": round(rep.migrate_seconds, 4),
         "verified_requests": rep.verified_requests, "recomputed_requests": rep.recomputed_requests,
         "fixture_sha": fx["plan_rows_sha256_16"],
