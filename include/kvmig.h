@@ -121,6 +121,31 @@ typedef struct kvm_reprefill_args {
   int32_t flags;          /* reserved, 0 */
 } kvm_reprefill_args;
 
+/* Paged-attention decode over a pool (the consumer of a migrated cache):
+ * for layers [layer0, layer0 + n_layers), requests b < batch and query heads
+ * qh < q_heads (kv head = qh / (q_heads / kv_heads)):
+ *   out[l][b][qh][:] = softmax_t(scale * q[l][b][qh] . K_t) . V_t,
+ *   t < seq_lens[b], K_t/V_t read through block_tables[b][t / 16].
+ * head_dim 128, 16-token blocks, q/out in the pool's 16-bit type
+ * (fp16, or bf16 with KVM_DECODE_BF16).  Split-K workspace is library-owned
+ * per device: calls on one device must be stream-ordered. */
+#define KVM_DECODE_BF16 0x1
+typedef struct kvm_decode_args {
+  int32_t pool;
+  int32_t layer0;
+  int32_t n_layers;
+  int32_t batch;
+  int32_t q_heads;
+  int32_t max_blocks;   /* row stride of block_tables */
+  int32_t max_seq_len;  /* >= every seq_lens[b]; sizes the split-K grid */
+  int32_t flags;
+  float scale;          /* usually 1/sqrt(head_dim) */
+  const void* q;        /* [n_layers][batch][q_heads][128] */
+  const int32_t* block_tables; /* [batch][max_blocks], device */
+  const int32_t* seq_lens;     /* [batch], device */
+  void* out;            /* [n_layers][batch][q_heads][128] */
+} kvm_decode_args;
+
 /* --- library / device ---------------------------------------------------- */
 int kvm_version(void);
 const char* kvm_last_error(void);
@@ -162,6 +187,8 @@ int kvm_compact(int pool, const int32_t* src_blocks, const int32_t* dst_blocks,
 int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream);
 /* tcgen05 re-prefill projection (see kvm_reprefill_args). */
 int kvm_reprefill(const kvm_reprefill_args* args, void* stream);
+/* Paged-attention decode reading the (migrated) block tables. */
+int kvm_paged_decode(const kvm_decode_args* args, void* stream);
 
 /* --- instrumentation -------------------------------------------------------- */
 /* Number of data-path kernels this process has launched through the ABI. */

@@ -36,8 +36,10 @@ EXPORTS = (
     "kvm_version", "kvm_last_error", "kvm_device_count", "kvm_init", "kvm_can_access_peer",
     "kvm_pool_register", "kvm_pool_unregister", "kvm_pool_piece_bytes", "kvm_pool_bytes",
     "kvm_ipc_export", "kvm_ipc_import", "kvm_ipc_close",
-    "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_launch_count",
+    "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_paged_decode",
+    "kvm_launch_count",
 )
+KVM_DECODE_BF16 = 0x1
 
 
 class PoolDesc(ctypes.Structure):
@@ -63,6 +65,14 @@ class ReprefillArgs(ctypes.Structure):
                 ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32)]
 
 
+class DecodeArgs(ctypes.Structure):
+    _fields_ = [("pool", ctypes.c_int32), ("layer0", ctypes.c_int32), ("n_layers", ctypes.c_int32),
+                ("batch", ctypes.c_int32), ("q_heads", ctypes.c_int32), ("max_blocks", ctypes.c_int32),
+                ("max_seq_len", ctypes.c_int32), ("flags", ctypes.c_int32), ("scale", ctypes.c_float),
+                ("q", ctypes.c_void_p), ("block_tables", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p),
+                ("out", ctypes.c_void_p)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -86,6 +96,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kvm_compact": ([I, P, P, I, P, I, P], I),
         "kvm_wait_flag": ([P, ctypes.c_uint32, P], I),
         "kvm_reprefill": ([ctypes.POINTER(ReprefillArgs), P], I),
+        "kvm_paged_decode": ([ctypes.POINTER(DecodeArgs), P], I),
         "kvm_launch_count": ([], I64),
     }
     for name, (args, res) in sig.items():

@@ -1,0 +1,71 @@
+"""Paged-attention decode over a KV pool (csrc/attention.cu, kvm_paged_decode).
+
+The consumer of a migrated cache: run on the destination with the block-table
+row the migration kernel rewrote, it must produce exactly what the source
+produced before the move.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import _native
+from .errors import ConfigError
+from .kvcache import KVPool
+
+
+def paged_decode(pool: KVPool, q, block_tables, seq_lens, out=None, *, layer0: int = 0,
+                 n_layers: int = None, max_seq_len: int = None, scale: float = None, stream=None):
+    """q: [n_layers][batch][q_heads][128] in the pool dtype; block_tables:
+    int32 [batch][max_blocks] (device); seq_lens: int32 [batch] (device).
+    Returns out (same shape as q)."""
+    import torch
+
+    n_layers = n_layers if n_layers is not None else q.shape[0]
+    if q.dim() != 4 or q.shape[0] != n_layers or q.shape[3] != pool.shape.head_dim:
+        raise ConfigError("q must be [n_layers][batch][q_heads][head_dim]")
+    if q.dtype != pool.dtype:
+        raise ConfigError("q must have the pool's dtype")
+    if block_tables.dtype != torch.int32 or seq_lens.dtype != torch.int32:
+        raise ValueError("block_tables and seq_lens must be int32")
+    if not (q.is_contiguous() and block_tables.is_contiguous()):
+        raise ValueError("q and block_tables must be contiguous")
+    batch, q_heads = q.shape[1], q.shape[2]
+    if out is None:
+        out = torch.empty_like(q)
+    if max_seq_len is None:
+        max_seq_len = int(seq_lens.max().item())
+    a = _native.DecodeArgs()
+    a.pool, a.layer0, a.n_layers, a.batch, a.q_heads = pool.pool_id, layer0, n_layers, batch, q_heads
+    a.max_blocks, a.max_seq_len = block_tables.shape[1], max(1, max_seq_len)
+    a.flags = _native.KVM_DECODE_BF16 if pool.dtype == torch.bfloat16 else 0
+    a.scale = scale if scale is not None else 1.0 / math.sqrt(pool.shape.head_dim)
+    a.q, a.block_tables, a.seq_lens, a.out = q.data_ptr(), block_tables.data_ptr(), seq_lens.data_ptr(), out.data_ptr()
+    s = stream if stream is not None else torch.cuda.current_stream(pool.device)
+    _native.check(_native.lib().kvm_paged_decode(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),
+                  "kvm_paged_decode")
+    return out
+
+
+def reference_decode(pool: KVPool, q, block_tables, seq_lens, layer0: int = 0, scale: float = None):
+    """fp32 torch reference (tests only): gather K/V through the tables."""
+    import torch
+
+    sh = pool.shape
+    scale = scale if scale is not None else 1.0 / math.sqrt(sh.head_dim)
+    L, B, Hq, D = q.shape
+    G = Hq // sh.kv_heads
+    out = torch.empty(L, B, Hq, D, dtype=torch.float32, device=q.device)
+    for l in range(L):
+        for b in range(B):
+            n = int(seq_lens[b])
+            t = torch.arange(n, device=q.device)
+            blk = block_tables[b].long()[t // sh.block_tokens]
+            K = pool.tensor[layer0 + l, 0, blk, t % sh.block_tokens].float()  # [n, Hkv, D]
+            V = pool.tensor[layer0 + l, 1, blk, t % sh.block_tokens].float()
+            Kq = K.repeat_interleave(G, dim=1)  # [n, Hq, D]
+            Vq = V.repeat_interleave(G, dim=1)
+            s = torch.einsum("hd,nhd->hn", q[l, b].float(), Kq) * scale
+            p = torch.softmax(s, dim=-1)
+            out[l, b] = torch.einsum("hn,nhd->hd", p, Vq)
+    return out

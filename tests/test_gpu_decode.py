@@ -1,0 +1,68 @@
+"""Paged-attention decode (the consumer of a migrated cache, §8f row 3):
+matches an fp32 torch reference within fp16/bf16 tolerance, and decoding on
+the destination after a migration is bit-identical to decoding on the source
+before it."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2501_06709_b200 import _native
+from paper_2501_06709_b200.attention import paged_decode, reference_decode
+from paper_2501_06709_b200.kvcache import BlockTable, KVPool, ModelShape
+
+pytestmark = pytest.mark.gpu
+
+
+def _fill_normal(pool, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    pool.tensor.copy_(torch.randn(pool.view_shape, generator=g, device="cuda").to(pool.dtype))
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("kv_heads,q_heads,seqs", [(4, 4, [1, 17, 300]), (2, 4, [256, 5]), (2, 16, [700]),
+                                                   (1, 8, [4096, 1, 33])])
+def test_decode_matches_reference(dtype, kv_heads, q_heads, seqs):
+    shape = ModelShape("dec", layers=2, kv_heads=kv_heads, head_dim=128, q_heads=q_heads, d_model=256)
+    nb = sum((s + 15) // 16 for s in seqs) + 8
+    pool = KVPool(shape, nb, dtype=dtype)
+    _fill_normal(pool, 1)
+    maxb = max((s + 15) // 16 for s in seqs)
+    perm = torch.randperm(nb, generator=torch.Generator().manual_seed(2))
+    tables = torch.full((len(seqs), maxb), -1, dtype=torch.int32)
+    off = 0
+    for b, s in enumerate(seqs):
+        k = (s + 15) // 16
+        tables[b, :k] = perm[off:off + k].to(torch.int32)
+        off += k
+    tables = tables.cuda()
+    lens = torch.tensor(seqs, dtype=torch.int32, device="cuda")
+    q = torch.randn(2, len(seqs), q_heads, 128, device="cuda").to(dtype)
+    out = paged_decode(pool, q, tables, lens)
+    ref = reference_decode(pool, q, tables, lens)
+    torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
+
+
+def test_decode_after_migration_is_bit_identical():
+    shape = ModelShape("dec", layers=3, kv_heads=8, head_dim=128, q_heads=8, d_model=256)
+    nb = 96
+    src, dst = KVPool(shape, nb), KVPool(shape, nb)
+    _fill_normal(src, 3)
+    _fill_normal(dst, 4)
+    seq = 700
+    n = (seq + 15) // 16
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(5))[:n].to(torch.int32).numpy()
+    db = dst.allocator.alloc(n)
+    table = BlockTable(2, n)
+    m = _native.Move()
+    m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, n, 1
+    m.src_blocks, m.dst_blocks, m.dst_table_row = sb.ctypes.data, db.ctypes.data, table.row_ptr(0)
+    _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    q = torch.randn(3, 1, 8, 128, device="cuda").half()
+    lens = torch.tensor([seq], dtype=torch.int32, device="cuda")
+    before = paged_decode(src, q, torch.from_numpy(sb)[None].cuda(), lens)
+    after = paged_decode(dst, q, table.rows[table.slot(0)][None].contiguous(), lens)   # the rewritten row
+    torch.cuda.synchronize()
+    assert torch.equal(before.view(torch.int16), after.view(torch.int16))
