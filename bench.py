@@ -259,7 +259,10 @@ def run_ours(args) -> int:
     pool.allocator.take(np.flatnonzero(used))
     db_np = pool.allocator.alloc(n)          # blocks this rank RECEIVES into
     table = BlockTable(4, n, device=device)
-    mailbox = torch.zeros(64, dtype=torch.int32, device=f"cuda:{device}")   # done flags
+    # one control allocation per rank, exported once: [0, 64) done flags, [64, 64 + n) the block-table
+    # row the incoming transfer rewrites (N > 1)
+    ctrl = torch.zeros(64 + n, dtype=torch.int32, device=f"cuda:{device}")
+    mailbox, rowbuf = ctrl[:64], ctrl[64:]
     stream = torch.cuda.Stream(device=device)
     sptr = ctypes.c_void_p(stream.cuda_stream)
 
@@ -273,22 +276,15 @@ def run_ours(args) -> int:
         from paper_2501_06709_b200 import kvcache as kvc
         hb = (ctypes.c_ubyte * 64)()
         ob = ctypes.c_int64()
-        _native.check(lib.kvm_ipc_export(ctypes.c_void_p(mailbox.data_ptr()), hb, ctypes.byref(ob)))
-        htab = (ctypes.c_ubyte * 64)()
-        otab = ctypes.c_int64()
-        _native.check(lib.kvm_ipc_export(ctypes.c_void_p(table.rows.data_ptr()), htab, ctypes.byref(otab)))
-        info = exchange_objects((h_pool, o_pool, bytes(hb), ob.value, bytes(htab), otab.value,
-                                 db_np.tolist()))
+        _native.check(lib.kvm_ipc_export(ctypes.c_void_p(ctrl.data_ptr()), hb, ctypes.byref(ob)))
+        info = exchange_objects((h_pool, o_pool, bytes(hb), ob.value, db_np.tolist()))
         peer = info[ri.send_to]
         dst_pool = kvc.KVPool.from_ipc(shape, nb, device, peer[0], peer[1])
         mb = ctypes.c_void_p()
         _native.check(lib.kvm_ipc_import(device, (ctypes.c_ubyte * 64).from_buffer_copy(peer[2]), peer[3],
                                          ctypes.byref(mb)))
-        tb = ctypes.c_void_p()
-        _native.check(lib.kvm_ipc_import(device, (ctypes.c_ubyte * 64).from_buffer_copy(peer[4]), peer[5],
-                                         ctypes.byref(tb)))
-        peer_flag, peer_row = mb.value, tb.value
-        peer_db = np.asarray(peer[6], dtype=np.int32)
+        peer_flag, peer_row = mb.value, mb.value + 64 * 4
+        peer_db = np.asarray(peer[4], dtype=np.int32)
     else:
         dst_pool, peer_flag, peer_row, peer_db = pool, mailbox.data_ptr(), table.row_ptr(0), db_np
 
@@ -338,8 +334,7 @@ def run_ours(args) -> int:
         ok = got == sent
     else:   # what this rank received must equal what recv_from sent
         sums = exchange_objects(sent)
-        ok = got == sums[ri.recv_from] and bool(torch.equal(table.rows[0, :n].cpu(),
-                                                              torch.from_numpy(db_np)))
+        ok = got == sums[ri.recv_from] and bool(torch.equal(rowbuf.cpu(), torch.from_numpy(db_np)))
     bit_exact = allreduce_max(0.0 if ok else 1.0, device) == 0.0
     seq[0] = 0
     mailbox.zero_()
@@ -410,7 +405,7 @@ def run_ours(args) -> int:
             with torch.cuda.stream(stream):
                 step(i, host=True)
             stream.synchronize()
-            row = table.rows[0, :n].cpu()
+            row = rowbuf.cpu()                  # D2H: the block-table row the incoming kernel rewrote
         torch.cuda.synchronize()
         e2e_s = allreduce_max(time.perf_counter() - t0, device)
         barrier()
@@ -461,7 +456,10 @@ def run_ours(args) -> int:
             "data": "synthetic (seeded random KV bits, NaN payloads included)",
             "config": {"workload": (f"{args.workload} intra-GPU migration (compaction into fresh blocks of the "
                                     f"same pool)" if world == 1 else
-                                    f"{args.workload} ring push i->(i+1) mod {world} over NVLink (CUDA IPC)"),
+                                    (f"{args.workload} ring push i->(i+1) mod {world} over NVLink (CUDA IPC)"
+                                     if ndev >= world else
+                                     f"{args.workload} ring push i->(i+1) mod {world}, ranks sharing "
+                                     f"{ndev} GPU (CUDA IPC test mode, no NVLink hop)")),
                        "baseline_config": cfg_desc, "kv_bytes_per_rank_per_step": kv_bytes, "blocks": n,
                        "pool_blocks": nb, "engine": args.engine, "l2_evict_first": bool(args.l2_evict_first),
                        "l2": "inputs larger than L2 (%.1f GiB per step per rank)" % (kv_bytes / 2 ** 30),
