@@ -146,6 +146,50 @@ typedef struct kvm_decode_args {
   void* out;            /* [n_layers][batch][q_heads][128] */
 } kvm_decode_args;
 
+/* Native planner (kvm_plan_hybrid): the reference's plan_hybrid
+ * (migration.py:128-170), bit-identical decisions and float64 ledgers. */
+#define KVM_MODE_KV_TRANSFER 0
+#define KVM_MODE_TOKEN_TRANSFER 1
+#define KVM_MODE_DEFERRED 2
+#define KVM_MODE_FORCED_KV_TRANSFER 3
+typedef struct kvm_pending {   /* PendingMove (migration.py:94-102) + its defer count */
+  int64_t item;
+  int64_t src;
+  int64_t dst;
+  int64_t kv_bytes;
+  int64_t tokens;
+  int64_t defer_count;
+} kvm_pending;
+typedef struct kvm_plan_params {  /* Topology (migration.py:25-58) + Boundaries (:61-74) */
+  int32_t gpus_per_machine;
+  int32_t max_defer;
+  double intra_bandwidth;
+  double inter_bandwidth;
+  double prefill_tokens_per_s;
+  double comp_budget;
+  double intra_comm_budget;
+  double inter_comm_budget;
+  int32_t n_overrides;            /* Boundaries.comm_budget entries */
+  int32_t _pad;
+  const int64_t* override_link;   /* machine id for ("intra", m), -1 for ("inter",) */
+  const double* override_budget;
+} kvm_plan_params;
+typedef struct kvm_planned {      /* PlannedMove, in consensus order */
+  int32_t index;                  /* into the input array */
+  int32_t mode;                   /* KVM_MODE_* */
+  double latency_s;
+} kvm_planned;
+typedef struct kvm_plan_ledgers { /* MigrationPlan.link_bytes / dest_tokens, first-use order */
+  int32_t capacity;               /* entries available in each array (>= n is always enough) */
+  int32_t n_links;
+  int32_t n_dests;
+  int32_t _pad;
+  int64_t* link_key;
+  double* link_used;
+  int64_t* dest_key;
+  double* dest_used;
+} kvm_plan_ledgers;
+
 /* --- library / device ---------------------------------------------------- */
 int kvm_version(void);
 const char* kvm_last_error(void);
@@ -189,6 +233,11 @@ int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream);
 int kvm_reprefill(const kvm_reprefill_args* args, void* stream);
 /* Paged-attention decode reading the (migrated) block tables. */
 int kvm_paged_decode(const kvm_decode_args* args, void* stream);
+
+/* --- control plane ------------------------------------------------------------ */
+/* plan_hybrid on the host CPU (no GPU needed); out has n entries; ledgers may be NULL. */
+int kvm_plan_hybrid(const kvm_pending* moves, int n, const kvm_plan_params* params, kvm_planned* out,
+                    kvm_plan_ledgers* ledgers);
 
 /* --- instrumentation -------------------------------------------------------- */
 /* Number of data-path kernels this process has launched through the ABI. */

@@ -37,7 +37,7 @@ EXPORTS = (
     "kvm_pool_register", "kvm_pool_unregister", "kvm_pool_piece_bytes", "kvm_pool_bytes",
     "kvm_ipc_export", "kvm_ipc_import", "kvm_ipc_close",
     "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_paged_decode",
-    "kvm_launch_count",
+    "kvm_plan_hybrid", "kvm_launch_count",
 )
 KVM_DECODE_BF16 = 0x1
 
@@ -73,6 +73,29 @@ class DecodeArgs(ctypes.Structure):
                 ("out", ctypes.c_void_p)]
 
 
+class Pending(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in ("item", "src", "dst", "kv_bytes", "tokens", "defer_count")]
+
+
+class PlanParams(ctypes.Structure):
+    _fields_ = [("gpus_per_machine", ctypes.c_int32), ("max_defer", ctypes.c_int32),
+                ("intra_bandwidth", ctypes.c_double), ("inter_bandwidth", ctypes.c_double),
+                ("prefill_tokens_per_s", ctypes.c_double), ("comp_budget", ctypes.c_double),
+                ("intra_comm_budget", ctypes.c_double), ("inter_comm_budget", ctypes.c_double),
+                ("n_overrides", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("override_link", ctypes.c_void_p), ("override_budget", ctypes.c_void_p)]
+
+
+class Planned(ctypes.Structure):
+    _fields_ = [("index", ctypes.c_int32), ("mode", ctypes.c_int32), ("latency_s", ctypes.c_double)]
+
+
+class PlanLedgers(ctypes.Structure):
+    _fields_ = [("capacity", ctypes.c_int32), ("n_links", ctypes.c_int32), ("n_dests", ctypes.c_int32),
+                ("_pad", ctypes.c_int32), ("link_key", ctypes.c_void_p), ("link_used", ctypes.c_void_p),
+                ("dest_key", ctypes.c_void_p), ("dest_used", ctypes.c_void_p)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -97,6 +120,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "kvm_wait_flag": ([P, ctypes.c_uint32, P], I),
         "kvm_reprefill": ([ctypes.POINTER(ReprefillArgs), P], I),
         "kvm_paged_decode": ([ctypes.POINTER(DecodeArgs), P], I),
+        "kvm_plan_hybrid": ([ctypes.POINTER(Pending), I, ctypes.POINTER(PlanParams), ctypes.POINTER(Planned),
+                             ctypes.POINTER(PlanLedgers)], I),
         "kvm_launch_count": ([], I64),
     }
     for name, (args, res) in sig.items():
