@@ -130,6 +130,8 @@ typedef struct kvm_reprefill_args {
  * (fp16, or bf16 with KVM_DECODE_BF16).  Split-K workspace is library-owned
  * per device: calls on one device must be stream-ordered. */
 #define KVM_DECODE_BF16 0x1
+#define KVM_DECODE_CUDA_CORES 0x2 /* force the CUDA-core path (G in {1,2,4,8});
+                                     default: tensor-core mma path for G <= 8 */
 typedef struct kvm_decode_args {
   int32_t pool;
   int32_t layer0;

@@ -40,6 +40,7 @@ EXPORTS = (
     "kvm_plan_hybrid", "kvm_launch_count",
 )
 KVM_DECODE_BF16 = 0x1
+KVM_DECODE_CUDA_CORES = 0x2
 
 
 class PoolDesc(ctypes.Structure):

@@ -15,10 +15,12 @@ from .kvcache import KVPool
 
 
 def paged_decode(pool: KVPool, q, block_tables, seq_lens, out=None, *, layer0: int = 0,
-                 n_layers: int = None, max_seq_len: int = None, scale: float = None, stream=None):
+                 n_layers: int = None, max_seq_len: int = None, scale: float = None, stream=None,
+                 cuda_cores: bool = False):
     """q: [n_layers][batch][q_heads][128] in the pool dtype; block_tables:
     int32 [batch][max_blocks] (device); seq_lens: int32 [batch] (device).
-    Returns out (same shape as q)."""
+    Runs on tensor cores (mma.sync, cp.async-staged tiles) for up to 8 query
+    heads per kv head, unless cuda_cores=True.  Returns out (same shape as q)."""
     import torch
 
     n_layers = n_layers if n_layers is not None else q.shape[0]
@@ -38,7 +40,8 @@ def paged_decode(pool: KVPool, q, block_tables, seq_lens, out=None, *, layer0: i
     a = _native.DecodeArgs()
     a.pool, a.layer0, a.n_layers, a.batch, a.q_heads = pool.pool_id, layer0, n_layers, batch, q_heads
     a.max_blocks, a.max_seq_len = block_tables.shape[1], max(1, max_seq_len)
-    a.flags = _native.KVM_DECODE_BF16 if pool.dtype == torch.bfloat16 else 0
+    a.flags = (_native.KVM_DECODE_BF16 if pool.dtype == torch.bfloat16 else 0) | (
+        _native.KVM_DECODE_CUDA_CORES if cuda_cores else 0)
     a.scale = scale if scale is not None else 1.0 / math.sqrt(pool.shape.head_dim)
     a.q, a.block_tables, a.seq_lens, a.out = q.data_ptr(), block_tables.data_ptr(), seq_lens.data_ptr(), out.data_ptr()
     s = stream if stream is not None else torch.cuda.current_stream(pool.device)

@@ -9,7 +9,9 @@
 //     out[l,b,qh] = sum_t softmax(s)_t * V[l][blocks_b[t/16]][t%16][h]
 //
 // Flash-decoding split-K: CTA = (split, kv head, layer*batch+b), 4 warps; warp
-// w streams blocks w, w+4, ... of the split.  Within a warp, lanes 0-15 take
+// w streams blocks w, w+4, ... of the split.  Default path (any G <= 8):
+// tensor cores, decode_gqa_kernel below.  CUDA-core path (KVM_DECODE_CUDA_CORES,
+// G in {1,2,4,8}): within a warp, lanes 0-15 take
 // even tokens and lanes 16-31 odd tokens of a block, each lane holding 8 of
 // the 128 dims (one 16-byte vector of the token's K/V row, so a warp load is
 // two coalesced 256-byte rows).  All 16 K and V vectors of a block are loaded
@@ -23,10 +25,12 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "kvmig_common.cuh"
 
@@ -35,7 +39,7 @@ namespace att {
 
 constexpr int D = 128;           // head_dim supported by this kernel
 constexpr int WARPS = 4;
-constexpr int BLOCKS_PER_SPLIT = 16;
+constexpr int BLOCKS_PER_SPLIT_DEFAULT = 16;
 
 struct Params {
   const uint8_t* pool;
@@ -46,7 +50,7 @@ struct Params {
   float* ws_ml;   // [lb][q_heads][splits][2]  (m in log2 units, l)
   float* ws_acc;  // [lb][q_heads][splits][D]
   int64_t plane_bytes, piece_bytes, tok_stride;  // tok_stride = kv_heads * D * 2
-  int32_t layer0, n_layers, batch, q_heads, kv_heads, max_blocks, splits, num_blocks;
+  int32_t layer0, n_layers, batch, q_heads, kv_heads, max_blocks, splits, num_blocks, bps;
   float scale_log2;  // scale * log2(e)
 };
 
@@ -66,8 +70,8 @@ __global__ void __launch_bounds__(WARPS * 32) decode_split_kernel(const __grid_c
   const int half = lane >> 4, c = lane & 15;
   const int seq = __ldg(p.seq_lens + b);
   const int nblk = (seq + 15) >> 4;
-  const int blk_lo = split * BLOCKS_PER_SPLIT;
-  const int blk_hi = min(nblk, blk_lo + BLOCKS_PER_SPLIT);
+  const int blk_lo = split * p.bps;
+  const int blk_hi = min(nblk, blk_lo + p.bps);
 
   __shared__ float s_m[WARPS][G], s_l[WARPS][G];
   __shared__ float s_acc[WARPS][G][D];
@@ -185,6 +189,242 @@ __global__ void __launch_bounds__(WARPS * 32) decode_split_kernel(const __grid_c
   }
 }
 
+// ---------------------------------------------------------------------------
+// Grouped-query path (G = q_heads / kv_heads in 2..8): tensor cores.
+// Per warp and 16-token block:  S[16 tok x 8 heads] = K[16 x 128] . Q^T   (8 x mma.m16n8k16)
+//                                O^T[128 x 8] += V^T[128 x 16] . P[16 x 8] (8 x mma.m16n8k16)
+// K and V tiles (16 tokens x 256 B) are staged per warp with 16-byte cp.async
+// into XOR-swizzled, double-buffered shared memory (the next block streams in
+// while this one is multiplied); fragments come from ldmatrix (K) and
+// ldmatrix.trans (V^T); P is transposed in registers with movmatrix.
+// Heads G..7 of the n=8 MMA are zero-padded.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, const uint32_t* b);
+template <>
+__device__ __forceinline__ void mma16816<__half>(float* c, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+template <>
+__device__ __forceinline__ void mma16816<__nv_bfloat16>(float* c, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// smem tile of one 16-token block for one kv head: [16 rows][16 chunks of 16 B],
+// chunk index XOR-swizzled with (row & 7) so ldmatrix row fetches are conflict-free
+__device__ __forceinline__ uint32_t tile_off(int row, int chunk) {
+  return (uint32_t)(row * 256 + ((chunk ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, uint32_t saddr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, uint32_t saddr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr));
+}
+
+constexpr int GQA_TILE = 16 * 256;                  // bytes of K (or V) per block and kv head
+constexpr int GQA_WARP_SMEM = 2 /*buffers*/ * 2 /*K,V*/ * GQA_TILE;
+constexpr int GQA_SMEM = WARPS * GQA_WARP_SMEM;     // 64 KiB (the merge area aliases it)
+
+template <typename T>
+__global__ void __launch_bounds__(WARPS * 32) decode_gqa_kernel(const __grid_constant__ Params p, int G) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  const int split = blockIdx.x, h = blockIdx.y, lb = blockIdx.z;
+  const int layer_rel = lb / p.batch, b = lb - layer_rel * p.batch;
+  const int layer = p.layer0 + layer_rel;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int seq = __ldg(p.seq_lens + b);
+  const int nblk = (seq + 15) >> 4;
+  const int blk_lo = split * p.bps;
+  const int blk_hi = min(nblk, blk_lo + p.bps);
+  const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(gsm) + warp * GQA_WARP_SMEM;
+
+  // Q^T fragments (B operand of S = K Q^T): head g, dims 16kk + 2t (+8); heads >= G are zero
+  uint32_t qf[8][2];
+  {
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(
+        static_cast<const T*>(p.q) + ((int64_t)lb * p.q_heads + h * G + min(g, G - 1)) * D);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      qf[kk][0] = g < G ? __ldg(qrow + kk * 8 + t) : 0u;
+      qf[kk][1] = g < G ? __ldg(qrow + kk * 8 + 4 + t) : 0u;
+    }
+  }
+  float m[2] = {-CUDART_INF_F, -CUDART_INF_F}, l[2] = {0.f, 0.f};
+  float o[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+
+  const int32_t* table = p.tables + (int64_t)b * p.max_blocks;
+  const uint8_t* kplane = p.pool + ((int64_t)layer * 2 + 0) * p.plane_bytes + (int64_t)h * D * 2;
+  const uint8_t* vplane = kplane + p.plane_bytes;
+
+  // stage block `blk` (K and V rows of kv head h) into buffer `buf`: 16 B per lane per step,
+  // consecutive lanes on consecutive chunks of a row (two 256 B rows per warp instruction)
+  auto stage = [&](int blk, int buf) {
+    const int64_t pb = __ldg(table + blk);
+    const int ntok = min(16, seq - blk * 16);
+    const uint8_t* kb = kplane + pb * p.piece_bytes;
+    const uint8_t* vb = vplane + pb * p.piece_bytes;
+    const uint32_t ks = wbase + buf * 2 * GQA_TILE, vs = ks + GQA_TILE;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int c = i * 32 + lane, row = c >> 4, ch = c & 15;
+      const bool ok = row < ntok;
+      const int64_t go = (int64_t)(ok ? row : 0) * p.tok_stride + ch * 16;
+      cp_async16(ks + tile_off(row, ch), kb + go, ok);
+      cp_async16(vs + tile_off(row, ch), vb + go, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  int buf = 0;
+  if (blk_lo + warp < blk_hi) stage(blk_lo + warp, 0);
+  for (int blk = blk_lo + warp; blk < blk_hi; blk += WARPS) {
+    const int nxt = blk + WARPS;
+    if (nxt < blk_hi) {
+      stage(nxt, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    const int ntok = min(16, seq - blk * 16);
+    const bool r0 = g < ntok, r1 = g + 8 < ntok;
+    const uint32_t ks = wbase + buf * 2 * GQA_TILE, vs = ks + GQA_TILE;
+    // S = K Q^T: A fragments straight from the K tile (lane -> matrix lane/8, row lane%8)
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int mi = lane >> 3, mr = lane & 7;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t af[4];
+      ldsm_x4(af, ks + tile_off(mr + 8 * (mi & 1), 2 * kk + (mi >> 1)));
+      mma16816<T>(sc, af, qf[kk]);
+    }
+    sc[0] = r0 ? sc[0] * p.scale_log2 : -CUDART_INF_F;
+    sc[1] = r0 ? sc[1] * p.scale_log2 : -CUDART_INF_F;
+    sc[2] = r1 ? sc[2] * p.scale_log2 : -CUDART_INF_F;
+    sc[3] = r1 ? sc[3] * p.scale_log2 : -CUDART_INF_F;
+    float pr[4];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {  // head 2t + hh: column hh of the C fragment
+      float mx = fmaxf(sc[hh], sc[hh + 2]);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const float mn = fmaxf(m[hh], mx);  // finite: every block has >= 1 valid token
+      const float corr = exp2f(m[hh] - mn);
+      pr[hh] = exp2f(sc[hh] - mn);
+      pr[hh + 2] = exp2f(sc[hh + 2] - mn);
+      l[hh] = l[hh] * corr + pr[hh] + pr[hh + 2];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[j][hh] *= corr;
+        o[j][hh + 2] *= corr;
+      }
+      m[hh] = mn;
+    }
+    // P as the B operand: transpose the C-layout 8x8 blocks (tokens 0-7, 8-15)
+    uint32_t pf[2] = {movtrans(pack2<T>(pr[0], pr[1])), movtrans(pack2<T>(pr[2], pr[3]))};
+    // O^T += V^T P: A = V^T via ldmatrix.trans of the V tile
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t af[4];
+      ldsm_x4_t(af, vs + tile_off(mr + 8 * (mi >> 1), 2 * j + (mi & 1)));
+      mma16816<T>(o[j], af, pf);
+    }
+    __syncwarp();
+    buf ^= 1;
+  }
+  // l: sum the per-lane partials over the 8 token rows (lanes with equal t)
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 4);
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 8);
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 16);
+  }
+  __syncthreads();  // tiles are dead: reuse the staging smem for the cross-warp merge
+  float* s_m = reinterpret_cast<float*>(gsm);          // [WARPS][8]
+  float* s_l = s_m + WARPS * 8;                         // [WARPS][8]
+  float* s_o = s_l + WARPS * 8;                         // [WARPS][8][D]
+  // O^T fragment: o[j] = O^T[16j+g][2t], [16j+g][2t+1], [16j+g+8][2t], [16j+g+8][2t+1]
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    s_o[(warp * 8 + 2 * t) * D + 16 * j + g] = o[j][0];
+    s_o[(warp * 8 + 2 * t + 1) * D + 16 * j + g] = o[j][1];
+    s_o[(warp * 8 + 2 * t) * D + 16 * j + g + 8] = o[j][2];
+    s_o[(warp * 8 + 2 * t + 1) * D + 16 * j + g + 8] = o[j][3];
+  }
+  if (g == 0) {
+    s_m[warp * 8 + 2 * t] = m[0];
+    s_m[warp * 8 + 2 * t + 1] = m[1];
+    s_l[warp * 8 + 2 * t] = l[0];
+    s_l[warp * 8 + 2 * t + 1] = l[1];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * D; idx += WARPS * 32) {
+    const int hq = idx / D, d = idx - hq * D;
+    float M = -CUDART_INF_F;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, s_m[w * 8 + hq]);
+    float L = 0.f, A = 0.f;
+    if (M != -CUDART_INF_F) {
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        const float e = exp2f(s_m[w * 8 + hq] - M);
+        L += s_l[w * 8 + hq] * e;
+        A += s_o[(w * 8 + hq) * D + d] * e;
+      }
+    }
+    const int qh = h * G + hq;
+    if (p.splits == 1) {
+      T* out = static_cast<T*>(p.out) + ((int64_t)lb * p.q_heads + qh) * D + d;
+      *out = static_cast<T>(L > 0.f ? A / L : 0.f);
+    } else {
+      const int64_t slot = ((int64_t)lb * p.q_heads + qh) * p.splits + split;
+      p.ws_acc[slot * D + d] = A;
+      if (d == 0) {
+        p.ws_ml[slot * 2 + 0] = M;
+        p.ws_ml[slot * 2 + 1] = L;
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(D) decode_combine_kernel(const __grid_constant__ Params p) {
   const int qh = blockIdx.x, lb = blockIdx.y, d = threadIdx.x;
@@ -225,7 +465,29 @@ static int launch_g(const Params& p, cudaStream_t st) {
 }
 
 template <typename T>
-static int launch_t(const Params& p, int G, cudaStream_t st) {
+static int launch_gqa(const Params& p, int G, cudaStream_t st) {
+  static bool attr[2] = {false, false};
+  const int ti = sizeof(T) == 2 && std::is_same<T, __half>::value ? 0 : 1;
+  if (!attr[ti]) {
+    KVM_CUDA_TRY(cudaFuncSetAttribute(decode_gqa_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, GQA_SMEM));
+    attr[ti] = true;
+  }
+  dim3 grid(p.splits, p.kv_heads, p.n_layers * p.batch);
+  decode_gqa_kernel<T><<<grid, WARPS * 32, GQA_SMEM, st>>>(p, G);
+  KVM_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  if (p.splits > 1) {
+    dim3 g2(p.q_heads, p.n_layers * p.batch);
+    decode_combine_kernel<T><<<g2, D, 0, st>>>(p);
+    KVM_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  }
+  return KVM_OK;
+}
+
+template <typename T>
+static int launch_t(const Params& p, int G, cudaStream_t st, bool tensor_path) {
+  if (tensor_path && G >= 1 && G <= 8) return launch_gqa<T>(p, G, st);
   switch (G) {
     case 1: return launch_g<T, 1>(p, st);
     case 2: return launch_g<T, 2>(p, st);
@@ -271,7 +533,26 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
   p.kv_heads = d.kv_heads;
   p.max_blocks = a->max_blocks;
   p.num_blocks = d.num_blocks;
-  p.splits = (a->max_seq_len + 16 * BLOCKS_PER_SPLIT - 1) / (16 * BLOCKS_PER_SPLIT);
+  {
+    static int env_bps = -1;
+    if (env_bps < 0) {
+      const char* e = getenv("KVM_DECODE_BLOCKS_PER_SPLIT");  // tuning knob
+      env_bps = e ? std::max(1, atoi(e)) : 0;
+    }
+    if (env_bps) {
+      p.bps = env_bps;
+    } else {
+      // long splits amortise the per-CTA merge; keep >= ~3 CTAs per SM of work
+      const int64_t items = (int64_t)d.kv_heads * a->n_layers * a->batch;
+      const int max_blk = (a->max_seq_len + 15) / 16;
+      int bps = 64;
+      while (bps > BLOCKS_PER_SPLIT_DEFAULT / 2 &&
+             items * ((max_blk + bps - 1) / bps) < 3LL * sm_count(pool->device))
+        bps /= 2;
+      p.bps = bps;
+    }
+  }
+  p.splits = (a->max_seq_len + 16 * p.bps - 1) / (16 * p.bps);
   p.scale_log2 = a->scale * 1.4426950408889634f;
   p.ws_ml = nullptr;
   p.ws_acc = nullptr;
@@ -294,13 +575,12 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
     }
     p.ws_acc = w.ptr;
     p.ws_ml = w.ptr + slots * D;
-    if (!rc)
-      rc = (a->flags & KVM_DECODE_BF16) ? launch_t<__nv_bfloat16>(p, G, static_cast<cudaStream_t>(stream))
-                                        : launch_t<__half>(p, G, static_cast<cudaStream_t>(stream));
-  } else {
-    rc = (a->flags & KVM_DECODE_BF16) ? launch_t<__nv_bfloat16>(p, G, static_cast<cudaStream_t>(stream))
-                                      : launch_t<__half>(p, G, static_cast<cudaStream_t>(stream));
   }
+  const bool tensor_path = !(a->flags & KVM_DECODE_CUDA_CORES);
+  if (!rc)
+    rc = (a->flags & KVM_DECODE_BF16)
+             ? launch_t<__nv_bfloat16>(p, G, static_cast<cudaStream_t>(stream), tensor_path)
+             : launch_t<__half>(p, G, static_cast<cudaStream_t>(stream), tensor_path);
   if (cur != pool->device) cudaSetDevice(cur);
   return rc;
 }
