@@ -490,7 +490,9 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="7b-4k")
-    ap.add_argument("--engine", choices=["ldg", "bulk"], default="bulk")
+    ap.add_argument("--engine", choices=["ldg", "bulk"], default=None,
+                    help="copy engine; default bulk (TMA) for local HBM at N=1, ldg (128-bit peer "
+                         "stores, the proven NVLink pattern) for N>1")
     ap.add_argument("--l2-evict-first", type=int, choices=[0, 1], default=0,
                     help="stream KV through L2 with an evict-first policy (KVM_F_L2_EVICT_FIRST)")
     ap.add_argument("--cpu-budget-s", type=float, default=8.0)
@@ -500,6 +502,8 @@ def main(argv=None) -> int:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
         return run_reference(args)
+    if args.engine is None:
+        args.engine = "bulk" if int(os.environ.get("WORLD_SIZE", args.gpus)) == 1 else "ldg"
     return run_ours(args)
 
 
