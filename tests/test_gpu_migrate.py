@@ -244,3 +244,51 @@ def test_executor_plan_roundtrip():
     assert pools[0].allocator.n_free == 64
     rec = ex.compact(10)
     assert rec.bytes_moved == 4 * 16 * bpt
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_randomized_batches_vs_oracle(seed):
+    """Random shapes (piece sizes from 1 KiB to 160 KiB, odd head counts), random
+    pools and block lists, several moves of DIFFERENT shapes in one kvm_migrate
+    batch (one launch), random engine / block-list placement / flags."""
+    rng = np.random.default_rng(1000 + seed)
+    shapes = []
+    for k in range(int(rng.integers(1, 4))):
+        shapes.append(ModelShape(f"r{seed}_{k}", layers=int(rng.integers(1, 5)), kv_heads=int(rng.integers(1, 9)),
+                                 head_dim=int(rng.choice([8, 64, 128])), q_heads=1, d_model=64))
+    pools = []
+    for sh in shapes:
+        nb = int(rng.integers(8, 40))
+        src, dst = KVPool(sh, nb), KVPool(sh, nb)
+        _fill(src, int(rng.integers(1 << 30)))
+        _fill(dst, int(rng.integers(1 << 30)))
+        pools.append((src, dst))
+    engine = int(rng.choice([0, _native.KVM_F_ENGINE_BULK]))
+    host = bool(rng.integers(2))
+    moves, keep, checks = [], [], []
+    flags = torch.zeros(16, dtype=torch.int32, device="cuda")
+    for i in range(int(rng.integers(1, 9))):
+        src, dst = pools[int(rng.integers(len(pools)))]
+        free = np.flatnonzero(dst.allocator.free_mask())
+        n = int(rng.integers(0, min(len(free), src.num_blocks) + 1))
+        sb = rng.permutation(src.num_blocks)[:n].astype(np.int32)
+        db = dst.allocator.alloc(n)
+        if host:
+            keep += [sb, db]
+            m = _move(src, dst, sb, db, flag=flags[i:].data_ptr(), value=i + 1)
+        else:
+            sbd, dbd = torch.from_numpy(sb).cuda(), torch.from_numpy(db).cuda()
+            keep += [sbd, dbd]
+            m = _move(src, dst, sbd.data_ptr(), dbd.data_ptr(), flag=flags[i:].data_ptr(), value=i + 1, n=n)
+        moves.append(m)
+        checks.append((src, dst, sb, db))
+    expect = {}
+    for src, dst, sb, db in checks:  # oracle applies the moves in order on host copies
+        key = id(dst)
+        if key not in expect:
+            expect[key] = (dst, dst.tensor.view(torch.int16).cpu().numpy())
+        orc.migrate(src.tensor.view(torch.int16).cpu().numpy(), _desc(src), expect[key][1], _desc(dst), sb, db)
+    _run(moves, engine | (_native.KVM_F_BLOCKS_ON_HOST if host else 0))
+    for dst, exp in expect.values():
+        assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
+    assert flags[:len(moves)].cpu().tolist() == list(range(1, len(moves) + 1))
