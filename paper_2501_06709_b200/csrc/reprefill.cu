@@ -366,13 +366,13 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
     return fail(KVM_ERR_INVALID, "rows/d_model/q_cols/tok0 out of range");
   if (a->d_model % BK) return fail(KVM_ERR_CONFIG, "d_model must be a multiple of 64");
   if (kvd % 32 || a->q_cols % 32) return fail(KVM_ERR_CONFIG, "kv_heads*head_dim and q_cols must be multiples of 32");
+  if (a->rows == 0) return KVM_OK;  // nothing to recompute
   if (!a->x || !a->w || !a->dst_blocks) return fail(KVM_ERR_INVALID, "NULL x/w/dst_blocks");
   if ((int64_t)(a->tok0 + a->rows) > (int64_t)a->n_dst_blocks * d.block_tokens)
     return fail(KVM_ERR_INVALID, "dst_blocks do not cover tok0 + rows tokens");
   if (a->flags != 0) return fail(KVM_ERR_INVALID, "flags must be 0");
   if (reinterpret_cast<uintptr_t>(a->x) % 16 || reinterpret_cast<uintptr_t>(a->w) % 16)
     return fail(KVM_ERR_INVALID, "x and w must be 16-byte aligned");
-  if (a->rows == 0) return KVM_OK;
   EncodeTiled enc = encode_fn();
   if (!enc) return fail(KVM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
 

@@ -1,0 +1,78 @@
+"""CPU-only error behaviour of the host objects (no GPU): the reference's
+exception classes for the reference's kinds of misuse (errors.py:4-32)."""
+import numpy as np
+import pytest
+
+from paper_2501_06709_b200 import ConfigError, KvPackError, NotPlaced, RequestTooLarge
+from paper_2501_06709_b200.kvcache import BlockAllocator, ModelShape
+from paper_2501_06709_b200.planner import KV_TRANSFER, TOKEN_TRANSFER, PendingMove, PlannedMove
+from test_replay_cpu import MINI, HostExecutor, HostPool
+
+
+def _ex():
+    ex = HostExecutor({0: HostPool(MINI, 32, 0), 1: HostPool(MINI, 32, 1)})
+    ex.reprefill = None
+    return ex
+
+
+def test_exception_hierarchy_matches_reference():
+    for cls in (ConfigError, NotPlaced, RequestTooLarge):
+        assert issubclass(cls, KvPackError)
+
+
+def test_allocator_errors():
+    a = BlockAllocator(4)
+    with pytest.raises(ValueError):
+        a.alloc(-1)
+    with pytest.raises(RequestTooLarge):
+        a.alloc(5)
+    a.take([1])
+    with pytest.raises(ValueError):
+        a.take([1])
+    with pytest.raises(ValueError):
+        a.free([9])
+    with pytest.raises(ConfigError):
+        BlockAllocator(0)
+
+
+def test_executor_misuse():
+    ex = _ex()
+    ex.admit(1, 0, 40)
+    with pytest.raises(ValueError):
+        ex.admit(1, 0, 40)
+    with pytest.raises(NotPlaced):
+        ex.where(2)
+    with pytest.raises(NotPlaced):
+        ex.admit(3, 7, 10)            # no pool on GPU 7
+    with pytest.raises(RequestTooLarge):
+        ex.admit(4, 1, 10 ** 6)       # pool too small
+    ex.release(99)                     # releasing an unknown request is a no-op
+    with pytest.raises(ConfigError):  # token_transfer needs a re-prefill engine
+        ex.execute([PlannedMove(PendingMove(1, 0, 1, 0, 40), TOKEN_TRANSFER)])
+    # a move whose item is not physically at src moves nothing (sim.py:209-213 semantics)
+    rep = ex.execute([PlannedMove(PendingMove(1, 1, 0, 0, 40), KV_TRANSFER)])
+    assert rep.records[0].requests == [] and ex.where(1).gpu == 0
+
+
+def test_executor_bookkeeping_roundtrip():
+    ex = _ex()
+    ex.admit(5, 0, 33)                 # 3 blocks
+    ex.grow(5, 48)                     # still 3
+    assert len(ex.where(5).blocks) == 3
+    ex.grow(5, 49)                     # 4th block
+    assert len(ex.where(5).blocks) == 4
+    rep = ex.execute([PlannedMove(PendingMove(5, 0, 1, 49 * MINI.kv_bytes_per_token, 49), KV_TRANSFER)])
+    assert rep.records[0].requests == [5] and rep.tokens_moved == 49
+    assert ex.where(5).gpu == 1 and ex.pool(0).allocator.n_free == 32
+    assert ex.launched and ex.launched[-1][0][2] == 4   # one kvm_migrate, 4 blocks
+
+
+def test_multi_model_executor_requires_model():
+    other = ModelShape("other", layers=2, kv_heads=2, head_dim=64, q_heads=2, d_model=128)
+    ex = HostExecutor({0: {"mini": HostPool(MINI, 8, 0), "other": HostPool(other, 8, 1)}})
+    with pytest.raises(ValueError):
+        ex.admit(1, 0, 10)             # ambiguous: two models served
+    ex.admit(1, 0, 10, model="other")
+    assert ex.where(1).model == "other"
+    with pytest.raises(ConfigError):
+        HostExecutor({0: {"wrong-key": HostPool(MINI, 8, 0)}})
