@@ -40,6 +40,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -70,7 +71,9 @@ void count_launch(int64_t n) { g_launches.fetch_add(n); }
 // pool registry
 // ---------------------------------------------------------------------------
 static std::mutex g_mu;
-static std::vector<Pool> g_pools;
+// deque: push_back never moves existing entries, so a `const Pool*` handed out
+// by get_pool() stays valid while other threads register more pools
+static std::deque<Pool> g_pools;
 
 const Pool* get_pool(int id) {
   std::lock_guard<std::mutex> lk(g_mu);

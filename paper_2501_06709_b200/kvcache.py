@@ -170,13 +170,19 @@ class KVPool:
         return self.shape.pool_bytes(self.num_blocks)
 
     def close(self) -> None:
-        if self.pool_id is not None and self.pool_id >= 0:
+        if getattr(self, "pool_id", None) is not None and self.pool_id >= 0:
             _native.lib().kvm_pool_unregister(self.pool_id)
             self.pool_id = -1
         if self._mapped is not None:
             ptr, off = self._mapped
             _native.lib().kvm_ipc_close(ctypes.c_void_p(ptr), off)
             self._mapped = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library may already be gone
+            pass
 
     # -- cross-process (one process per GPU) ---------------------------------
     def ipc_handle(self) -> tuple:
