@@ -42,6 +42,7 @@ WORKLOADS = {
     "7b-4k": ("llama2-7b", 4096, "configs[1]: Llama-2-7B KV, 4k-token request"),
     "13b-8k": ("llama2-13b", 8192, "configs[2] shape: Llama-2-13B KV, 8k tokens (full transfer)"),
     "70b-16k": ("llama3-70b-gqa", 16384, "configs[3]: Llama-3-70B GQA KV, 16k tokens"),
+    "7b-512": ("llama2-7b", 512, "test size (contract tests only; not a BASELINE config)"),
 }
 NVLINK_PEAK_GBS = 900.0        # nominal per direction per GPU
 NVLINK_MEASURED_GBS = 770.0    # B200_PROFILING.md: measured peer copy per direction
@@ -382,7 +383,7 @@ def run_ours(args) -> int:
     if world == 1:
         ex = MigrationExecutor({0: pool}, {0: table}, engine=args.engine)
         pool.allocator.free(db_np)   # the request is resident in sb; db is free again
-        ex.loc[0] = Residency(0, sb_np.copy(), tokens)
+        ex.loc[0] = Residency(0, sb_np.copy(), tokens, pool.shape.name)
         table.set_host(0, sb_np)
         # make device bytes consistent with the residency (content is irrelevant to timing)
         for i in range(args.warmup):

@@ -298,7 +298,7 @@ class MigrationExecutor:
             self.loc[rid] = Residency(dst, np.asarray(dst_blocks, dtype=np.int32), tokens, old.model)
 
     def _table(self, gpu: int, model: str) -> Optional[BlockTable]:
-        return self.tables.get(gpu, {}).get(model)
+        return self.tables.get(gpu, {}).get(model or self.default_model)
 
     def _res(self, rid: int) -> Residency:
         try:

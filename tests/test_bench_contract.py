@@ -1,0 +1,50 @@
+"""bench.py keeps the driver's JSON contract: the reference arm on CPU here,
+the GPU arm under -m gpu (small test workload, no CPU-baseline sample)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(args, timeout=600):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=timeout, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    d = _run(["--impl", "reference", "--workload", "7b-512", "--steps", "3", "--warmup", "3"])
+    assert BASE_KEYS <= set(d) and d["impl"] == "reference"
+    assert d["unit"] == "GB/s" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
+
+
+def test_warmup_floor():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--warmup", "2"], capture_output=True,
+                         text=True, cwd=ROOT)
+    assert out.returncode != 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_contract():
+    d = _run(["--workload", "7b-512", "--steps", "5", "--warmup", "3", "--no-cpu-baseline"])
+    assert BASE_KEYS <= set(d) and "impl" not in d
+    assert d["bit_exact"] is True and d["value"] > 0 and d["n_gpus"] == 1
+    assert d["gpu_launches"] == 5
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
+    assert r["peak"] > 1000
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * 32 * 4 and e["d2h_bytes_per_step"] == 32 * 4
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]

@@ -76,3 +76,15 @@ def test_multi_model_executor_requires_model():
     assert ex.where(1).model == "other"
     with pytest.raises(ConfigError):
         HostExecutor({0: {"wrong-key": HostPool(MINI, 8, 0)}})
+
+
+def test_residency_without_model_uses_the_single_model():
+    """A Residency built by hand with the default model="" still resolves its
+    pool and block table on a single-model executor (bench.py does this)."""
+    from paper_2501_06709_b200.executor import Residency
+
+    ex = _ex()
+    ex.tables = {0: {"mini": "T0"}, 1: {"mini": "T1"}}
+    ex.loc[7] = Residency(0, np.arange(2, dtype=np.int32), 20)
+    assert ex.pool_of(7) is ex.pool(0)
+    assert ex._table(0, ex.loc[7].model) == "T0"
