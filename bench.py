@@ -312,8 +312,11 @@ def run_ours(args) -> int:
         m = make_move(host, fwd=(i % 2 == 0))
         _native.check(lib.kvm_migrate(ctypes.byref(m), 1, eng | (_native.KVM_F_BLOCKS_ON_HOST if host else 0),
                                       sptr))
-        if world > 1:   # wait for the incoming transfer from recv_from (dst-visible completion)
-            _native.check(lib.kvm_wait_flag(ctypes.c_void_p(mailbox.data_ptr()), seq[0], sptr))
+        if world > 1:   # wait for the incoming transfer from recv_from (dst-visible completion);
+            # bounded (30 s) so a lost peer write fails the run instead of wedging the GPU
+            _native.check(lib.kvm_wait_flag_timeout(ctypes.c_void_p(mailbox.data_ptr()), seq[0],
+                                                    30_000_000_000, ctypes.c_void_p(mailbox.data_ptr() + 4 * 63),
+                                                    sptr))
 
     # ---------------- correctness gate (bit-exact) before timing ----------------
     def gathered_checksum(blocks_np):
@@ -336,6 +339,8 @@ def run_ours(args) -> int:
     else:   # what this rank received must equal what recv_from sent
         sums = exchange_objects(sent)
         ok = got == sums[ri.recv_from] and bool(torch.equal(rowbuf.cpu(), torch.from_numpy(db_np)))
+    if world > 1 and int(mailbox[63].item()) != 0:
+        raise RuntimeError(f"rank {ri.rank}: incoming transfer from rank {ri.recv_from} timed out")
     bit_exact = allreduce_max(0.0 if ok else 1.0, device) == 0.0
     seq[0] = 0
     mailbox.zero_()

@@ -231,6 +231,10 @@ int kvm_compact(int pool, const int32_t* src_blocks, const int32_t* dst_blocks,
  * `stream`: makes a peer's completion flag a stream dependency of the
  * destination.  Flags carry monotonically increasing sequence numbers. */
 int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream);
+/* Same, bounded: gives up after timeout_ns (device %globaltimer) and sets
+ * *err_word = 1 (if non-NULL) — failure detection for a lost peer. */
+int kvm_wait_flag_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err_word,
+                          void* stream);
 /* tcgen05 re-prefill projection (see kvm_reprefill_args). */
 int kvm_reprefill(const kvm_reprefill_args* args, void* stream);
 /* Paged-attention decode reading the (migrated) block tables. */

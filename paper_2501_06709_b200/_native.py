@@ -37,7 +37,7 @@ EXPORTS = (
     "kvm_pool_register", "kvm_pool_unregister", "kvm_pool_piece_bytes", "kvm_pool_bytes",
     "kvm_ipc_export", "kvm_ipc_import", "kvm_ipc_close",
     "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_paged_decode",
-    "kvm_plan_hybrid", "kvm_launch_count",
+    "kvm_plan_hybrid", "kvm_wait_flag_timeout", "kvm_launch_count",
 )
 KVM_DECODE_BF16 = 0x1
 KVM_DECODE_CUDA_CORES = 0x2
@@ -119,6 +119,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kvm_migrate": ([ctypes.POINTER(Move), I, I, P], I),
         "kvm_compact": ([I, P, P, I, P, I, P], I),
         "kvm_wait_flag": ([P, ctypes.c_uint32, P], I),
+        "kvm_wait_flag_timeout": ([P, ctypes.c_uint32, ctypes.c_uint64, P, P], I),
         "kvm_reprefill": ([ctypes.POINTER(ReprefillArgs), P], I),
         "kvm_paged_decode": ([ctypes.POINTER(DecodeArgs), P], I),
         "kvm_plan_hybrid": ([ctypes.POINTER(Pending), I, ctypes.POINTER(PlanParams), ctypes.POINTER(Planned),

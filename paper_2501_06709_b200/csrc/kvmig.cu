@@ -445,12 +445,25 @@ __global__ void finalize_empty_kernel(const __grid_constant__ MigrateParams p) {
   }
 }
 
-__global__ void wait_flag_kernel(const uint32_t* flag, uint32_t value) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// timeout_ns == 0: wait forever.  On timeout, *err (if non-NULL) is set to 1 and
+// the kernel returns, so a lost peer write cannot wedge the GPU.
+__global__ void wait_flag_kernel(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err) {
   if (threadIdx.x == 0) {
     unsigned ns = 32;
+    const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_sys_u32(flag) < value) {
       __nanosleep(ns);
       if (ns < 1024) ns <<= 1;
+      if (timeout_ns && globaltimer_ns() - t0 > timeout_ns) {
+        if (err) atomicExch(err, 1u);
+        return;
+      }
     }
   }
 }
@@ -861,8 +874,13 @@ int kvm_compact(int pool, const int32_t* src_blocks, const int32_t* dst_blocks, 
 }
 
 int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream) {
+  return kvm_wait_flag_timeout(flag, value, 0, nullptr, stream);
+}
+
+int kvm_wait_flag_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err_word,
+                          void* stream) {
   if (!flag) return fail(KVM_ERR_INVALID, "flag is NULL");
-  wait_flag_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flag, value);
+  wait_flag_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flag, value, timeout_ns, err_word);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
   return KVM_OK;

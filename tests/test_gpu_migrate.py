@@ -292,3 +292,13 @@ def test_randomized_batches_vs_oracle(seed):
     for dst, exp in expect.values():
         assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
     assert flags[:len(moves)].cpu().tolist() == list(range(1, len(moves) + 1))
+
+
+def test_wait_flag_timeout_reports_instead_of_hanging():
+    flag = torch.zeros(2, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    _native.check(_native.lib().kvm_wait_flag_timeout(ctypes.c_void_p(flag.data_ptr()), 5, 20_000_000,
+                                                      ctypes.c_void_p(flag.data_ptr() + 4),
+                                                      ctypes.c_void_p(s.cuda_stream)))
+    s.synchronize()   # returns after ~20 ms although the flag never reaches 5
+    assert flag.cpu().tolist() == [0, 1]
