@@ -109,6 +109,11 @@ class MigrationExecutor:
         self.loc: Dict[int, Residency] = {}
         self._streams: Dict[int, "torch.cuda.Stream"] = {}
         _native.lib()  # fail loudly now if the native library is missing
+        devices = {p.device for per in self.pools.values() for p in per.values()}
+        if len(devices) > 1:
+            # single process, several GPUs: kernels on the source device store straight
+            # into the destination device's pool and block table (UVA peer access)
+            _native.check(_native.lib().kvm_init(1), "kvm_init(enable_peer_access)")
 
     # -- streams ---------------------------------------------------------------
     def stream(self, device: int):
