@@ -121,6 +121,33 @@ typedef struct kvm_reprefill_args {
   int32_t flags;          /* reserved, 0 */
 } kvm_reprefill_args;
 
+/* Adaptive split migration in ONE kernel on the destination GPU (extension of
+ * the reference's all-or-nothing choice, migration.py:155-169): the first
+ * prefix_blocks blocks (every layer, K and V) are copied from the source pool
+ * by warps that are idle in the re-prefill GEMM, while the tensor cores
+ * recompute K/V of tokens [16 * prefix_blocks, tokens) from x into dst_blocks.
+ * The source pool must be registered on the destination device (same GPU, or
+ * the peer's pool IPC-imported there: the prefix is then pulled over NVLink).
+ * The last CTA rewrites dst_table_row[0 .. ceil(tokens/16)) and publishes
+ * done_flag.  Argument rules as kvm_reprefill. */
+typedef struct kvm_split_args {
+  int32_t src_pool;
+  int32_t dst_pool;
+  int32_t tokens;         /* n: tokens of the request */
+  int32_t prefix_blocks;  /* transferred blocks; suffix s = n - 16 * prefix_blocks is re-prefilled */
+  int32_t d_model;
+  int32_t q_cols;
+  const int32_t* src_blocks; /* device, >= prefix_blocks entries */
+  const int32_t* dst_blocks; /* device, ceil(n / 16) entries */
+  const void* x;          /* bf16 [s][d_model] hidden states of the suffix */
+  const void* w;          /* bf16 [layers][q_cols + 2 * kv_heads * head_dim][d_model] */
+  void* q_out;            /* bf16 [layers][s][q_cols] or NULL */
+  int32_t* dst_table_row; /* optional */
+  uint32_t* done_flag;    /* optional */
+  uint32_t done_value;
+  int32_t flags;          /* reserved, 0 */
+} kvm_split_args;
+
 /* Paged-attention decode over a pool (the consumer of a migrated cache):
  * for layers [layer0, layer0 + n_layers), requests b < batch and query heads
  * qh < q_heads (kv head = qh / (q_heads / kv_heads)):
@@ -237,6 +264,8 @@ int kvm_wait_flag_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout
                           void* stream);
 /* tcgen05 re-prefill projection (see kvm_reprefill_args). */
 int kvm_reprefill(const kvm_reprefill_args* args, void* stream);
+/* Fused split migration: prefix copy + suffix re-prefill in one launch. */
+int kvm_split_migrate(const kvm_split_args* args, void* stream);
 /* Paged-attention decode reading the (migrated) block tables. */
 int kvm_paged_decode(const kvm_decode_args* args, void* stream);
 

@@ -37,7 +37,7 @@ EXPORTS = (
     "kvm_pool_register", "kvm_pool_unregister", "kvm_pool_piece_bytes", "kvm_pool_bytes",
     "kvm_ipc_export", "kvm_ipc_import", "kvm_ipc_close",
     "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_paged_decode",
-    "kvm_plan_hybrid", "kvm_wait_flag_timeout", "kvm_launch_count",
+    "kvm_plan_hybrid", "kvm_wait_flag_timeout", "kvm_split_migrate", "kvm_launch_count",
 )
 KVM_DECODE_BF16 = 0x1
 KVM_DECODE_CUDA_CORES = 0x2
@@ -64,6 +64,14 @@ class ReprefillArgs(ctypes.Structure):
                 ("x", ctypes.c_void_p), ("w", ctypes.c_void_p), ("q_out", ctypes.c_void_p),
                 ("dst_blocks", ctypes.c_void_p), ("done_flag", ctypes.c_void_p),
                 ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32)]
+
+
+class SplitArgs(ctypes.Structure):
+    _fields_ = [("src_pool", ctypes.c_int32), ("dst_pool", ctypes.c_int32), ("tokens", ctypes.c_int32),
+                ("prefix_blocks", ctypes.c_int32), ("d_model", ctypes.c_int32), ("q_cols", ctypes.c_int32),
+                ("src_blocks", ctypes.c_void_p), ("dst_blocks", ctypes.c_void_p), ("x", ctypes.c_void_p),
+                ("w", ctypes.c_void_p), ("q_out", ctypes.c_void_p), ("dst_table_row", ctypes.c_void_p),
+                ("done_flag", ctypes.c_void_p), ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32)]
 
 
 class DecodeArgs(ctypes.Structure):
@@ -122,6 +130,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kvm_wait_flag_timeout": ([P, ctypes.c_uint32, ctypes.c_uint64, P, P], I),
         "kvm_reprefill": ([ctypes.POINTER(ReprefillArgs), P], I),
         "kvm_paged_decode": ([ctypes.POINTER(DecodeArgs), P], I),
+        "kvm_split_migrate": ([ctypes.POINTER(SplitArgs), P], I),
         "kvm_plan_hybrid": ([ctypes.POINTER(Pending), I, ctypes.POINTER(PlanParams), ctypes.POINTER(Planned),
                              ctypes.POINTER(PlanLedgers)], I),
         "kvm_launch_count": ([], I64),

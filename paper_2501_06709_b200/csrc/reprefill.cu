@@ -63,7 +63,17 @@ struct Params {
   int32_t rows, n_out, d_model, layers, q_cols, kvd, tok0, block_tokens, n_dst_blocks;
   int32_t m_tiles, n_tiles, k_blocks, total_tiles;
   uint32_t done_value;
+  // fused split migration (kvm_split_migrate): the transferred prefix, streamed by
+  // warps 2-3 while the tensor cores re-prefill the suffix
+  const uint8_t* csrc;          // source pool base (local or peer-mapped)
+  const int32_t* csrc_blocks;   // source blocks of the prefix
+  int64_t c_src_plane;          // source pool bytes per (layer, K|V) plane
+  int64_t c_units;              // 8 KiB copy units: planes * prefix_blocks * units_per_piece
+  int32_t c_nblocks, c_upp;     // prefix blocks, units per piece
+  int32_t* table_row;           // if set: the last CTA writes table_row[i] = dst_blocks[i], i < table_n
+  int32_t table_n;
 };
+constexpr int CUNIT = 8192;     // copy unit per warp iteration: 32 lanes x 16 x 16 B
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -154,6 +164,53 @@ __device__ __forceinline__ void decode(const Params& p, int t, int& l, int& nt, 
   mt = r - nt * p.m_tiles;
 }
 
+// One 8 KiB unit of the fused prefix copy (every layer, K and V, of the
+// transferred blocks), claimed by a whole warp from the CTA's unit stream
+// (units blockIdx.x, blockIdx.x + gridDim.x, ...).  Returns false when the
+// CTA's share is exhausted.  16 x 16-byte loads in flight per lane.
+__device__ __forceinline__ bool copy_one_unit(const Params& p, int* next, int lane) {
+  int k = 0;
+  if (lane == 0) k = atomicAdd(next, 1);
+  k = __shfl_sync(0xffffffffu, k, 0);
+  const int64_t u = (int64_t)blockIdx.x + (int64_t)k * gridDim.x;
+  if (u >= p.c_units) return false;
+  const int32_t per_plane = p.c_nblocks * p.c_upp;
+  const int32_t plane = (int32_t)(u / per_plane);
+  const int32_t r = (int32_t)(u - (int64_t)plane * per_plane);
+  const int32_t bi = r / p.c_upp, ui = r - bi * p.c_upp;
+  const int64_t off = (int64_t)ui * CUNIT;
+  const int nv = (int)(min((int64_t)CUNIT, p.piece_bytes - off) >> 4);
+  const int4* src = reinterpret_cast<const int4*>(p.csrc + plane * p.c_src_plane +
+                                                  (int64_t)__ldg(p.csrc_blocks + bi) * p.piece_bytes + off);
+  int4* dst = reinterpret_cast<int4*>(p.pool + plane * p.plane_bytes +
+                                      (int64_t)__ldg(p.dst_blocks + bi) * p.piece_bytes + off);
+  int4 v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int i = lane + 32 * j;
+    if (i < nv) v[j] = __ldg(src + i);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int i = lane + 32 * j;
+    if (i < nv) dst[i] = v[j];
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+template <bool kCopy>
 __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -163,13 +220,16 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int s_last;
+  __shared__ int s_copy_next;  // next copy unit (CTA-local index) of the fused prefix transfer
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_x) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_w) : "memory");
+    if (p.total_tiles > 0) {  // (a split migration with no suffix has no tensor maps)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_x) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_w) : "memory");
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
@@ -180,6 +240,7 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (threadIdx.x == 0) s_copy_next = 0;
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
@@ -245,15 +306,25 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
         }
       }
     }
+  } else if (kCopy && (warp == 2 || warp == 3)) {
+    // ------------------- fused prefix transfer (split migration) -------------------
+    // warps 2-3 are idle in the GEMM for the whole kernel: they stream prefix copy
+    // units until the CTA's share is exhausted (the epilogue warps help between tiles)
+    while (copy_one_unit(p, &s_copy_next, lane)) {
+    }
   } else if (warp >= 4) {
     // ------------------------------ epilogue ------------------------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
     const int64_t row_bytes = (int64_t)p.kvd * 2;
+    bool copying = kCopy;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       int l, nt, mt;
       decode(p, t, l, nt, mt);
+      // fused split migration: while this tile's accumulator is being computed,
+      // the epilogue warp streams prefix copy units (the tile takes ~40 us)
+      while (copying && !mbar_test(tfull + acc, acc_phase)) copying = copy_one_unit(p, &s_copy_next, lane);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const int row = mt * BM + q * 32 + lane;
@@ -301,6 +372,7 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
         acc_phase ^= 1;
       }
     }
+    while (copying) copying = copy_one_unit(p, &s_copy_next, lane);  // GEMM done: finish the copy
   }
 
   tc_fence_before();
@@ -309,13 +381,23 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
-  // completion: last CTA publishes the done flag (system scope, after all K/V stores)
+  // completion: the last CTA rewrites the destination block-table row (split
+  // migration) and publishes the done flag, system scope, after all K/V stores
   if (threadIdx.x == 0) {
     fence_acq_rel_sys();
     const uint32_t old = atomicAdd(p.ctr, 1u);
     s_last = (old + 1 == gridDim.x);
     if (s_last) {
       *p.ctr = 0;
+      fence_acq_rel_sys();
+    }
+  }
+  __syncthreads();
+  if (s_last) {
+    if (p.table_row)
+      for (int i = threadIdx.x; i < p.table_n; i += THREADS) p.table_row[i] = __ldg(p.dst_blocks + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
       fence_acq_rel_sys();
       if (p.done_flag) st_release_sys_u32(p.done_flag, p.done_value);
     }
@@ -346,6 +428,13 @@ struct DevCtr {
   uint32_t next = 0;
   bool attr = false;
 };
+
+// Encode X / W tensor maps and the GEMM geometry.  Returns KVM_OK or an error code.
+static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
+                             int n_dst_blocks, const void* x, const void* w, void* q_out,
+                             const int32_t* dst_blocks);
+// Launch on the pool's device (current device already set); grid = min(work, SMs).
+static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream);
 static DevCtr g_ctr[64];
 static std::mutex g_rp_mu;
 
@@ -354,6 +443,105 @@ static std::mutex g_rp_mu;
 
 using namespace kvm;
 using namespace kvm::rp;
+
+namespace kvm {
+namespace rp {
+
+static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
+                             int n_dst_blocks, const void* x, const void* w, void* q_out,
+                             const int32_t* dst_blocks) {
+  const kvm_pool_desc& d = pool->desc;
+  const int kvd = d.kv_heads * d.head_dim;
+  EncodeTiled enc = encode_fn();
+  if (!enc) return fail(KVM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  const int n_out = q_cols + 2 * kvd;
+  if (rows > 0) {
+    cuuint64_t dims[2] = {(cuuint64_t)d_model, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d_model * 2};
+    cuuint32_t box[2] = {BK, BM};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&p.tmap_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuTensorMapEncodeTiled(x) failed: " + std::to_string((int)r));
+    cuuint64_t wd[3] = {(cuuint64_t)d_model, (cuuint64_t)n_out, (cuuint64_t)d.layers};
+    cuuint64_t ws[2] = {(cuuint64_t)d_model * 2, (cuuint64_t)d_model * 2 * n_out};
+    cuuint32_t wb[3] = {BK, BN, 1};
+    cuuint32_t we[3] = {1, 1, 1};
+    r = enc(&p.tmap_w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), wd, ws, wb, we,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuTensorMapEncodeTiled(w) failed: " + std::to_string((int)r));
+  }
+  p.pool = pool->base;
+  p.q_out = static_cast<__nv_bfloat16*>(q_out);
+  p.dst_blocks = dst_blocks;
+  p.plane_bytes = pool->plane_bytes;
+  p.piece_bytes = pool->piece_bytes;
+  p.rows = rows;
+  p.n_out = n_out;
+  p.d_model = d_model;
+  p.layers = d.layers;
+  p.q_cols = q_cols;
+  p.kvd = kvd;
+  p.tok0 = tok0;
+  p.block_tokens = d.block_tokens;
+  p.n_dst_blocks = n_dst_blocks;
+  p.m_tiles = (rows + BM - 1) / BM;
+  p.n_tiles = (n_out + BN - 1) / BN;
+  p.k_blocks = d_model / BK;
+  const int64_t total = (int64_t)p.m_tiles * p.n_tiles * d.layers;
+  if (total > 0x7fffffff) return fail(KVM_ERR_INVALID, "problem too large");
+  p.total_tiles = (int)total;
+  return KVM_OK;
+}
+
+static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(g_rp_mu);
+  DevCtr& dc = g_ctr[dev];
+  if (!dc.ctr) {
+    KVM_CUDA_TRY(cudaMalloc(&dc.ctr, 64 * sizeof(uint32_t)));
+    KVM_CUDA_TRY(cudaMemset(dc.ctr, 0, 64 * sizeof(uint32_t)));
+  }
+  if (!dc.attr) {
+    KVM_CUDA_TRY(cudaFuncSetAttribute(reprefill_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES));
+    KVM_CUDA_TRY(cudaFuncSetAttribute(reprefill_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES));
+    dc.attr = true;
+  }
+  p.ctr = dc.ctr + (dc.next++ % 64);
+  int64_t work = p.total_tiles;
+  if (copy) work = std::max<int64_t>(work, (p.c_units + 1) / 2);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sm_count(dev)));
+  if (copy)
+    reprefill_kernel<true><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
+  else
+    reprefill_kernel<false><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
+  KVM_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  return KVM_OK;
+}
+
+struct DevScope {
+  int prev = -1, dev;
+  explicit DevScope(int d) : dev(d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevScope() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
+
+static bool is_sm100(int dev) {
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  return major == 10;
+}
+
+}  // namespace rp
+}  // namespace kvm
 
 extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
@@ -373,98 +561,60 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (a->flags != 0) return fail(KVM_ERR_INVALID, "flags must be 0");
   if (reinterpret_cast<uintptr_t>(a->x) % 16 || reinterpret_cast<uintptr_t>(a->w) % 16)
     return fail(KVM_ERR_INVALID, "x and w must be 16-byte aligned");
-  EncodeTiled enc = encode_fn();
-  if (!enc) return fail(KVM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
-
-  int dev = pool->device;
-  int cur = -1;
-  cudaGetDevice(&cur);
-  if (cur != dev) cudaSetDevice(dev);
-  int major = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-  if (major != 10) {
-    if (cur != dev) cudaSetDevice(cur);
-    return fail(KVM_ERR_UNSUPPORTED, "kvm_reprefill needs an sm_100 (B200) device");
-  }
-
+  DevScope ds(pool->device);
+  if (!is_sm100(pool->device)) return fail(KVM_ERR_UNSUPPORTED, "kvm_reprefill needs an sm_100 (B200) device");
   Params p;
   memset(&p, 0, sizeof(p));
-  const int n_out = a->q_cols + 2 * kvd;
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)a->d_model, (cuuint64_t)a->rows};
-    cuuint64_t strides[1] = {(cuuint64_t)a->d_model * 2};
-    cuuint32_t box[2] = {BK, BM};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(&p.tmap_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->x), dims, strides, box,
-                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      if (cur != dev) cudaSetDevice(cur);
-      return fail(KVM_ERR_CUDA, "cuTensorMapEncodeTiled(x) failed: " + std::to_string((int)r));
-    }
-  }
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)a->d_model, (cuuint64_t)n_out, (cuuint64_t)d.layers};
-    cuuint64_t strides[2] = {(cuuint64_t)a->d_model * 2, (cuuint64_t)a->d_model * 2 * n_out};
-    cuuint32_t box[3] = {BK, BN, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&p.tmap_w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->w), dims, strides, box,
-                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      if (cur != dev) cudaSetDevice(cur);
-      return fail(KVM_ERR_CUDA, "cuTensorMapEncodeTiled(w) failed: " + std::to_string((int)r));
-    }
-  }
-  p.pool = pool->base;
-  p.q_out = static_cast<__nv_bfloat16*>(a->q_out);
-  p.dst_blocks = a->dst_blocks;
+  int rc = build_gemm_params(p, pool, a->rows, a->d_model, a->q_cols, a->tok0, a->n_dst_blocks, a->x, a->w,
+                             a->q_out, a->dst_blocks);
+  if (rc) return rc;
   p.done_flag = a->done_flag;
   p.done_value = a->done_value;
-  p.plane_bytes = pool->plane_bytes;
-  p.piece_bytes = pool->piece_bytes;
-  p.rows = a->rows;
-  p.n_out = n_out;
-  p.d_model = a->d_model;
-  p.layers = d.layers;
-  p.q_cols = a->q_cols;
-  p.kvd = kvd;
-  p.tok0 = a->tok0;
-  p.block_tokens = d.block_tokens;
-  p.n_dst_blocks = a->n_dst_blocks;
-  p.m_tiles = (a->rows + BM - 1) / BM;
-  p.n_tiles = (n_out + BN - 1) / BN;
-  p.k_blocks = a->d_model / BK;
-  const int64_t total = (int64_t)p.m_tiles * p.n_tiles * d.layers;
-  if (total > 0x7fffffff) {
-    if (cur != dev) cudaSetDevice(cur);
-    return fail(KVM_ERR_INVALID, "problem too large");
-  }
-  p.total_tiles = (int)total;
+  return launch_gemm(p, pool->device, false, static_cast<cudaStream_t>(stream));
+}
 
-  int rc = KVM_OK;
-  {
-    std::lock_guard<std::mutex> lk(g_rp_mu);
-    DevCtr& dc = g_ctr[dev];
-    if (!dc.ctr) {
-      cudaError_t e = cudaMalloc(&dc.ctr, 64 * sizeof(uint32_t));
-      if (e == cudaSuccess) e = cudaMemset(dc.ctr, 0, 64 * sizeof(uint32_t));
-      if (e != cudaSuccess) rc = cuda_fail(e, "reprefill counter alloc");
-    }
-    if (!rc && !dc.attr) {
-      cudaError_t e = cudaFuncSetAttribute(reprefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      if (e != cudaSuccess) rc = cuda_fail(e, "cudaFuncSetAttribute(reprefill)");
-      dc.attr = true;
-    }
-    p.ctr = dc.ctr + (dc.next++ % 64);
-    if (!rc) {
-      const int grid = std::min(p.total_tiles, sm_count(dev));
-      reprefill_kernel<<<grid, THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(p);
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) rc = cuda_fail(e, "reprefill_kernel launch");
-      else count_launch();
-    }
-  }
-  if (cur != dev) cudaSetDevice(cur);
-  return rc;
+extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
+  if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
+  const Pool* dst = get_pool(a->dst_pool);
+  const Pool* src = dst ? get_pool(a->src_pool) : nullptr;
+  if (!dst || !src) return KVM_ERR_NOT_FOUND;
+  const kvm_pool_desc &sd = src->desc, &d = dst->desc;
+  if (sd.layers != d.layers || sd.kv_heads != d.kv_heads || sd.head_dim != d.head_dim ||
+      sd.block_tokens != d.block_tokens || sd.elem_bytes != d.elem_bytes)
+    return fail(KVM_ERR_CONFIG, "src and dst pools differ in KV shape");
+  if (src->device != dst->device)
+    return fail(KVM_ERR_INVALID, "the split kernel runs on the destination: register (or IPC-import) the "
+                                 "source pool on the destination device");
+  if (d.elem_bytes != 2) return fail(KVM_ERR_CONFIG, "re-prefill writes bf16 KV: pool elem_bytes must be 2");
+  const int kvd = d.kv_heads * d.head_dim;
+  const int bt = d.block_tokens;
+  if (a->tokens < 0 || a->prefix_blocks < 0 || (int64_t)a->prefix_blocks * bt > a->tokens)
+    return fail(KVM_ERR_INVALID, "prefix_blocks * block_tokens must be <= tokens");
+  const int n_blocks = (a->tokens + bt - 1) / bt;
+  const int suffix = a->tokens - a->prefix_blocks * bt;
+  if (a->d_model <= 0 || a->d_model % BK) return fail(KVM_ERR_CONFIG, "d_model must be a positive multiple of 64");
+  if (kvd % 32 || a->q_cols < 0 || a->q_cols % 32)
+    return fail(KVM_ERR_CONFIG, "kv_heads*head_dim and q_cols must be multiples of 32");
+  if (!a->dst_blocks || (a->prefix_blocks && !a->src_blocks) || (suffix && (!a->x || !a->w)))
+    return fail(KVM_ERR_INVALID, "NULL pointer argument");
+  if (a->flags != 0) return fail(KVM_ERR_INVALID, "flags must be 0");
+  if (a->tokens == 0) return KVM_OK;
+  DevScope ds(dst->device);
+  if (!is_sm100(dst->device)) return fail(KVM_ERR_UNSUPPORTED, "kvm_split_migrate needs an sm_100 (B200) device");
+  Params p;
+  memset(&p, 0, sizeof(p));
+  int rc = build_gemm_params(p, dst, suffix, a->d_model, a->q_cols, a->prefix_blocks * bt, n_blocks, a->x, a->w,
+                             a->q_out, a->dst_blocks);
+  if (rc) return rc;
+  p.done_flag = a->done_flag;
+  p.done_value = a->done_value;
+  p.table_row = a->dst_table_row;
+  p.table_n = a->dst_table_row ? n_blocks : 0;
+  p.csrc = src->base;
+  p.csrc_blocks = a->src_blocks;
+  p.c_src_plane = src->plane_bytes;
+  p.c_nblocks = a->prefix_blocks;
+  p.c_upp = (int32_t)((dst->piece_bytes + CUNIT - 1) / CUNIT);
+  p.c_units = (int64_t)2 * d.layers * a->prefix_blocks * p.c_upp;
+  return launch_gemm(p, dst->device, p.c_units > 0, static_cast<cudaStream_t>(stream));
 }

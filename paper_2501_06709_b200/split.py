@@ -103,3 +103,27 @@ def wait_split(flags_dev, plan: SplitPlan, seq: int, stream) -> None:
 def flops_per_token(shape, with_q: bool = True) -> int:
     n_out = (shape.q_cols if with_q else 0) + 2 * shape.kv_cols
     return 2 * shape.d_model * n_out * shape.layers
+
+
+def split_migrate_fused(src: KVPool, dst: KVPool, src_blocks_dev, dst_blocks_dev, plan: SplitPlan, x_suffix, w,
+                        *, stream=None, table_row: int = 0, done_flag: int = 0, done_value: int = 1) -> None:
+    """One-launch split migration on the destination (kvm_split_migrate): warps
+    idle in the re-prefill GEMM copy the prefix while the tensor cores
+    recompute the suffix.  src must be registered on dst's device (same GPU, or
+    an IPC-imported peer pool: the prefix is then pulled over NVLink)."""
+    import torch
+
+    if plan.suffix and (x_suffix is None or x_suffix.shape[0] != plan.suffix):
+        raise ValueError("x_suffix must have `suffix` rows")
+    q_cols = w.shape[1] - 2 * dst.shape.kv_cols
+    a = _native.SplitArgs()
+    a.src_pool, a.dst_pool, a.tokens, a.prefix_blocks = src.pool_id, dst.pool_id, plan.tokens, plan.prefix_blocks
+    a.d_model, a.q_cols = w.shape[2], q_cols
+    a.src_blocks, a.dst_blocks = src_blocks_dev.data_ptr(), dst_blocks_dev.data_ptr()
+    a.x = x_suffix.data_ptr() if plan.suffix else None
+    a.w = w.data_ptr()
+    a.q_out = None
+    a.dst_table_row, a.done_flag, a.done_value, a.flags = table_row or None, done_flag or None, done_value, 0
+    s = stream if stream is not None else torch.cuda.current_stream(dst.device)
+    _native.check(_native.lib().kvm_split_migrate(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),
+                  "kvm_split_migrate")

@@ -51,3 +51,50 @@ def test_split_migration(tokens, suffix):
             torch.testing.assert_close(dst.tensor[l, 1, blk, slot].reshape(suffix, kvd).float(),
                                        ref[:, qc + kvd:], atol=1e-2, rtol=1.6e-2)
     assert flags.cpu().tolist() == [7 if pre else 0, 7 if suffix else 0]
+
+
+@pytest.mark.parametrize("tokens,suffix", [(1024, 240), (1000, 232), (512, 0), (512, 512), (16 * 40, None),
+                                           (4096, 1024)])
+def test_fused_split_migration(tokens, suffix):
+    """kvm_split_migrate: one launch; prefix copied by the GEMM's idle warps."""
+    from paper_2501_06709_b200.split import split_migrate_fused
+
+    shape = ModelShape("spf", layers=6, kv_heads=4, head_dim=128, q_heads=8, d_model=512)
+    if suffix is None:
+        suffix = split_point(tokens, shape.kv_bytes_per_token, 770e9, flops_per_token(shape), 1.2e15)
+    plan = make_split(tokens, suffix)
+    nb = plan.total_blocks + 20
+    src, dst = KVPool(shape, nb, dtype=torch.bfloat16), KVPool(shape, nb, dtype=torch.bfloat16)
+    src.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    dst.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    before = dst.tensor.view(torch.int16).clone()
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(3))[:plan.total_blocks].to(torch.int32).cuda()
+    db = torch.from_numpy(dst.allocator.alloc(plan.total_blocks)).cuda()
+    x = synthetic_hidden(shape, max(suffix, 1), 0, seed=4)[:suffix].contiguous()
+    w = synthetic_weights(shape, 0, with_q=True, seed=5)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    table = BlockTable(1, plan.total_blocks)
+    split_migrate_fused(src, dst, sb, db, plan, x, w, table_row=table.row_ptr(0), done_flag=flag.data_ptr(),
+                        done_value=9)
+    torch.cuda.synchronize()
+    pre = plan.prefix_blocks
+    assert torch.equal(dst.tensor[:, :, db[:pre].long()].view(torch.int16),
+                       src.tensor[:, :, sb[:pre].long()].view(torch.int16))
+    if suffix:
+        kvd, qc = shape.kv_cols, shape.q_cols
+        toks = torch.arange(plan.prefix_tokens, tokens, device="cuda")
+        blk, slot = db.long()[toks // 16], toks % 16
+        for l in range(shape.layers):
+            ref = x.float() @ w[l].float().t()
+            torch.testing.assert_close(dst.tensor[l, 0, blk, slot].reshape(suffix, kvd).float(),
+                                       ref[:, qc:qc + kvd], atol=1e-2, rtol=1.6e-2)
+            torch.testing.assert_close(dst.tensor[l, 1, blk, slot].reshape(suffix, kvd).float(),
+                                       ref[:, qc + kvd:], atol=1e-2, rtol=1.6e-2)
+    # nothing outside the request's destination slots changed
+    mask = torch.ones(nb, 16, dtype=torch.bool, device="cuda")
+    mask[db[:pre].long()] = False
+    if suffix:
+        mask[blk, slot] = False
+    assert torch.equal(dst.tensor.view(torch.int16)[:, :, mask], before[:, :, mask])
+    assert np.array_equal(table.rows[0].cpu().numpy(), db.cpu().numpy())
+    assert flag.item() == 9

@@ -23,7 +23,8 @@ import torch  # noqa: E402
 from paper_2501_06709_b200 import _native  # noqa: E402
 from paper_2501_06709_b200.kvcache import LLAMA2_13B, KVPool  # noqa: E402
 from paper_2501_06709_b200.reprefill import reprefill, split_point, synthetic_hidden, synthetic_weights  # noqa: E402
-from paper_2501_06709_b200.split import flops_per_token, make_split, split_migrate, wait_split  # noqa: E402
+from paper_2501_06709_b200.split import (flops_per_token, make_split, split_migrate,  # noqa: E402
+                                         split_migrate_fused, wait_split)
 
 NVLINK_GBS = 770e9
 TENSOR_FLOPS = 1.28e15  # measured kvm_reprefill rate on 13B (tools/bench_reprefill.py)
@@ -92,6 +93,11 @@ def main():
         _native.check(_native.lib().kvm_migrate(ctypes_byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST |
                                                 _native.KVM_F_ENGINE_BULK, ctypes_stream(sbs)))
 
+    sbd = torch.from_numpy(sb).cuda()
+
+    def run_fused():
+        split_migrate_fused(src, dst, sbd, db, plan, x, w, stream=sbs)
+
     def run_suffix_only():
         reprefill(dst, x, w, db, tok0=plan.prefix_tokens, stream=sbs)
 
@@ -125,6 +131,13 @@ def main():
                     got = dst.tensor[l, kv, blk, slot].reshape(plan.suffix, kvd).float()
                     r = ref[:, lo:lo + kvd]
                     worst = max(worst, float(((got - r).abs() - 1.6e-2 * r.abs()).max()))
+        # fused one-launch variant: parity again, then timing
+        dst.tensor.view(torch.int16).zero_()
+        run_fused()
+        torch.cuda.synchronize()
+        exact_fused = bool(torch.equal(dst.tensor[:, :, db[:plan.prefix_blocks].long()].view(torch.int16),
+                                       src.tensor[:, :, pi].view(torch.int16)))
+        t_fused = timeit(run_fused)
         t_split = timeit(lambda: run_split(True))
         t_serial = timeit(lambda: run_split(False))
         t_full = timeit(run_full)
@@ -135,10 +148,13 @@ def main():
         "suffix_reprefilled": plan.suffix, "prefix_blocks": plan.prefix_blocks,
         "kv_bytes": kv_bytes, "prefix_bytes": plan.prefix_tokens * shape.kv_bytes_per_token,
         "suffix_flops": plan.suffix * fpt,
-        "ms": {"split_overlapped_1gpu": round(t_split, 4), "split_serialized_1gpu": round(t_serial, 4),
+        "ms": {"split_fused_one_kernel": round(t_fused, 4),
+               "split_overlapped_1gpu": round(t_split, 4), "split_serialized_1gpu": round(t_serial, 4),
                "full_transfer_1gpu": round(t_full, 4), "prefix_transfer_only": round(t_prefix, 4),
                "suffix_reprefill_only": round(t_suffix, 4)},
-        "overlap_efficiency": round((t_prefix + t_suffix) / t_split, 3) if t_split else None,
+        "overlap_efficiency_two_streams": round((t_prefix + t_suffix) / t_split, 3) if t_split else None,
+        "overlap_efficiency_fused": round((t_prefix + t_suffix) / t_fused, 3) if t_fused else None,
+        "fused_prefix_bit_exact": exact_fused,
         "suffix_tflops": round(plan.suffix * fpt / t_suffix / 1e9, 1) if t_suffix else None,
         "model_2gpu_ms": {"full_transfer_nvlink": round(kv_bytes / NVLINK_GBS * 1e3, 3),
                           "split": round(max(plan.prefix_tokens * shape.kv_bytes_per_token / NVLINK_GBS,
