@@ -278,6 +278,52 @@ class MigrationExecutor:
             self._pending_commit = post
         return rec
 
+    def split_move(self, rid: int, dst_gpu: int, suffix: Optional[int] = None, *, link_bytes_per_s: float = 770e9,
+                   tensor_flops_per_s: float = 1.28e15) -> ExecRecord:
+        """Adaptive split (extension of migration.py:155-169): transfer the first
+        n - s tokens' blocks and re-prefill the last s tokens, in ONE fused
+        kernel on the destination (kvm_split_migrate).  s defaults to the
+        balanced point of the reference's linear cost terms
+        (reprefill.split_point).  Needs a ReprefillEngine; the source pool must
+        be registered on the destination's device."""
+        import torch
+
+        from .reprefill import split_point
+        from .split import flops_per_token, make_split, split_migrate_fused
+
+        if self.reprefill is None:
+            raise ConfigError("split moves need a re-prefill engine")
+        res = self._res(rid)
+        src_pool, dst_pool = self.pool(res.gpu, res.model), self.pool(dst_gpu, res.model)
+        sh = dst_pool.shape
+        if suffix is None:
+            suffix = split_point(res.tokens, sh.kv_bytes_per_token, link_bytes_per_s,
+                                 flops_per_token(sh, with_q=self.reprefill.with_q), tensor_flops_per_s)
+        # the transferred prefix must be whole blocks
+        suffix = res.tokens - ((res.tokens - suffix) // sh.block_tokens) * sh.block_tokens
+        plan = make_split(res.tokens, suffix, sh.block_tokens)
+        dst_blocks = dst_pool.allocator.alloc(plan.total_blocks)
+        dev = dst_pool.device
+        s = self.stream(dev)
+        with torch.cuda.stream(s):
+            sbd = torch.from_numpy(np.ascontiguousarray(res.blocks, dtype=np.int32)).to(f"cuda:{dev}")
+            dbd = torch.from_numpy(dst_blocks).to(f"cuda:{dev}")
+            x = self.reprefill.hidden(sh, rid, max(suffix, 1), dev)[:suffix].contiguous()
+            table = self._table(dst_gpu, res.model)
+            row = 0
+            if table is not None:
+                table.set_host(rid, dst_blocks)
+                row = table.row_ptr(rid)
+            split_migrate_fused(src_pool, dst_pool, sbd, dbd, plan, x, self.reprefill.weights[(dev, sh.name)],
+                                stream=s, table_row=row)
+            for t in (sbd, dbd, x):
+                t.record_stream(s)
+        s.synchronize()
+        self._commit([(rid, dst_gpu, res.tokens, dst_blocks)])
+        return ExecRecord(rid, res.gpu, dst_gpu, "split", [rid], plan.total_blocks,
+                          plan.prefix_blocks * sh.piece_bytes * 2 * sh.layers, suffix,
+                          plan.prefix_tokens, {rid: res.tokens})
+
     def commit(self) -> None:
         """Finish a wait=False execute(): await streams, then free sources."""
         self.synchronize()

@@ -98,3 +98,25 @@ def test_fused_split_migration(tokens, suffix):
     assert torch.equal(dst.tensor.view(torch.int16)[:, :, mask], before[:, :, mask])
     assert np.array_equal(table.rows[0].cpu().numpy(), db.cpu().numpy())
     assert flag.item() == 9
+
+
+def test_executor_split_move():
+    """MigrationExecutor.split_move: the fused split through the host API."""
+    from paper_2501_06709_b200.executor import MigrationExecutor
+    from paper_2501_06709_b200.reprefill import ReprefillEngine
+
+    shape = ModelShape("spx", layers=4, kv_heads=4, head_dim=128, q_heads=4, d_model=512)
+    pools = {0: KVPool(shape, 64, dtype=torch.bfloat16), 1: KVPool(shape, 64, dtype=torch.bfloat16)}
+    tables = {0: BlockTable(4, 64), 1: BlockTable(4, 64)}
+    ex = MigrationExecutor(pools, tables, reprefill=ReprefillEngine(shape, [0], with_q=False))
+    pools[0].tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    ex.admit(3, 0, 600)
+    sb = ex.where(3).blocks.copy()
+    rec = ex.split_move(3, 1, suffix=200)
+    r = ex.where(3)
+    assert r.gpu == 1 and rec.tokens_recomputed == 200 + (600 - 200) % 16
+    pre = (600 - rec.tokens_recomputed) // 16
+    assert torch.equal(pools[1].tensor[:, :, torch.from_numpy(r.blocks[:pre]).long().cuda()].view(torch.int16),
+                       pools[0].tensor[:, :, torch.from_numpy(sb[:pre]).long().cuda()].view(torch.int16))
+    assert np.array_equal(tables[1].rows[tables[1].slot(3), :len(r.blocks)].cpu().numpy(), r.blocks)
+    assert pools[0].allocator.n_free == 64
