@@ -251,7 +251,9 @@ int kvm_ipc_close(void* mapped_ptr, int64_t offset);
  * that owns the first move's source pool.  Asynchronous on `stream`. */
 #define KVM_MAX_MOVES 96
 int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream);
-/* src pool == dst pool: move n blocks of one request into fresh blocks. */
+/* src pool == dst pool: move n blocks of one request into fresh blocks.  The
+ * src and dst block sets must be disjoint (verified with KVM_F_BLOCKS_ON_HOST;
+ * with device-resident lists it is the caller's contract). */
 int kvm_compact(int pool, const int32_t* src_blocks, const int32_t* dst_blocks,
                 int n_blocks, int32_t* table_row, int flags, void* stream);
 /* Device-side wait until *flag >= value (unsigned; system-scope acquire), on

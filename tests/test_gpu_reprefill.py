@@ -112,3 +112,22 @@ def test_reprefill_13b_balanced_split():
     mask = torch.ones(nb, 16, dtype=torch.bool, device="cuda")
     mask[blocks.long()[toks // 16], toks % 16] = False
     assert torch.equal(after[:, :, mask], before[:, :, mask])
+
+
+@pytest.mark.parametrize("kv_heads,head_dim,q_heads", [(3, 64, 1), (1, 32, 3), (5, 96, 0)])
+def test_reprefill_n_not_multiple_of_tile(kv_heads, head_dim, q_heads):
+    """n_out = q_cols + 2*kv_cols not a multiple of the 256-column N tile."""
+    shape = ModelShape("nt", layers=2, kv_heads=kv_heads, head_dim=head_dim, q_heads=max(q_heads, 1), d_model=128)
+    rows, tok0 = 50, 7
+    nb = (tok0 + rows + 15) // 16 + 3
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    before = pool.tensor.view(torch.int16).clone()
+    blocks = torch.randperm(nb, generator=torch.Generator().manual_seed(1))[:(tok0 + rows + 15) // 16]
+    blocks = blocks.to(torch.int32).cuda()
+    x = synthetic_hidden(shape, rows, 0, seed=3)
+    w = synthetic_weights(shape, 0, with_q=q_heads > 0, seed=4)
+    assert w.shape[1] % 256 != 0
+    reprefill(pool, x, w, blocks, tok0=tok0)
+    torch.cuda.synchronize()
+    _check(shape, pool, blocks, tok0, rows, _ref(x, w), None, before)
