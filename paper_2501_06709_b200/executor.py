@@ -125,6 +125,17 @@ class MigrationExecutor:
             self._streams[device] = s
         return s
 
+    def ordered_stream(self, device: int):
+        """The executor's stream for `device`, made to wait for everything the
+        caller has queued on its current stream (pool fills, hidden states,
+        weights...): the usual side-stream contract, so a migration or
+        re-prefill never reads data that is still being produced."""
+        import torch
+
+        s = self.stream(device)
+        s.wait_stream(torch.cuda.current_stream(device))
+        return s
+
     def synchronize(self) -> None:
         for s in self._streams.values():
             s.synchronize()
@@ -226,7 +237,7 @@ class MigrationExecutor:
                     if self.reprefill is None:
                         raise ConfigError("token_transfer planned but executor has no re-prefill engine")
                     self.reprefill(self, rid, mv.dst, dst_blocks, res.tokens,
-                                   self.stream(dst_pool.device))
+                                   self.ordered_stream(dst_pool.device))
                     table = self._table(mv.dst, res.model)
                     if table is not None:
                         table.set_host(rid, dst_blocks)
@@ -263,7 +274,7 @@ class MigrationExecutor:
         if table is not None:
             table.set_host(rid, dst)
             row = table.row_ptr(rid)
-        s = self.stream(pool.device)
+        s = self.ordered_stream(pool.device)
         _native.check(_native.lib().kvm_compact(
             pool.pool_id, sb.ctypes.data, dst.ctypes.data, nb, ctypes.c_void_p(row),
             _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag, ctypes.c_void_p(s.cuda_stream)),
@@ -304,7 +315,9 @@ class MigrationExecutor:
         plan = make_split(res.tokens, suffix, sh.block_tokens)
         dst_blocks = dst_pool.allocator.alloc(plan.total_blocks)
         dev = dst_pool.device
-        s = self.stream(dev)
+        s = self.ordered_stream(dev)
+        if src_pool.device != dev:
+            s.wait_stream(torch.cuda.current_stream(src_pool.device))
         with torch.cuda.stream(s):
             sbd = torch.from_numpy(np.ascontiguousarray(res.blocks, dtype=np.int32)).to(f"cuda:{dev}")
             dbd = torch.from_numpy(dst_blocks).to(f"cuda:{dev}")
@@ -334,7 +347,7 @@ class MigrationExecutor:
     def _launch_migrate(self, dev: int, moves: List[_native.Move]) -> None:
         """One fused kvm_migrate launch for every move leaving `dev` this slot."""
         arr = (_native.Move * len(moves))(*moves)
-        s = self.stream(dev)
+        s = self.ordered_stream(dev)
         _native.check(_native.lib().kvm_migrate(arr, len(moves),
                                                 _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag,
                                                 ctypes.c_void_p(s.cuda_stream)), "kvm_migrate")

@@ -89,7 +89,7 @@ class LiveMigration:
         if self._table is not None:  # fused: this launch fills entries [lo, hi) of the dst row
             self._table.set_host(self.rid, self.dst_blocks)
             m.dst_table_row = self._table.row_ptr(self.rid) + 4 * lo
-        s = self.ex.stream(self.src_pool.device)
+        s = self.ex.ordered_stream(self.src_pool.device)
         _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | self.flags,
                                                 ctypes.c_void_p(s.cuda_stream)), "kvm_migrate (live)")
 

@@ -31,6 +31,8 @@ def test_split_migration(tokens, suffix):
     flags = torch.zeros(2, dtype=torch.int32, device="cuda")
     table = BlockTable(1, plan.total_blocks)
     sa, sb_ = torch.cuda.Stream(), torch.cuda.Stream()
+    sa.wait_stream(torch.cuda.current_stream())   # inputs were produced on the default stream
+    sb_.wait_stream(torch.cuda.current_stream())
     split_migrate(src, dst, sb, db, plan, x, w, xfer_stream=sa, rp_stream=sb_, flags_dev=flags, seq=7,
                   table_row=table.row_ptr(0), engine_flags=_native.KVM_F_CTAS_PER_SM(3))
     wait_split(flags, plan, 7, sb_)

@@ -35,6 +35,7 @@ def main():
     w = synthetic_weights(shape, 0, with_q=not a.kv_only)
     flops = reprefill_flops(shape, rows, with_q=not a.kv_only)
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # x, w, pool were produced on the default stream
 
     def timeit(fn):
         for _ in range(a.warmup):

@@ -113,6 +113,8 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / a.iters
 
+    sbs.wait_stream(torch.cuda.current_stream())   # pools, x and w were produced on the default stream
+    sa.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(sbs):
         # parity first: prefix bit-exact, suffix within bf16 tolerance
         run_split(True)

@@ -19,6 +19,7 @@ for rows in (512, 77, 1, 300):
     s = torch.cuda.Stream()
     for it in range(n // 4):
         pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+        s.wait_stream(torch.cuda.current_stream())  # x, w and the pool fill come from the default stream
         reprefill(pool, x, w, db, tok0=0, stream=s)
         s.synchronize()
         k = pool.tensor[:, 0, db.long()[toks // 16], toks % 16].reshape(shape.layers, rows, kvd).float()
