@@ -47,6 +47,9 @@ class HostExecutor(MigrationExecutor):
     def stream(self, device):
         return _Stream()
 
+    def ordered_stream(self, device):
+        return _Stream()
+
     def _launch_migrate(self, dev, moves):
         self.launched.append([(m.src_pool, m.dst_pool, m.n_blocks) for m in moves])
 
