@@ -51,6 +51,10 @@ extern "C" {
 #define KVM_ERR_CUDA (-3)        /* CUDA runtime failure      -> KvmCudaError */
 #define KVM_ERR_NOT_FOUND (-4)   /* unknown pool id           -> NotPlaced    */
 #define KVM_ERR_UNSUPPORTED (-5) /* feature not built / device too old        */
+#define KVM_ERR_KEY (-6)         /* unknown GPU / request / group -> KeyError  */
+#define KVM_ERR_TOO_LARGE (-7)   /* request exceeds a GPU    -> RequestTooLarge */
+#define KVM_ERR_NO_CATEGORY (-8) /* empty GPU has no class   -> NoCategory     */
+#define KVM_ERR_ASSERT (-9)      /* invariant broken         -> AssertionError */
 
 /* kvm_migrate flags */
 #define KVM_F_BLOCKS_ON_HOST 0x1 /* src_blocks/dst_blocks are host pointers; the
@@ -275,6 +279,132 @@ int kvm_paged_decode(const kvm_decode_args* args, void* stream);
 /* plan_hybrid on the host CPU (no GPU needed); out has n entries; ledgers may be NULL. */
 int kvm_plan_hybrid(const kvm_pending* moves, int n, const kvm_plan_params* params, kvm_planned* out,
                     kvm_plan_ledgers* ledgers);
+
+/* --- native online scheduler (host CPU) -------------------------------------
+ * The reference's ClusterState (model.py:116-305) and MellScheduler
+ * (scheduler.py:217-1200) in C++: the caller of the data path, which emits
+ * the logical moves that become PendingMoves (sim.py:177-187).  Same
+ * decisions as the reference on every input (tests/test_scheduler_native.py).
+ * Optional ids (Python None) are encoded as KVM_NONE.  Results come back as
+ * records of 5 int64 words {tag, a, b, c, d} in a buffer owned by the handle,
+ * valid until the next call on it. */
+#define KVM_NONE INT64_MIN
+/* SizeClass (model.py:23-28) */
+#define KVM_CLASS_L 0
+#define KVM_CLASS_M 1
+#define KVM_CLASS_S 2
+#define KVM_CLASS_T 3
+#define KVM_CLASS_TINY 4
+/* Move.reason strings (scheduler.py:24-31) */
+#define KVM_REASON_ALLOCATE 0
+#define KVM_REASON_L_FILL 1
+#define KVM_REASON_DEPART_REFILL 2
+#define KVM_REASON_UPDATE 3
+#define KVM_REASON_BATCH 4
+/* OperationLog.kind (scheduler.py:34-45) */
+#define KVM_LOG_ALLOCATE 0
+#define KVM_LOG_DEPART 1
+#define KVM_LOG_UPDATE 2
+#define KVM_LOG_EPOCH 3
+/* OperationLog.events kinds */
+#define KVM_EVENT_REJECTED 0
+#define KVM_EVENT_ABORTED 1
+/* result records */
+#define KVM_REC_LOG 1          /* {tag, kind, request_id}                  */
+#define KVM_REC_MOVE 2         /* {tag, item, src, dst, reason} (last log) */
+#define KVM_REC_EVENT 3        /* {tag, kind, id}               (last log) */
+#define KVM_REC_TERMINATED 4   /* {tag, gpu}                               */
+#define KVM_REC_BATCHED 5      /* {tag, 0|1}                               */
+#define KVM_REC_EPOCH_COUNTS 6 /* {tag, sequential, adopted} (batching)    */
+#define KVM_REC_CLASS 7        /* {tag, item, KVM_CLASS_*} scheduled_class  */
+/* snapshot records (dict contents in the reference's insertion order) */
+#define KVM_SNAP_COUNTERS 10      /* {tag, next_activation_seq, next_group_id, next_gpu_id, version} */
+#define KVM_SNAP_GPU 11           /* {tag, id, machine_id, activation_seq, n_residents} */
+#define KVM_SNAP_RESIDENT 12      /* {tag, item} x n_residents after its GPU */
+#define KVM_SNAP_PLACEMENT 13     /* {tag, item, gpu} */
+#define KVM_SNAP_SIZE 14          /* {tag, request, bytes} */
+#define KVM_SNAP_GROUP 15         /* {tag, gid, aggregate_bytes, n_members} */
+#define KVM_SNAP_MEMBER 16        /* {tag, request} x n_members after its group */
+#define KVM_SNAP_REQUEST_GROUP 17 /* {tag, request, gid} */
+#define KVM_SNAP_FREE_ID 18       /* {tag, gpu id} released ids, ascending */
+/* verify_properties codes (scheduler.py:102-191) */
+#define KVM_VIOLATION_CAPACITY 0
+#define KVM_VIOLATION_P1 1
+#define KVM_VIOLATION_P2 2
+#define KVM_VIOLATION_P3 3
+#define KVM_VIOLATION_P4_MISSING 4
+#define KVM_VIOLATION_P4_MULTIPLE 5
+#define KVM_VIOLATION_P5 6
+/* kvm_cluster_op ops: ClusterState methods (model.py line) */
+#define KVM_CL_ACTIVATE_GPU 0      /* ret = id                      :191 */
+#define KVM_CL_TERMINATE_GPU 1     /* a = gpu                       :208 */
+#define KVM_CL_PLACE 2             /* a = item, b = gpu             :223 */
+#define KVM_CL_UNPLACE 3           /* a = item, ret = gpu           :230 */
+#define KVM_CL_GPU_OF 4            /* a = item, ret = gpu|KVM_NONE  :238 */
+#define KVM_CL_SET_SIZE 5          /* a = request, b = bytes        :148 */
+#define KVM_CL_PUT_SIZE 6          /* sizes[a] = b (raw dict write)       */
+#define KVM_CL_DEL_SIZE 7          /* del sizes[a]                        */
+#define KVM_CL_NEW_GROUP 8         /* ret = gid                     :241 */
+#define KVM_CL_GROUP_ADD 9         /* a = gid, b = request          :159 */
+#define KVM_CL_GROUP_REMOVE 10     /* a = gid, b = request          :168 */
+#define KVM_CL_DEL_GROUP 11        /* del groups[a]                       */
+#define KVM_CL_ITEM_SIZE 12        /*                               :143 */
+#define KVM_CL_ITEM_CLASS 13       /*                               :177 */
+#define KVM_CL_USED_BYTES 14       /*                               :183 */
+#define KVM_CL_GPU_CLASS 15        /*                               :254 */
+#define KVM_CL_GPU_FAMILY 16       /*                               :261 */
+#define KVM_CL_LATEST_OF_FAMILY 17 /* a = class, ret = gpu|KVM_NONE :276 */
+#define KVM_CL_CHECK_CAPACITY 18   /*                               :293 */
+#define KVM_CL_ITEM_OF_REQUEST 19  /*                               :248 */
+#define KVM_CL_SET_ACTIVATION_SEQ 20      /* gpus[a].activation_seq = b    */
+#define KVM_CL_SET_NEXT_ACTIVATION_SEQ 21 /* next_activation_seq = a       */
+#define KVM_CL_VERSION 22          /* mutation counter (snapshot cache key) */
+#define KVM_CL_CLASSIFY 23         /* classify_request(a, b)        :72  */
+/* kvm_sched_op ops: MellScheduler public operations */
+#define KVM_SCHED_ALLOCATE 0      /* ids[0], size   scheduler.py:641 */
+#define KVM_SCHED_DEPART 1        /* ids[0]         scheduler.py:684 */
+#define KVM_SCHED_UPDATE 2        /* ids[0]         scheduler.py:774 */
+#define KVM_SCHED_HANDLE_GROWTH 3 /* ids[0..n)      scheduler.py:852 */
+#define KVM_SCHED_DUMP_CLASSES 4  /* scheduled_class as KVM_REC_CLASS records, by item */
+
+typedef struct kvm_cluster kvm_cluster;
+typedef struct kvm_sched kvm_sched;
+typedef struct kvm_sched_params { /* PriorityConfig (scheduler.py:48-62) + batching */
+  double weight_free_mem;
+  double weight_request_count;
+  double weight_same_machine;
+  int32_t batching;
+  int32_t _pad;
+} kvm_sched_params;
+
+/* ClusterState(capacity_bytes, gpus_per_machine)          model.py:122-139 */
+int kvm_cluster_create(int64_t capacity_bytes, int64_t gpus_per_machine, kvm_cluster** out);
+void kvm_cluster_destroy(kvm_cluster* cluster);
+int kvm_cluster_op(kvm_cluster* cluster, int op, int64_t a, int64_t b, int64_t* ret);
+/* terminate_idle_gpus (model.py:215-219): ids valid until the next call */
+int kvm_cluster_terminate_idle(kvm_cluster* cluster, const int64_t** ids, int64_t* n);
+int kvm_cluster_snapshot(kvm_cluster* cluster, const int64_t** recs, int64_t* n_recs);
+/* verify_properties (scheduler.py:102-191); n_exempt < 0 = default exemption
+ * (latest GPU per category); out = n pairs {gpu, KVM_VIOLATION_*} */
+int kvm_cluster_verify(kvm_cluster* cluster, const int64_t* exempt, int64_t n_exempt, const int64_t** pairs,
+                       int64_t* n);
+/* MellScheduler(cluster, priority_cfg, batching)      scheduler.py:220-229.
+ * The cluster must outlive the scheduler. */
+int kvm_sched_create(kvm_cluster* cluster, const kvm_sched_params* params, kvm_sched** out);
+void kvm_sched_destroy(kvm_sched* sched);
+int kvm_sched_set_batching(kvm_sched* sched, int batching);
+/* step_epoch(arrivals, completions, growths)         scheduler.py:979-1007
+ * arrivals / growths: n pairs {request, bytes}; completions: n ids. */
+int kvm_sched_step_epoch(kvm_sched* sched, const int64_t* arrivals, int64_t n_arrivals,
+                         const int64_t* completions, int64_t n_completions, const int64_t* growths,
+                         int64_t n_growths, const int64_t** recs, int64_t* n_recs);
+int kvm_sched_op(kvm_sched* sched, int op, const int64_t* ids, int64_t n_ids, int64_t size,
+                 const int64_t** recs, int64_t* n_recs);
+/* scheduled_class.get(item): KVM_CLASS_* or -1 */
+int kvm_sched_class_of(kvm_sched* sched, int64_t item, int32_t* cls);
+/* allocation_priority(dst) when src == KVM_NONE, else migration_priority(src, dst)
+ * (scheduler.py:68-84) */
+int kvm_sched_priority(kvm_sched* sched, int64_t src, int64_t dst, double* out);
 
 /* --- instrumentation -------------------------------------------------------- */
 /* Number of data-path kernels this process has launched through the ABI. */

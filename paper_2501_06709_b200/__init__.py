@@ -3,7 +3,9 @@
 Drop-in for the reference's migration path (`kvpack.migration` +
 the sim.py:207-227 data plane): the planner API keeps the reference's names;
 the KV pools, block tables and executor carry out the plan on sm_100a kernels
-in libkvmig.so (include/kvmig.h).  See DESIGN.md.
+in libkvmig.so (include/kvmig.h); the online scheduler that emits the moves
+(`MellScheduler`, `ClusterState`) is the reference's, restated natively in
+C++ in the same library.  See DESIGN.md.
 """
 from .errors import (ConfigError, KvmCudaError, KvmUnsupported, KvPackError, NativeLibraryMissing,
                      NoCategory, NotPlaced, ParseError, RequestTooLarge)
@@ -19,11 +21,25 @@ __all__ = [
 ]
 
 
+# the online scheduler and its cluster model (native, csrc/scheduler.cpp)
+_CLUSTER_NAMES = ("ClusterState", "GpuState", "MultiItemGroup", "SizeClass", "Request", "kv_size_at",
+                  "classify_request", "classify_gpu", "request_weight", "total_weight", "active_gpu_count")
+_SCHED_NAMES = ("MellScheduler", "PriorityConfig", "DEFAULT_PRIORITY", "Move", "OperationLog", "EpochResult",
+                "allocation_priority", "migration_priority", "Violation", "verify_properties",
+                "batch_operations")
+
+
 def __getattr__(name):  # data-path objects load the native library lazily
     if name in ("KVPool", "BlockTable", "BlockAllocator", "ModelShape", "LLAMA2_7B",
                 "LLAMA2_13B", "LLAMA3_70B", "SHAPES"):
         from . import kvcache
         return getattr(kvcache, name)
+    if name in _CLUSTER_NAMES:
+        from . import cluster
+        return getattr(cluster, name)
+    if name in _SCHED_NAMES:
+        from . import scheduler
+        return getattr(scheduler, name)
     if name in ("MigrationExecutor", "ExecReport", "ExecRecord", "Residency"):
         from . import executor
         return getattr(executor, name)

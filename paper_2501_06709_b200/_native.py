@@ -10,7 +10,8 @@ import ctypes
 import os
 import threading
 
-from .errors import ConfigError, KvmCudaError, KvmUnsupported, NativeLibraryMissing, NotPlaced
+from .errors import (ConfigError, KvmCudaError, KvmUnsupported, NativeLibraryMissing, NoCategory, NotPlaced,
+                     RequestTooLarge)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libkvmig.so")
@@ -21,6 +22,11 @@ KVM_ERR_CONFIG = -2
 KVM_ERR_CUDA = -3
 KVM_ERR_NOT_FOUND = -4
 KVM_ERR_UNSUPPORTED = -5
+KVM_ERR_KEY = -6
+KVM_ERR_TOO_LARGE = -7
+KVM_ERR_NO_CATEGORY = -8
+KVM_ERR_ASSERT = -9
+KVM_NONE = -(2 ** 63)
 
 KVM_F_BLOCKS_ON_HOST = 0x1
 KVM_F_ENGINE_BULK = 0x2
@@ -38,6 +44,10 @@ EXPORTS = (
     "kvm_ipc_export", "kvm_ipc_import", "kvm_ipc_close",
     "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_paged_decode",
     "kvm_plan_hybrid", "kvm_wait_flag_timeout", "kvm_split_migrate", "kvm_launch_count",
+    "kvm_cluster_create", "kvm_cluster_destroy", "kvm_cluster_op", "kvm_cluster_terminate_idle",
+    "kvm_cluster_snapshot", "kvm_cluster_verify", "kvm_sched_create", "kvm_sched_destroy",
+    "kvm_sched_set_batching", "kvm_sched_step_epoch", "kvm_sched_op", "kvm_sched_class_of",
+    "kvm_sched_priority",
 )
 KVM_DECODE_BF16 = 0x1
 KVM_DECODE_CUDA_CORES = 0x2
@@ -105,6 +115,12 @@ class PlanLedgers(ctypes.Structure):
                 ("dest_key", ctypes.c_void_p), ("dest_used", ctypes.c_void_p)]
 
 
+class SchedParams(ctypes.Structure):
+    _fields_ = [("weight_free_mem", ctypes.c_double), ("weight_request_count", ctypes.c_double),
+                ("weight_same_machine", ctypes.c_double), ("batching", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -134,6 +150,19 @@ def _declare(L: ctypes.CDLL) -> None:
         "kvm_plan_hybrid": ([ctypes.POINTER(Pending), I, ctypes.POINTER(PlanParams), ctypes.POINTER(Planned),
                              ctypes.POINTER(PlanLedgers)], I),
         "kvm_launch_count": ([], I64),
+        "kvm_cluster_create": ([I64, I64, ctypes.POINTER(P)], I),
+        "kvm_cluster_destroy": ([P], None),
+        "kvm_cluster_op": ([P, I, I64, I64, ctypes.POINTER(I64)], I),
+        "kvm_cluster_terminate_idle": ([P, ctypes.POINTER(P), ctypes.POINTER(I64)], I),
+        "kvm_cluster_snapshot": ([P, ctypes.POINTER(P), ctypes.POINTER(I64)], I),
+        "kvm_cluster_verify": ([P, P, I64, ctypes.POINTER(P), ctypes.POINTER(I64)], I),
+        "kvm_sched_create": ([P, ctypes.POINTER(SchedParams), ctypes.POINTER(P)], I),
+        "kvm_sched_destroy": ([P], None),
+        "kvm_sched_set_batching": ([P, I], I),
+        "kvm_sched_step_epoch": ([P, P, I64, P, I64, P, I64, ctypes.POINTER(P), ctypes.POINTER(I64)], I),
+        "kvm_sched_op": ([P, I, P, I64, I64, ctypes.POINTER(P), ctypes.POINTER(I64)], I),
+        "kvm_sched_class_of": ([P, I64, ctypes.POINTER(ctypes.c_int32)], I),
+        "kvm_sched_priority": ([P, I64, I64, ctypes.POINTER(ctypes.c_double)], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -172,7 +201,23 @@ def check(rc: int, what: str = "") -> int:
         raise NotPlaced(text)
     if rc == KVM_ERR_UNSUPPORTED:
         raise KvmUnsupported(text)
+    if rc == KVM_ERR_KEY:
+        raise KeyError(text)
+    if rc == KVM_ERR_TOO_LARGE:
+        raise RequestTooLarge(text)
+    if rc == KVM_ERR_NO_CATEGORY:
+        raise NoCategory(text)
+    if rc == KVM_ERR_ASSERT:
+        raise AssertionError(text)
     raise KvmCudaError(text)
+
+
+def records(ptr: ctypes.c_void_p, n: ctypes.c_int64, width: int = 5) -> list:
+    """Copy a library-owned int64 record buffer (n records of `width` words)."""
+    count = int(n.value) * width
+    if count == 0:
+        return []
+    return ctypes.cast(ptr, ctypes.POINTER(ctypes.c_int64))[:count]
 
 
 def launch_count() -> int:

@@ -8,9 +8,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libkvmig.so")
-SOURCES = ["kvmig.cu", "reprefill.cu", "attention.cu", "planner.cpp"]
+SOURCES = ["kvmig.cu", "reprefill.cu", "attention.cu", "planner.cpp", "scheduler.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared", "--expt-relaxed-constexpr"]
 
 
 def _stale() -> bool:

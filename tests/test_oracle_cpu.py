@@ -124,7 +124,7 @@ def test_oracle_reprefill_matches_numpy():
 def _header_symbols():
     with open(os.path.join(ROOT, "include", "kvmig.h")) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(kvm_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(kvm_\w+)\(", text, re.M)))
 
 
 def test_abi_library_exports_every_header_symbol():

@@ -30,3 +30,21 @@ def test_reference_tests_pass_with_our_planner(test_file, tmp_path):
                          capture_output=True, text=True, env=env, cwd=str(tmp_path), timeout=600)
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
     assert " passed" in out.stdout and "failed" not in out.stdout
+
+
+def test_entire_reference_suite_with_native_scheduler(tmp_path):
+    """Every reference test (scheduler, model, sim, acceptance sweeps, oracle,
+    baselines, CLI, ...) with BOTH the planner and the native C++ scheduler /
+    cluster model (paper_2501_06709_b200.scheduler, .cluster) swapped into
+    kvpack (KVPACK_PATCH_SCHEDULER=1 in tests/refsuite/patch_kvpack.py)."""
+    if not os.path.isdir(REF):
+        pytest.skip("reference tree not mounted")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([os.path.join(REF, "src"), os.path.join(HERE, "refsuite"),
+                                         env.get("PYTHONPATH", "")])
+    env["KVPACK_PATCH_SCHEDULER"] = "1"
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "patch_kvpack", "-p", "no:cacheprovider",
+                          "--rootdir", str(tmp_path), os.path.join(REF, "tests")],
+                         capture_output=True, text=True, env=env, cwd=str(tmp_path), timeout=1200)
+    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
+    assert " passed" in out.stdout and "failed" not in out.stdout
