@@ -79,6 +79,111 @@ def tokens_at(rec, slot: int, tokens_per_slot: int) -> int:
     return prompt + min(response, tokens_per_slot * max(0, slot - arrival))
 
 
+class Fingerprints:
+    """Per-request KV fingerprints on an executor's pools: every block a
+    request owns holds a value that depends on (request, logical block, layer,
+    K|V), written when the block is gained; `verify()` checks every resident
+    request still reads back its own values wherever it now lives (requests
+    whose KV was re-prefilled are skipped: their bytes are recomputed, not
+    copied)."""
+
+    def __init__(self, executor):
+        self.ex = executor
+        self.recomputed: set = set()
+        self._stamped: Dict[int, int] = {}   # rid -> number of blocks stamped
+
+    def stamp(self, rid: int) -> None:
+        """Write the fingerprint into blocks the request gained since last time."""
+        if rid in self.recomputed:
+            return
+        import torch
+
+        r = self.ex.where(rid)
+        start = self._stamped.get(rid, 0)
+        if start >= len(r.blocks):
+            return
+        pool = self.ex.pool(r.gpu, r.model)
+        idx = torch.from_numpy(r.blocks[start:].astype(np.int64)).to(pool.tensor.device)
+        pool.tensor.view(torch.int16)[:, :, idx] = self.values(rid, start, len(r.blocks), pool)
+        self._stamped[rid] = len(r.blocks)
+
+    def forget(self, rid: int) -> None:
+        self._stamped.pop(rid, None)
+        self.recomputed.discard(rid)
+
+    @staticmethod
+    def values(rid, lo, hi, pool):
+        import torch
+
+        L = pool.shape.layers
+        dev = pool.tensor.device
+        i = torch.arange(lo, hi, device=dev, dtype=torch.int32)
+        base = (rid * 7919 + i * 104729) % 16381
+        lay = torch.arange(L, device=dev, dtype=torch.int32)[:, None, None] * 2
+        kv = torch.arange(2, device=dev, dtype=torch.int32)[None, :, None]
+        v = (base[None, None, :] * 2 + lay * 3 + kv) % 32749 - 16374
+        return v.to(torch.int16)[..., None, None, None].expand(L, 2, hi - lo, *pool.view_shape[3:])
+
+    def verify(self) -> int:
+        """Number of resident requests checked; raises on the first mismatch."""
+        import torch
+
+        n = 0
+        for rid, r in self.ex.loc.items():
+            if rid in self.recomputed:
+                continue
+            pool = self.ex.pool(r.gpu, r.model)
+            got = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(r.blocks.astype(np.int64)).to(
+                pool.tensor.device)]
+            if not torch.equal(got, self.values(rid, 0, len(r.blocks), pool)):
+                raise AssertionError(f"request {rid} on GPU {r.gpu}: KV bytes differ from its fingerprint")
+            n += 1
+        return n
+
+
+class FingerprintedExecutor:
+    """Executor proxy for the live loop (runtime.run_slots): the same
+    admit / grow / release / execute calls, with every block a request gains
+    fingerprinted so `verify()` can prove the migrated bytes are intact."""
+
+    def __init__(self, executor):
+        self.ex = executor
+        self.fp = Fingerprints(executor)
+        self.reports: list = []
+
+    @property
+    def loc(self):
+        return self.ex.loc
+
+    def admit(self, rid, gpu, tokens, model=None):
+        r = self.ex.admit(rid, gpu, tokens, model=model)
+        self.fp.stamp(rid)
+        return r
+
+    def grow(self, rid, tokens):
+        r = self.ex.grow(rid, tokens)
+        self.fp.stamp(rid)
+        return r
+
+    def release(self, rid):
+        self.ex.release(rid)
+        self.fp.forget(rid)
+
+    def execute(self, plan, members_of=None):
+        report = self.ex.execute(plan, members_of=members_of)
+        for rec in report.records:
+            if rec.mode == TOKEN_TRANSFER:
+                self.fp.recomputed.update(rec.requests)
+        self.reports.append(report)
+        return report
+
+    def verify(self) -> int:
+        import torch
+
+        torch.cuda.synchronize()
+        return self.fp.verify()
+
+
 class TraceReplay:
     """Drive a MigrationExecutor with a recorded reference run."""
 
@@ -99,8 +204,8 @@ class TraceReplay:
         self.model_bpt: Dict[str, int] = dict(fixture.get("model_bpt", {}))
         # fixture model name -> executor pool key (e.g. a down-scaled shape's name)
         self.model_map: Dict[str, str] = dict(model_map or {})
-        self.recomputed: set = set()
-        self._stamped: Dict[int, int] = {}   # rid -> number of blocks stamped
+        self.fp = Fingerprints(executor)
+        self.recomputed = self.fp.recomputed
         self.reports: list = []              # per-slot ExecReport (None if nothing executed)
 
     def bpt_of(self, rid: int) -> int:
@@ -109,50 +214,11 @@ class TraceReplay:
 
     # -- fingerprints ------------------------------------------------------------
     def _stamp(self, rid: int) -> None:
-        """Write the fingerprint into blocks the request gained since last time."""
-        if not self.fingerprint or rid in self.recomputed:
-            return
-        import torch
-
-        r = self.ex.where(rid)
-        start = self._stamped.get(rid, 0)
-        if start >= len(r.blocks):
-            return
-        pool = self.ex.pool(r.gpu, r.model)
-        idx = torch.from_numpy(r.blocks[start:].astype(np.int64)).to(pool.tensor.device)
-        vals = self._values(rid, start, len(r.blocks), pool)
-        pool.tensor.view(torch.int16)[:, :, idx] = vals
-        self._stamped[rid] = len(r.blocks)
-
-    @staticmethod
-    def _values(rid, lo, hi, pool):
-        import torch
-
-        L = pool.shape.layers
-        dev = pool.tensor.device
-        i = torch.arange(lo, hi, device=dev, dtype=torch.int32)
-        base = (rid * 7919 + i * 104729) % 16381
-        lay = torch.arange(L, device=dev, dtype=torch.int32)[:, None, None] * 2
-        kv = torch.arange(2, device=dev, dtype=torch.int32)[None, :, None]
-        v = (base[None, None, :] * 2 + lay * 3 + kv) % 32749 - 16374
-        return v.to(torch.int16)[..., None, None, None].expand(L, 2, hi - lo, *pool.view_shape[3:])
+        if self.fingerprint:
+            self.fp.stamp(rid)
 
     def verify(self) -> int:
-        """Every resident (not re-prefilled) request reads back its fingerprint."""
-        import torch
-
-        n = 0
-        for rid, r in self.ex.loc.items():
-            if rid in self.recomputed or not self.fingerprint:
-                continue
-            pool = self.ex.pool(r.gpu, r.model)
-            got = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(r.blocks.astype(np.int64)).to(
-                pool.tensor.device)]
-            exp = self._values(rid, 0, len(r.blocks), pool)
-            if not torch.equal(got, exp):
-                raise AssertionError(f"request {rid} on GPU {r.gpu}: KV bytes differ from its fingerprint")
-            n += 1
-        return n
+        return self.fp.verify() if self.fingerprint else 0
 
     # -- the slot loop -------------------------------------------------------------
     def run(self, max_slots: Optional[int] = None, verify_every: int = 0) -> ReplayReport:
@@ -169,8 +235,7 @@ class TraceReplay:
             for rid in list(ev["done"]) + list(ev["gone"]):
                 if rid in ex.loc:
                     ex.release(rid)
-                    self._stamped.pop(rid, None)
-                    self.recomputed.discard(rid)
+                    self.fp.forget(rid)
             # 2. decode growth of resident requests on their physical GPU
             for rid in list(ex.loc):
                 if rid in self.trace:
