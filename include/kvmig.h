@@ -122,8 +122,12 @@ typedef struct kvm_reprefill_args {
   const int32_t* dst_blocks; /* device, n_dst_blocks entries */
   uint32_t* done_flag;    /* optional, set to done_value when all layers landed */
   uint32_t done_value;
-  int32_t flags;          /* reserved, 0 */
+  int32_t flags;          /* 0 or KVM_REPREFILL_SINGLE_CTA */
 } kvm_reprefill_args;
+/* kvm_reprefill engine: default = CTA-pair kernel (tcgen05 cta_group::2, features
+ * on M, tokens on N, 256 x 256 tiles); this flag selects the single-CTA kernel
+ * (M = 128 tokens, N = 256 features), which is also the split kernel's GEMM. */
+#define KVM_REPREFILL_SINGLE_CTA 0x1
 
 /* Adaptive split migration in ONE kernel on the destination GPU (extension of
  * the reference's all-or-nothing choice, migration.py:155-169): the first
@@ -149,7 +153,7 @@ typedef struct kvm_split_args {
   int32_t* dst_table_row; /* optional */
   uint32_t* done_flag;    /* optional */
   uint32_t done_value;
-  int32_t flags;          /* reserved, 0 */
+  int32_t flags;          /* 0 or KVM_REPREFILL_SINGLE_CTA (GEMM engine) */
 } kvm_split_args;
 
 /* Paged-attention decode over a pool (the consumer of a migrated cache):

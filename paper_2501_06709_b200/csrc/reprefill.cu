@@ -52,16 +52,17 @@ constexpr uint32_t TMEM_COLS = 512;
 
 struct Params {
   CUtensorMap tmap_x;  // [rows][d_model] bf16, box {64, 128}
-  CUtensorMap tmap_w;  // [layers][n_out][d_model] bf16, box {64, 256, 1}
+  CUtensorMap tmap_w;  // [layers][n_out][d_model] bf16, box {64, 256, 1} (pair kernel: {64, 128, 1})
   uint8_t* pool;
   __nv_bfloat16* q_out;
   const int32_t* dst_blocks;
   uint32_t* done_flag;
   uint32_t* ctr;
+  uint32_t* tile_ctr;   // pair kernel: dynamic tile counter (self-resetting)
   int64_t plane_bytes;  // num_blocks * piece_bytes
   int64_t piece_bytes;
   int32_t rows, n_out, d_model, layers, q_cols, kvd, tok0, block_tokens, n_dst_blocks;
-  int32_t m_tiles, n_tiles, k_blocks, total_tiles;
+  int32_t m_tiles, n_tiles, k_blocks, total_tiles;  // pair kernel: m = 256-feature tiles, n = 256-token tiles
   uint32_t done_value;
   // fused split migration (kvm_split_migrate): the transferred prefix, streamed by
   // warps 2-3 while the tensor cores re-prefill the suffix
@@ -405,6 +406,360 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair kernel (cta_group::2): features on M, tokens on N
+// ---------------------------------------------------------------------------
+// D^T[f, t] = W[l][f, :] . X[t, :] with the two SMs of a TPC cooperating on one
+// 256 x 256 tile: each CTA stages 128 weight rows (A) and half of the token
+// tile (B) per k-block, so the per-SM shared-memory traffic per MMA is half of
+// the single-CTA kernel's (which is shared-memory-bandwidth bound at
+// M=128/N=256).  Tokens on N make the tile exact for any token count (N is a
+// multiple of 16, no 128-row padding of the suffix), and n_out (a multiple of
+// 256 for every Llama shape) fills M.  The accumulator holds features on TMEM
+// lanes and tokens on columns, so the epilogue transposes each 32 x 32 block
+// through a warp-private shared-memory tile before writing 64-byte token rows
+// into the paged pool.
+namespace pair {
+constexpr int BM = 256, BN = 256, BK = 64, STAGES = 6;
+constexpr int A_BYTES = 128 * BK * 2;                 // this CTA's 128 weight rows
+constexpr int B_BYTES = 128 * BK * 2;                 // this CTA's half of the token tile (box rows)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;        // 32 KiB
+constexpr int EPI_BYTES = 4 * 32 * 32 * 2;            // 4 warps x [32 tokens][32 features] bf16
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 1024;
+constexpr uint32_t TMEM_COLS = 512;                   // two 128 x 256 fp32 accumulators per CTA
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's smem, completing bytes on the leader CTA's barrier
+__device__ __forceinline__ void tma_2d_pair(const CUtensorMap* m, uint32_t bar_cluster, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_pair(const CUtensorMap* m, uint32_t bar_cluster, void* dst, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// arrive on the barrier at this offset in both CTAs once the issued MMAs complete
+__device__ __forceinline__ void commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+// wait on a local barrier whose arrivals may come from the peer CTA (cluster-scope acquire)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Dynamic tile schedule shared by the pair: the leader's producer takes the next
+// tile from a global counter and broadcasts it through a small ring in both
+// CTAs' shared memory; every role of both CTAs consumes the same sequence.  (A
+// static stride lets pairs drift apart: with a partial token tile every
+// n_tiles tiles, pairs whose stride residue skips it run ahead, which idles SMs
+// at the tail and breaks the L2 reuse of weight tiles.)
+constexpr int TQ = 4;
+constexpr uint32_t TQ_CONSUMERS = 10;  // leader: MMA + 4 epilogue warps; peer: producer + 4 epilogue warps
+struct TileQueue {
+  uint64_t* full;   // [TQ], both CTAs
+  uint64_t* empty;  // [TQ], used in the leader
+  int32_t* slot;    // [TQ], both CTAs
+  int i;
+  uint32_t ph;
+  __device__ __forceinline__ int next(bool arrive_empty) {  // consumer side
+    mbar_wait_cluster(full + i, ph);
+    const int t = *(volatile int32_t*)(slot + i);
+    if (arrive_empty) arrive_remote(mapa(smem_u32(empty + i), 0));
+    if (++i == TQ) i = 0, ph ^= 1;
+    return t;
+  }
+};
+__device__ __forceinline__ uint32_t idesc(int n) {  // kind::f16, D=f32, A=B=bf16 K-major, M=256
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void decode_pair(const Params& p, int t, int& l, int& mt, int& nt) {
+  const int per_layer = p.m_tiles * p.n_tiles;  // tokens fastest: consecutive tiles share a weight tile
+  l = t / per_layer;
+  const int r = t - l * per_layer;
+  mt = r / p.n_tiles;
+  nt = r - mt * p.n_tiles;
+}
+__device__ __forceinline__ int tile_n(const Params& p, int nt) {  // MMA N of a token tile (multiple of 16)
+  const int left = min(BN, p.rows - nt * BN);
+  return (left + 15) & ~15;
+}
+
+template <bool kCopy>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefill_pair_kernel(
+    const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi = smem + STAGES * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  TileQueue tq;
+  tq.full = tempty + 2;
+  tq.empty = tq.full + TQ;
+  tq.slot = reinterpret_cast<int32_t*>(tq.empty + TQ);
+  tq.i = 0;
+  tq.ph = 0;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq.slot + TQ);
+  __shared__ int s_last;
+  __shared__ int s_copy_next;  // next copy unit (CTA-local index) of the fused prefix transfer
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+
+  if (warp == 0 && lane == 0) {
+    if (p.total_tiles > 0) {  // (a split migration with no suffix has no tensor maps)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_x) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_w) : "memory");
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);   // leader: its own arrive.expect_tx (both CTAs' bytes complete on it)
+      mbar_init(empty + s, 1);  // both: the leader's multicast MMA commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);      // both: multicast commit
+      mbar_init(tempty + a, 256);   // leader: 128 epilogue threads of each CTA
+    }
+    for (int i = 0; i < TQ; ++i) {
+      mbar_init(tq.full + i, 1);
+      mbar_init(tq.empty + i, TQ_CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x == 0) s_copy_next = 0;
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs: own smem, leader's barrier) ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      while (true) {
+        int t;
+        if (rank == 0) {  // take the next tile and broadcast it to both CTAs
+          mbar_wait(tq.empty + tq.i, tq.ph ^ 1);
+          t = (int)atomicAdd(p.tile_ctr, 1u);
+          tq.slot[tq.i] = t;
+          st_cluster_u32(mapa(smem_u32(tq.slot + tq.i), 1), (uint32_t)t);
+          mbar_arrive(tq.full + tq.i);
+          arrive_remote(mapa(smem_u32(tq.full + tq.i), 1));
+          if (++tq.i == TQ) tq.i = 0, tq.ph ^= 1;
+        } else {
+          t = tq.next(true);
+        }
+        if (t >= p.total_tiles) break;
+        int l, mt, nt;
+        decode_pair(p, t, l, mt, nt);
+        const int half = tile_n(p, nt) >> 1;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          if (rank == 0) mbar_expect_tx(full + stage, 2 * STAGE_BYTES);
+          const uint32_t bar = mapa(smem_u32(full + stage), 0);
+          tma_3d_pair(&p.tmap_w, bar, sa, kb * BK, mt * BM + (int)rank * 128, l);
+          tma_2d_pair(&p.tmap_x, bar, sb, kb * BK, nt * BN + (int)rank * half);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader CTA only) ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = tq.next(true); t < p.total_tiles; t = tq.next(true)) {
+        int l, mt, nt;
+        decode_pair(p, t, l, mt, nt);
+        const uint32_t id = idesc(tile_n(p, nt));
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_pair(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), id, (kb | k) != 0);
+          commit_both(empty + stage);  // both CTAs may refill this stage once the MMAs read it
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        commit_both(tfull + acc);  // both CTAs' accumulator halves are ready
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (kCopy && (warp == 2 || warp == 3)) {
+    // fused split migration: warps idle in the GEMM stream the transferred prefix
+    while (copy_one_unit(p, &s_copy_next, lane)) {
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> bf16 -> smem transpose -> paged pool ----------------
+    const int q = warp & 3;
+    bool copying = kCopy;
+    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(epi + q * 32 * 32 * 2);  // [32 tokens][32 features]
+    const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    while (true) {
+      const int slot = tq.i;
+      const int t = tq.next(false);
+      __syncwarp();
+      if (lane == 0) arrive_remote(mapa(smem_u32(tq.empty + slot), 0));
+      if (t >= p.total_tiles) break;
+      int l, mt, nt;
+      decode_pair(p, t, l, mt, nt);
+      // fused split migration: stream prefix copy units while this tile computes
+      while (copying && !mbar_test(tfull + acc, acc_phase)) copying = copy_one_unit(p, &s_copy_next, lane);
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int f0 = mt * BM + (int)rank * 128 + q * 32;  // this warp's 32 features
+      const int n_tok = min(BN, p.rows - nt * BN);
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
+      // destination of features [f0, f0 + 32) for a token: Q (dense) or the K / V row in the pool
+      int kind = -1;  // 0: Q, 1: K, 2: V
+      int fcol = 0;
+      if (f0 < p.q_cols) {
+        kind = p.q_out ? 0 : -1;
+        fcol = f0;
+      } else if (f0 < p.n_out) {
+        const int kc = f0 - p.q_cols;
+        kind = kc >= p.kvd ? 2 : 1;
+        fcol = kc - (kind == 2 ? p.kvd : 0);
+      }
+      const int chunks = (n_tok + 31) >> 5;
+#pragma unroll 1
+      for (int c = 0; c < chunks; ++c) {
+        uint32_t r[32];
+        TMEM_LD_32x32b_X32(taddr + c * 32, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (kind < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tile[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int tr = 8 * i + (lane >> 2);          // token row of the 32 x 32 block
+          const int tok_i = nt * BN + c * 32 + tr;      // token index within the suffix
+          const uint4 v = *reinterpret_cast<const uint4*>(tile + tr * 32 + (lane & 3) * 8);
+          if (tok_i < p.rows) {
+            uint8_t* dst;
+            if (kind == 0) {
+              dst = reinterpret_cast<uint8_t*>(p.q_out + ((int64_t)l * p.rows + tok_i) * p.q_cols + fcol);
+            } else {
+              const int tok = p.tok0 + tok_i;
+              const int blk = __ldg(p.dst_blocks + tok / p.block_tokens);
+              dst = p.pool + ((int64_t)l * 2 + (kind - 1)) * p.plane_bytes + (int64_t)blk * p.piece_bytes +
+                    (int64_t)(tok % p.block_tokens) * p.kvd * 2 + (int64_t)fcol * 2;
+            }
+            *reinterpret_cast<uint4*>(dst + (lane & 3) * 16) = v;
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      arrive_remote(tempty_leader + (uint32_t)(acc * 8));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    while (copying) copying = copy_one_unit(p, &s_copy_next, lane);  // GEMM done: finish the copy
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's MMAs / TMEM reads are done before either CTA deallocates
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    const uint32_t old = atomicAdd(p.ctr, 1u);
+    s_last = (old + 1 == gridDim.x);
+    if (s_last) {
+      *p.ctr = 0;
+      *p.tile_ctr = 0;  // every CTA has left its tile loop
+      fence_acq_rel_sys();
+    }
+  }
+  __syncthreads();
+  if (s_last) {  // the last CTA rewrites the destination block-table row, then publishes
+    if (p.table_row)
+      for (int i = threadIdx.x; i < p.table_n; i += THREADS) p.table_row[i] = __ldg(p.dst_blocks + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      if (p.done_flag) st_release_sys_u32(p.done_flag, p.done_value);
+    }
+  }
+}
+}  // namespace pair
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -424,7 +779,7 @@ static EncodeTiled encode_fn() {
 }
 
 struct DevCtr {
-  uint32_t* ctr = nullptr;  // 64 self-resetting completion counters, one per in-flight launch
+  uint32_t* ctr = nullptr;  // 64 self-resetting completion counters (one per in-flight launch) + 64 tile counters
   uint32_t next = 0;
   bool attr = false;
 };
@@ -432,9 +787,11 @@ struct DevCtr {
 // Encode X / W tensor maps and the GEMM geometry.  Returns KVM_OK or an error code.
 static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
                              int n_dst_blocks, const void* x, const void* w, void* q_out,
-                             const int32_t* dst_blocks);
+                             const int32_t* dst_blocks, bool pair = false);
 // Launch on the pool's device (current device already set); grid = min(work, SMs).
 static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream);
+// CTA-pair kernel: grid = 2 x min(work, co-resident clusters).
+static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream);
 static DevCtr g_ctr[64];
 static std::mutex g_rp_mu;
 
@@ -449,7 +806,7 @@ namespace rp {
 
 static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
                              int n_dst_blocks, const void* x, const void* w, void* q_out,
-                             const int32_t* dst_blocks) {
+                             const int32_t* dst_blocks, bool pair) {
   const kvm_pool_desc& d = pool->desc;
   const int kvd = d.kv_heads * d.head_dim;
   EncodeTiled enc = encode_fn();
@@ -466,7 +823,7 @@ static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model,
     if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuTensorMapEncodeTiled(x) failed: " + std::to_string((int)r));
     cuuint64_t wd[3] = {(cuuint64_t)d_model, (cuuint64_t)n_out, (cuuint64_t)d.layers};
     cuuint64_t ws[2] = {(cuuint64_t)d_model * 2, (cuuint64_t)d_model * 2 * n_out};
-    cuuint32_t wb[3] = {BK, BN, 1};
+    cuuint32_t wb[3] = {BK, pair ? 128u : (cuuint32_t)BN, 1};
     cuuint32_t we[3] = {1, 1, 1};
     r = enc(&p.tmap_w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), wd, ws, wb, we,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -487,8 +844,13 @@ static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model,
   p.tok0 = tok0;
   p.block_tokens = d.block_tokens;
   p.n_dst_blocks = n_dst_blocks;
-  p.m_tiles = (rows + BM - 1) / BM;
-  p.n_tiles = (n_out + BN - 1) / BN;
+  if (pair) {  // M = features (256 per CTA pair), N = tokens (256)
+    p.m_tiles = (n_out + pair::BM - 1) / pair::BM;
+    p.n_tiles = (rows + pair::BN - 1) / pair::BN;
+  } else {
+    p.m_tiles = (rows + BM - 1) / BM;
+    p.n_tiles = (n_out + BN - 1) / BN;
+  }
   p.k_blocks = d_model / BK;
   const int64_t total = (int64_t)p.m_tiles * p.n_tiles * d.layers;
   if (total > 0x7fffffff) return fail(KVM_ERR_INVALID, "problem too large");
@@ -500,8 +862,8 @@ static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(g_rp_mu);
   DevCtr& dc = g_ctr[dev];
   if (!dc.ctr) {
-    KVM_CUDA_TRY(cudaMalloc(&dc.ctr, 64 * sizeof(uint32_t)));
-    KVM_CUDA_TRY(cudaMemset(dc.ctr, 0, 64 * sizeof(uint32_t)));
+    KVM_CUDA_TRY(cudaMalloc(&dc.ctr, 128 * sizeof(uint32_t)));
+    KVM_CUDA_TRY(cudaMemset(dc.ctr, 0, 128 * sizeof(uint32_t)));
   }
   if (!dc.attr) {
     KVM_CUDA_TRY(cudaFuncSetAttribute(reprefill_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -518,6 +880,46 @@ static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
     reprefill_kernel<true><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
   else
     reprefill_kernel<false><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
+  KVM_CUDA_TRY(cudaGetLastError());
+  count_launch();
+  return KVM_OK;
+}
+
+static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
+  static bool attr[64] = {};
+  static int clusters[64] = {};
+  std::lock_guard<std::mutex> lk(g_rp_mu);
+  DevCtr& dc = g_ctr[dev];
+  if (!dc.ctr) {
+    KVM_CUDA_TRY(cudaMalloc(&dc.ctr, 128 * sizeof(uint32_t)));
+    KVM_CUDA_TRY(cudaMemset(dc.ctr, 0, 128 * sizeof(uint32_t)));
+  }
+  if (!attr[dev]) {
+    KVM_CUDA_TRY(cudaFuncSetAttribute(pair::reprefill_pair_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES));
+    KVM_CUDA_TRY(cudaFuncSetAttribute(pair::reprefill_pair_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (sm_count(dev) / 2));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = pair::SMEM_BYTES;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, pair::reprefill_pair_kernel<false>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = sm_count(dev) / 2;
+    }
+    clusters[dev] = n;
+    attr[dev] = true;
+  }
+  p.tile_ctr = dc.ctr + 64 + (dc.next % 64);
+  p.ctr = dc.ctr + (dc.next++ % 64);
+  int64_t work = p.total_tiles;
+  if (copy) work = std::max<int64_t>(work, (p.c_units + 3) / 4);  // ~4 copy warps per cluster
+  const int grid = 2 * (int)std::max<int64_t>(1, std::min<int64_t>(work, clusters[dev]));
+  if (copy)
+    pair::reprefill_pair_kernel<true><<<grid, THREADS, pair::SMEM_BYTES, stream>>>(p);
+  else
+    pair::reprefill_pair_kernel<false><<<grid, THREADS, pair::SMEM_BYTES, stream>>>(p);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
   return KVM_OK;
@@ -558,18 +960,20 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a->x || !a->w || !a->dst_blocks) return fail(KVM_ERR_INVALID, "NULL x/w/dst_blocks");
   if ((int64_t)(a->tok0 + a->rows) > (int64_t)a->n_dst_blocks * d.block_tokens)
     return fail(KVM_ERR_INVALID, "dst_blocks do not cover tok0 + rows tokens");
-  if (a->flags != 0) return fail(KVM_ERR_INVALID, "flags must be 0");
+  if (a->flags & ~KVM_REPREFILL_SINGLE_CTA) return fail(KVM_ERR_INVALID, "unknown flags");
   if (reinterpret_cast<uintptr_t>(a->x) % 16 || reinterpret_cast<uintptr_t>(a->w) % 16)
     return fail(KVM_ERR_INVALID, "x and w must be 16-byte aligned");
   DevScope ds(pool->device);
   if (!is_sm100(pool->device)) return fail(KVM_ERR_UNSUPPORTED, "kvm_reprefill needs an sm_100 (B200) device");
   Params p;
   memset(&p, 0, sizeof(p));
+  const bool pair_kernel = !(a->flags & KVM_REPREFILL_SINGLE_CTA);
   int rc = build_gemm_params(p, pool, a->rows, a->d_model, a->q_cols, a->tok0, a->n_dst_blocks, a->x, a->w,
-                             a->q_out, a->dst_blocks);
+                             a->q_out, a->dst_blocks, pair_kernel);
   if (rc) return rc;
   p.done_flag = a->done_flag;
   p.done_value = a->done_value;
+  if (pair_kernel) return launch_pair(p, pool->device, false, static_cast<cudaStream_t>(stream));
   return launch_gemm(p, pool->device, false, static_cast<cudaStream_t>(stream));
 }
 
@@ -597,14 +1001,15 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
     return fail(KVM_ERR_CONFIG, "kv_heads*head_dim and q_cols must be multiples of 32");
   if (!a->dst_blocks || (a->prefix_blocks && !a->src_blocks) || (suffix && (!a->x || !a->w)))
     return fail(KVM_ERR_INVALID, "NULL pointer argument");
-  if (a->flags != 0) return fail(KVM_ERR_INVALID, "flags must be 0");
+  if (a->flags & ~KVM_REPREFILL_SINGLE_CTA) return fail(KVM_ERR_INVALID, "unknown flags");
   if (a->tokens == 0) return KVM_OK;
   DevScope ds(dst->device);
   if (!is_sm100(dst->device)) return fail(KVM_ERR_UNSUPPORTED, "kvm_split_migrate needs an sm_100 (B200) device");
   Params p;
   memset(&p, 0, sizeof(p));
+  const bool pair_kernel = !(a->flags & KVM_REPREFILL_SINGLE_CTA);
   int rc = build_gemm_params(p, dst, suffix, a->d_model, a->q_cols, a->prefix_blocks * bt, n_blocks, a->x, a->w,
-                             a->q_out, a->dst_blocks);
+                             a->q_out, a->dst_blocks, pair_kernel);
   if (rc) return rc;
   p.done_flag = a->done_flag;
   p.done_value = a->done_value;
@@ -616,5 +1021,6 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   p.c_nblocks = a->prefix_blocks;
   p.c_upp = (int32_t)((dst->piece_bytes + CUNIT - 1) / CUNIT);
   p.c_units = (int64_t)2 * d.layers * a->prefix_blocks * p.c_upp;
+  if (pair_kernel) return launch_pair(p, dst->device, p.c_units > 0, static_cast<cudaStream_t>(stream));
   return launch_gemm(p, dst->device, p.c_units > 0, static_cast<cudaStream_t>(stream));
 }

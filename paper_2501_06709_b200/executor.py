@@ -261,9 +261,13 @@ class MigrationExecutor:
             self._pending_commit = post
         return report
 
-    def compact(self, rid: int, wait: bool = True) -> ExecRecord:
+    def compact(self, rid: int, wait: bool = True, row_out=None) -> ExecRecord:
         """1-GPU case: move a request into the lowest free blocks of its own
-        pool (defragmentation; kvm_compact = migrate with src pool == dst pool)."""
+        pool (defragmentation; kvm_compact = migrate with src pool == dst pool).
+
+        row_out: optional pinned host int32 tensor; the rewritten block-table
+        row is copied into it on the same stream right after the kernel, so one
+        synchronize covers the move and the read-back."""
         res = self._res(rid)
         pool = self.pool(res.gpu, res.model)
         nb = len(res.blocks)
@@ -279,6 +283,13 @@ class MigrationExecutor:
             pool.pool_id, sb.ctypes.data, dst.ctypes.data, nb, ctypes.c_void_p(row),
             _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag, ctypes.c_void_p(s.cuda_stream)),
             "kvm_compact")
+        if row_out is not None:
+            if table is None:
+                raise ConfigError("row_out needs a block table on this GPU")
+            import torch
+
+            with torch.cuda.stream(s):
+                row_out[:nb].copy_(table.rows[table.slot(rid), :nb], non_blocking=True)
         rec = ExecRecord(rid, res.gpu, res.gpu, "compact", [rid], nb,
                          nb * pool.shape.piece_bytes * 2 * pool.shape.layers, 0)
         post = [(rid, res.gpu, res.tokens, dst)]

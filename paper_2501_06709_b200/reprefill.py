@@ -45,12 +45,13 @@ def synthetic_hidden(shape: ModelShape, rows: int, device: int, seed: int = 2):
 
 
 def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=None,
-              done_flag: int = 0, done_value: int = 1) -> None:
+              done_flag: int = 0, done_value: int = 1, single_cta: bool = False) -> None:
     """Launch kvm_reprefill: K/V of tokens [tok0, tok0 + rows) into `dst_blocks`.
 
     x: bf16 [rows][d_model] (device), w: bf16 [layers][n_out][d_model] with
     n_out = q_cols + 2 * kv_cols, dst_blocks: int32 device tensor covering the
-    token range, q_out: optional bf16 [layers][rows][q_cols].
+    token range, q_out: optional bf16 [layers][rows][q_cols].  single_cta
+    selects the single-CTA kernel instead of the default CTA-pair one.
     """
     import torch
 
@@ -77,7 +78,8 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
     a.x, a.w = x.data_ptr(), w.data_ptr()
     a.q_out = q_out.data_ptr() if q_out is not None else None
     a.dst_blocks = dst_blocks.data_ptr()
-    a.done_flag, a.done_value, a.flags = done_flag or None, done_value, 0
+    a.done_flag, a.done_value = done_flag or None, done_value
+    a.flags = _native.KVM_REPREFILL_SINGLE_CTA if single_cta else 0
     s = stream if stream is not None else torch.cuda.current_stream(pool.device)
     _native.check(_native.lib().kvm_reprefill(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),
                   "kvm_reprefill")

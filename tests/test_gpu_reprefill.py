@@ -43,9 +43,10 @@ def _check(shape, pool, blocks, tok0, rows, ref, q_out, before):
     assert torch.equal(after[:, :, mask], before[:, :, mask])
 
 
+@pytest.mark.parametrize("single_cta", [False, True])
 @pytest.mark.parametrize("rows,tok0,with_q", [(1, 0, True), (77, 5, True), (128, 0, False),
-                                              (300, 21, True), (513, 16, False)])
-def test_reprefill_small_shapes(rows, tok0, with_q):
+                                              (300, 21, True), (513, 16, False), (1000, 3, True)])
+def test_reprefill_small_shapes(rows, tok0, with_q, single_cta):
     shape = ModelShape("rp", layers=3, kv_heads=4, head_dim=64, q_heads=8, d_model=256)
     nblk = (tok0 + rows + 15) // 16
     nb = nblk + 10
@@ -56,12 +57,13 @@ def test_reprefill_small_shapes(rows, tok0, with_q):
     x = synthetic_hidden(shape, rows, 0, seed=rows)
     w = synthetic_weights(shape, 0, with_q=with_q, seed=rows + 1)
     q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda") if with_q else None
-    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q)
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q, single_cta=single_cta)
     torch.cuda.synchronize()
     _check(shape, pool, blocks, tok0, rows, _ref(x, w), q, before)
 
 
-def test_reprefill_matches_c_oracle():
+@pytest.mark.parametrize("single_cta", [False, True])
+def test_reprefill_matches_c_oracle(single_cta):
     shape = ModelShape("rp", layers=2, kv_heads=2, head_dim=64, q_heads=2, d_model=128)
     rows, tok0, nb = 40, 3, 6
     pool = KVPool(shape, nb, dtype=torch.bfloat16)
@@ -70,7 +72,7 @@ def test_reprefill_matches_c_oracle():
     x = synthetic_hidden(shape, rows, 0, seed=9)
     w = synthetic_weights(shape, 0, with_q=True, seed=10)
     q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda")
-    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q)
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q, single_cta=single_cta)
     torch.cuda.synchronize()
     exp = np.zeros(pool.view_shape, dtype=np.uint16)
     q_exp = np.zeros((shape.layers, rows, shape.q_cols), dtype=np.uint16)
@@ -83,7 +85,8 @@ def test_reprefill_matches_c_oracle():
     torch.testing.assert_close(q.float().cpu(), to_f(q_exp.reshape(-1)).view(q_exp.shape), atol=ATOL, rtol=RTOL)
 
 
-def test_reprefill_13b_balanced_split():
+@pytest.mark.parametrize("single_cta", [False, True])
+def test_reprefill_13b_balanced_split(single_cta):
     """BASELINE configs[2]: 13B, suffix of s ~ 1.4k tokens of an 8k request."""
     shape = LLAMA2_13B
     rows, tok0 = 1360, 8192 - 1360
@@ -95,7 +98,7 @@ def test_reprefill_13b_balanced_split():
     x = synthetic_hidden(shape, rows, 0, seed=2)
     w = synthetic_weights(shape, 0, with_q=True, seed=3)
     before = pool.tensor.view(torch.int16).clone()
-    reprefill(pool, x, w, blocks, tok0=tok0)
+    reprefill(pool, x, w, blocks, tok0=tok0, single_cta=single_cta)
     torch.cuda.synchronize()
     # check a sample of layers against fp32 (full einsum over 40 layers is 8.6 TFLOP)
     kvd, qc = shape.kv_cols, shape.q_cols
@@ -114,8 +117,9 @@ def test_reprefill_13b_balanced_split():
     assert torch.equal(after[:, :, mask], before[:, :, mask])
 
 
+@pytest.mark.parametrize("single_cta", [False, True])
 @pytest.mark.parametrize("kv_heads,head_dim,q_heads", [(3, 64, 1), (1, 32, 3), (5, 96, 0)])
-def test_reprefill_n_not_multiple_of_tile(kv_heads, head_dim, q_heads):
+def test_reprefill_n_not_multiple_of_tile(kv_heads, head_dim, q_heads, single_cta):
     """n_out = q_cols + 2*kv_cols not a multiple of the 256-column N tile."""
     shape = ModelShape("nt", layers=2, kv_heads=kv_heads, head_dim=head_dim, q_heads=max(q_heads, 1), d_model=128)
     rows, tok0 = 50, 7
@@ -128,6 +132,6 @@ def test_reprefill_n_not_multiple_of_tile(kv_heads, head_dim, q_heads):
     x = synthetic_hidden(shape, rows, 0, seed=3)
     w = synthetic_weights(shape, 0, with_q=q_heads > 0, seed=4)
     assert w.shape[1] % 256 != 0
-    reprefill(pool, x, w, blocks, tok0=tok0)
+    reprefill(pool, x, w, blocks, tok0=tok0, single_cta=single_cta)
     torch.cuda.synchronize()
     _check(shape, pool, blocks, tok0, rows, _ref(x, w), None, before)

@@ -55,9 +55,10 @@ def test_split_migration(tokens, suffix):
     assert flags.cpu().tolist() == [7 if pre else 0, 7 if suffix else 0]
 
 
+@pytest.mark.parametrize("single_cta", [False, True])
 @pytest.mark.parametrize("tokens,suffix", [(1024, 240), (1000, 232), (512, 0), (512, 512), (16 * 40, None),
                                            (4096, 1024)])
-def test_fused_split_migration(tokens, suffix):
+def test_fused_split_migration(tokens, suffix, single_cta):
     """kvm_split_migrate: one launch; prefix copied by the GEMM's idle warps."""
     from paper_2501_06709_b200.split import split_migrate_fused
 
@@ -77,7 +78,7 @@ def test_fused_split_migration(tokens, suffix):
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
     table = BlockTable(1, plan.total_blocks)
     split_migrate_fused(src, dst, sb, db, plan, x, w, table_row=table.row_ptr(0), done_flag=flag.data_ptr(),
-                        done_value=9)
+                        done_value=9, single_cta=single_cta)
     torch.cuda.synchronize()
     pre = plan.prefix_blocks
     assert torch.equal(dst.tensor[:, :, db[:pre].long()].view(torch.int16),

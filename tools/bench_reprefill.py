@@ -51,9 +51,11 @@ def main():
 
     with torch.cuda.stream(s):
         ms = timeit(lambda: reprefill(pool, x, w, blocks, stream=s))
-        out = {"kernel": "reprefill_kernel (tcgen05)", "shape": a.shape, "rows": rows,
+        ms1 = timeit(lambda: reprefill(pool, x, w, blocks, stream=s, single_cta=True))
+        out = {"kernel": "reprefill_pair_kernel (tcgen05 cta_group::2)", "shape": a.shape, "rows": rows,
                "kv_only": a.kv_only, "flops": flops, "ms": round(ms, 4),
-               "tflops": round(flops / ms / 1e9, 1)}
+               "tflops": round(flops / ms / 1e9, 1),
+               "single_cta_ms": round(ms1, 4), "single_cta_tflops": round(flops / ms1 / 1e9, 1)}
         if not a.no_cublas:
             y = torch.empty(rows, w.shape[1], dtype=torch.bfloat16, device="cuda")
 

@@ -140,6 +140,8 @@ def main():
         exact_fused = bool(torch.equal(dst.tensor[:, :, db[:plan.prefix_blocks].long()].view(torch.int16),
                                        src.tensor[:, :, pi].view(torch.int16)))
         t_fused = timeit(run_fused)
+        t_fused_single = timeit(lambda: split_migrate_fused(src, dst, sbd, db, plan, x, w, stream=sbs,
+                                                            single_cta=True))
         t_split = timeit(lambda: run_split(True))
         t_serial = timeit(lambda: run_split(False))
         t_full = timeit(run_full)
@@ -151,6 +153,7 @@ def main():
         "kv_bytes": kv_bytes, "prefix_bytes": plan.prefix_tokens * shape.kv_bytes_per_token,
         "suffix_flops": plan.suffix * fpt,
         "ms": {"split_fused_one_kernel": round(t_fused, 4),
+               "split_fused_one_kernel_single_cta_gemm": round(t_fused_single, 4),
                "split_overlapped_1gpu": round(t_split, 4), "split_serialized_1gpu": round(t_serial, 4),
                "full_transfer_1gpu": round(t_full, 4), "prefix_transfer_only": round(t_prefix, 4),
                "suffix_reprefill_only": round(t_suffix, 4)},
