@@ -239,6 +239,7 @@ def run_ours(args) -> int:
     ri = rank_info_from_env()
     world = ri.world
     ndev = torch.cuda.device_count()
+    shared_gpu = world > 1 and ndev < world
     device = ri.local_rank % max(ndev, 1)
     torch.cuda.set_device(device)
     if world > 1:
@@ -309,7 +310,13 @@ def run_ours(args) -> int:
         m = make_move(host, fwd=(i % 2 == 0))
         _native.check(lib.kvm_migrate(ctypes.byref(m), 1, eng | (_native.KVM_F_BLOCKS_ON_HOST if host else 0),
                                       sptr))
-        if world > 1:   # wait for the incoming transfer from recv_from (dst-visible completion);
+        if world > 1 and shared_gpu:
+            # test mode, several ranks on ONE GPU: a device-side spin on the incoming flag can starve
+            # the peer process's context (no time-slicing of a running kernel was observed), so the
+            # receive completes on the host: own push done, then every rank has pushed.
+            stream.synchronize()
+            barrier()
+        elif world > 1:   # wait for the incoming transfer from recv_from (dst-visible completion);
             # bounded (30 s) so a lost peer write fails the run instead of wedging the GPU
             _native.check(lib.kvm_wait_flag_timeout(ctypes.c_void_p(mailbox.data_ptr()), seq[0],
                                                     30_000_000_000, ctypes.c_void_p(mailbox.data_ptr() + 4 * 63),
@@ -326,6 +333,9 @@ def run_ours(args) -> int:
         return int(acc.item())
 
     sent = gathered_checksum(sb_np)
+    # every rank's pool (and the blocks it receives into) is initialised before any peer pushes into it
+    torch.cuda.synchronize()
+    barrier()
     with torch.cuda.stream(stream):
         step(0, host=False)
     stream.synchronize()
@@ -338,6 +348,11 @@ def run_ours(args) -> int:
         ok = got == sums[ri.recv_from] and bool(torch.equal(rowbuf.cpu(), torch.from_numpy(db_np)))
     if world > 1 and int(mailbox[63].item()) != 0:
         raise RuntimeError(f"rank {ri.rank}: incoming transfer from rank {ri.recv_from} timed out")
+    if not ok:
+        print(f"rank {ri.rank}: parity gate failed: received checksum {got}, sent "
+              f"{sums[ri.recv_from] if world > 1 else sent}, table row ok "
+              f"{bool(torch.equal(rowbuf.cpu(), torch.from_numpy(db_np))) if world > 1 else None}",
+              file=sys.stderr)
     bit_exact = allreduce_max(0.0 if ok else 1.0, device) == 0.0
     seq[0] = 0
     mailbox.zero_()

@@ -575,7 +575,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  __syncthreads();  // (also orders the TMEM-address write for racecheck)
+  cluster_sync();   // barriers of both CTAs initialised, TMEM allocated in both
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 

@@ -48,3 +48,25 @@ def test_gpu_arm_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * 32 * 4 and e["d2h_bytes_per_step"] == 32 * 4
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks_contract():
+    """The N>1 launch (torchrun, one process per rank): on a 1-GPU box both ranks
+    share the GPU (CUDA-IPC ring push, host-side receive); rank 0 prints one line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--workload", "7b-512", "--steps", "5", "--warmup", "3",
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= set(d) and d["n_gpus"] == 2 and d["bit_exact"] is True and d["value"] > 0
+    assert d["e2e"]["value"] > 0
