@@ -1,0 +1,125 @@
+/*
+ * A non-Python host driving the C ABI (include/kvmig.h) directly: the native
+ * scheduler emits moves for a tiny trace, and -- when a GPU is present -- one
+ * paged-KV move is executed with kvm_compact and checked byte for byte.
+ *
+ *   gcc -std=c99 -O2 -I include tools/c_host_demo.c \
+ *       -L paper_2501_06709_b200/_lib -lkvmig -Wl,-rpath,$PWD/paper_2501_06709_b200/_lib -o c_host_demo
+ *   ./c_host_demo            # scheduler (CPU) + migration (GPU, if any)
+ *   ./c_host_demo --cpu-only
+ *
+ * Exit status 0 on success.  This is what a C/C++/Go/Java host binds (the
+ * reference itself is Python; INTEGRATION.md shows its ctypes stub).
+ */
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "kvmig.h"
+
+/* cudart, declared here so the demo builds without the CUDA headers */
+extern int cudaMalloc(void** p, size_t n);
+extern int cudaFree(void* p);
+extern int cudaMemcpy(void* dst, const void* src, size_t n, int kind);
+extern int cudaDeviceSynchronize(void);
+#define H2D 1
+#define D2H 2
+
+static int check(int rc, const char* what) {
+  if (rc < 0) {
+    fprintf(stderr, "%s failed (%d): %s\n", what, rc, kvm_last_error());
+    exit(1);
+  }
+  return rc;
+}
+
+static const char* REASON[] = {"allocate", "l-fill", "depart-refill", "update", "batch"};
+
+static int scheduler_demo(void) {
+  /* ClusterState(capacity=120000 B, 4 GPUs per machine); MellScheduler with the
+   * reference's default priorities and batching (scheduler.py:48-62, 220-229) */
+  kvm_cluster* cl = NULL;
+  kvm_sched* sc = NULL;
+  kvm_sched_params prm = {1.0, 0.25, 0.5, 1, 0};
+  check(kvm_cluster_create(120000, 4, &cl), "kvm_cluster_create");
+  check(kvm_sched_create(cl, &prm, &sc), "kvm_sched_create");
+  /* epoch 1: four arrivals (request, bytes): one per size class */
+  int64_t arr[] = {1, 72000, 2, 45000, 3, 30100, 4, 7500};
+  const int64_t* rec = NULL;
+  int64_t n = 0;
+  check(kvm_sched_step_epoch(sc, arr, 4, NULL, 0, NULL, 0, &rec, &n), "step_epoch");
+  int moves = 0, fresh = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t* r = rec + 5 * i;
+    if (r[0] == KVM_REC_MOVE) {
+      ++moves;
+      fresh += r[2] == KVM_NONE;
+      printf("move item %lld -> GPU %lld (%s)\n", (long long)r[1], (long long)r[3], REASON[r[4]]);
+    }
+  }
+  /* epoch 2: request 2 completes, request 3 grows into an M-class item */
+  int64_t comp[] = {2};
+  int64_t grow[] = {3, 44000};
+  check(kvm_sched_step_epoch(sc, NULL, 0, comp, 1, grow, 1, &rec, &n), "step_epoch");
+  int migrations = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t* r = rec + 5 * i;
+    if (r[0] == KVM_REC_MOVE && r[2] != KVM_NONE) ++migrations;
+  }
+  int64_t gpu = 0;
+  check(kvm_cluster_op(cl, KVM_CL_GPU_OF, 1, 0, &gpu), "gpu_of");
+  /* errors come back as codes: an unknown request is NotPlaced */
+  const int64_t bad[] = {999};
+  int rc = kvm_sched_op(sc, KVM_SCHED_DEPART, bad, 1, 0, &rec, &n);
+  kvm_sched_destroy(sc);
+  kvm_cluster_destroy(cl);
+  printf("scheduler: %d placements (%d fresh), %d migrations in epoch 2, request 1 on GPU %lld, "
+         "depart(999) -> %d\n", moves, fresh, migrations, (long long)gpu, rc);
+  return (moves == 4 && fresh == 4 && rc == KVM_ERR_NOT_FOUND) ? 0 : 1;
+}
+
+static int migration_demo(void) {
+  int ndev = 0;
+  if (kvm_device_count(&ndev) < 0 || ndev == 0) {
+    printf("migration: no GPU, skipped\n");
+    return 0;
+  }
+  kvm_pool_desc d = {4, 8, 128, 16, 32, 2}; /* 4 layers, 8 kv heads x 128, 32 blocks of 16 tokens */
+  int64_t bytes = 0;
+  check(kvm_pool_bytes(&d, &bytes), "kvm_pool_bytes");
+  uint16_t* host = (uint16_t*)malloc((size_t)bytes);
+  uint16_t* back = (uint16_t*)malloc((size_t)bytes);
+  for (int64_t i = 0; i < bytes / 2; ++i) host[i] = (uint16_t)(i * 2654435761u >> 7);
+  void* dev = NULL;
+  if (cudaMalloc(&dev, (size_t)bytes) != 0) return 1;
+  cudaMemcpy(dev, host, (size_t)bytes, H2D);
+  int pool = check(kvm_pool_register(0, dev, &d), "kvm_pool_register");
+  int32_t src[] = {7, 3, 30, 12, 5};
+  int32_t dst[] = {0, 1, 2, 4, 6};
+  check(kvm_compact(pool, src, dst, 5, NULL, KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK, NULL), "kvm_compact");
+  cudaDeviceSynchronize();
+  cudaMemcpy(back, dev, (size_t)bytes, D2H);
+  int64_t piece = 0;
+  check(kvm_pool_piece_bytes(pool, &piece), "piece bytes");
+  int64_t plane = piece * d.num_blocks;
+  int bad = 0;
+  for (int p = 0; p < 2 * d.layers; ++p)
+    for (int b = 0; b < 5; ++b)
+      bad |= memcmp((char*)back + p * plane + dst[b] * piece, (char*)host + p * plane + src[b] * piece,
+                    (size_t)piece) != 0;
+  kvm_pool_unregister(pool);
+  cudaFree(dev);
+  free(host);
+  free(back);
+  printf("migration: 5 blocks x %d planes moved, %s\n", 2 * d.layers, bad ? "MISMATCH" : "bit-exact");
+  return bad;
+}
+
+int main(int argc, char** argv) {
+  int cpu_only = argc > 1 && strcmp(argv[1], "--cpu-only") == 0;
+  printf("libkvmig ABI %d\n", kvm_version());
+  int rc = scheduler_demo();
+  if (!cpu_only) rc |= migration_demo();
+  return rc;
+}
