@@ -135,3 +135,32 @@ def test_reprefill_n_not_multiple_of_tile(kv_heads, head_dim, q_heads, single_ct
     reprefill(pool, x, w, blocks, tok0=tok0, single_cta=single_cta)
     torch.cuda.synchronize()
     _check(shape, pool, blocks, tok0, rows, _ref(x, w), None, before)
+
+
+@pytest.mark.parametrize("shape_name,rows,tok0", [("llama3-70b-gqa", 2000, 16384 - 2000), ("llama2-7b", 3000, 100)])
+def test_reprefill_full_shapes_pair_kernel(shape_name, rows, tok0):
+    """The default CTA-pair kernel at the other model shapes (70B GQA: d_model 8192,
+    n_out 10240; 7B: 4096 / 12288), sampled layers against fp32, Q included."""
+    from paper_2501_06709_b200.kvcache import SHAPES
+
+    shape = SHAPES[shape_name]
+    nblk = (tok0 + rows + 15) // 16
+    nb = nblk + 4
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    blocks = torch.randperm(nb, generator=torch.Generator().manual_seed(7))[:nblk].to(torch.int32).cuda()
+    x = synthetic_hidden(shape, rows, 0, seed=11)
+    w = synthetic_weights(shape, 0, with_q=True, seed=12)
+    q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda")
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q)
+    torch.cuda.synchronize()
+    kvd, qc = shape.kv_cols, shape.q_cols
+    toks = torch.arange(tok0, tok0 + rows, device="cuda")
+    blk, slot = blocks.long()[toks // 16], toks % 16
+    for l in (0, shape.layers // 2, shape.layers - 1):
+        ref = x.float() @ w[l].float().t()
+        torch.testing.assert_close(q[l].float(), ref[:, :qc], atol=ATOL, rtol=RTOL)
+        torch.testing.assert_close(pool.tensor[l, 0, blk, slot].reshape(rows, kvd).float(), ref[:, qc:qc + kvd],
+                                   atol=ATOL, rtol=RTOL)
+        torch.testing.assert_close(pool.tensor[l, 1, blk, slot].reshape(rows, kvd).float(), ref[:, qc + kvd:],
+                                   atol=ATOL, rtol=RTOL)
