@@ -34,15 +34,29 @@ from .planner import PendingMove, plan_hybrid
 
 @dataclass
 class LoopResult:
+    """Per-slot series with the reference's MetricsSeries columns (sim.py:27-63):
+    active_gpus, migrations (= logical_moves), deferred, forced, used_bytes,
+    capacity_bytes; plus the executed plan rows and bytes physically moved."""
     plan_rows: List[list] = field(default_factory=list)   # (slot, item, src, dst, kv_bytes, tokens, mode)
     active_gpus: List[int] = field(default_factory=list)
     logical_moves: List[int] = field(default_factory=list)
     deferred: List[int] = field(default_factory=list)
     forced: List[int] = field(default_factory=list)
+    used_bytes: List[int] = field(default_factory=list)      # sim.py:231-234 (KV bytes that exist)
+    capacity_bytes: List[int] = field(default_factory=list)  # active GPUs x C
     bytes_moved: int = 0
     completed: int = 0
     rejected: int = 0
     aborted: int = 0
+
+    @property
+    def peak_gpus(self) -> int:
+        return max(self.active_gpus, default=0)
+
+    @property
+    def mean_utilization(self) -> float:
+        r = [u / c for u, c in zip(self.used_bytes, self.capacity_bytes) if c > 0]
+        return sum(r) / len(r) if r else 0.0
 
 
 def _completion_slot(arrival: int, response: int, tps: int) -> int:
@@ -169,7 +183,12 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
             defer_counts.pop(planned.move.item, None)
         for mv in plan.deferred:
             defer_counts[mv.item] = defer_counts.get(mv.item, 0) + 1
-        out.active_gpus.append(sum(1 for g in cluster.gpus.values() if g.residents))
+        active = sum(1 for g in cluster.gpus.values() if g.residents)
+        out.active_gpus.append(active)
+        sizes = cluster.sizes
+        out.used_bytes.append(sum(min(_size_at(rec, slot, tps, bpt_of(rid)), cluster.capacity_bytes)
+                                  for rid, rec in running.items() if rid in sizes))
+        out.capacity_bytes.append(active * cluster.capacity_bytes)
         out.logical_moves.append(n_moves)
         out.deferred.append(len(plan.deferred))
         out.forced.append(len(plan.forced))

@@ -179,3 +179,23 @@ def test_errors_and_views():
     assert osch.verify_properties(c) == []
     with pytest.raises(KeyError):
         c.place(3, 42)
+
+
+def test_loop_metrics_match_reference_sim():
+    """run_slots with the native scheduler reproduces kvpack.sim.run's whole
+    MetricsSeries (active_gpus, migrations, deferred, forced, used_bytes,
+    capacity_bytes) on the B200-shaped config, not only its plan rows."""
+    ref = _ref_or_skip()
+    from kvpack.config import config_from_dict
+    from kvpack.sim import run as ref_run
+
+    fx = load_golden("trace_7b_c48g_seed0.json")
+    doc = {"schema_version": 1, **{k: v for k, v in fx["config"].items()}}
+    cfg = config_from_dict(doc)
+    trace = ref.Trace(records=[ref.ArrivalRecord(*r) for r in fx["trace"]])
+    m = ref_run(cfg, trace).metrics
+    out = _loop(fx, fx["config"]["workload"]["kv_bytes_per_token"])
+    assert out.active_gpus == m.active_gpus and out.logical_moves == m.migrations
+    assert out.deferred == m.deferred and out.forced == m.forced
+    assert out.used_bytes == m.used_bytes and out.capacity_bytes == m.capacity_bytes
+    assert out.peak_gpus == m.peak_gpus and out.mean_utilization == m.mean_utilization
