@@ -63,6 +63,18 @@ class ExecRecord:
 class ExecReport:
     records: List[ExecRecord] = field(default_factory=list)
     launches: int = 0
+    # with MigrationExecutor(timing=True) and wait=True: device time per GPU from
+    # the first launch of this call to the last (CUDA events on the executor's
+    # stream), in ms
+    device_ms: Dict[int, float] = field(default_factory=dict)
+
+    @property
+    def copy_GBps(self) -> Optional[float]:
+        """Payload bytes copied / the slowest GPU's device time (None without timing)."""
+        if not self.device_ms:
+            return None
+        ms = max(self.device_ms.values())
+        return self.bytes_moved / ms / 1e6 if ms > 0 else None
 
     @property
     def bytes_moved(self) -> int:
@@ -88,9 +100,11 @@ class MigrationExecutor:
     """
 
     def __init__(self, pools: Dict[int, KVPool], tables: Optional[Dict[int, BlockTable]] = None,
-                 engine: str = "bulk", reprefill: Optional[Callable] = None):
+                 engine: str = "bulk", reprefill: Optional[Callable] = None, timing: bool = False):
         import torch
 
+        self.timing = timing
+        self._events: Dict[int, list] = {}
         if engine not in ENGINES:
             raise ConfigError(f"engine must be one of {sorted(ENGINES)}")
         if not pools:
@@ -134,7 +148,22 @@ class MigrationExecutor:
 
         s = self.stream(device)
         s.wait_stream(torch.cuda.current_stream(device))
+        if self.timing and device not in self._events:   # first launch on this GPU in this call
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            self._events[device] = [e0, None]
         return s
+
+    def _close_timing(self, report: "ExecReport") -> None:
+        import torch
+
+        for dev, ev in self._events.items():
+            ev[1] = torch.cuda.Event(enable_timing=True)
+            ev[1].record(self.stream(dev))
+        self.synchronize()
+        for dev, (e0, e1) in self._events.items():
+            report.device_ms[dev] = e0.elapsed_time(e1)
+        self._events = {}
 
     def synchronize(self) -> None:
         for s in self._streams.values():
@@ -202,6 +231,7 @@ class MigrationExecutor:
         executed: List[PlannedMove] = plan.executed if isinstance(plan, MigrationPlan) else [
             p for p in plan if p.mode != "deferred"]
         report = ExecReport()
+        self._events = {}
         by_dev: Dict[int, List[Tuple[_native.Move, int, int, np.ndarray, np.ndarray]]] = {}
         keep = []  # host arrays must outlive the kvm_migrate call
         post: List[Tuple[int, int, int, np.ndarray]] = []  # (rid, dst, tokens, dst_blocks)
@@ -255,6 +285,8 @@ class MigrationExecutor:
             self._launch_migrate(dev, moves)
             report.launches += 1
         if wait:
+            if self.timing:
+                self._close_timing(report)
             self.synchronize()
             self._commit(post)
         else:

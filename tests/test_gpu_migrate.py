@@ -222,7 +222,7 @@ def test_executor_plan_roundtrip():
 
     pools = {0: KVPool(SMALL, 64), 1: KVPool(SMALL, 64)}
     tables = {0: BlockTable(8, 16), 1: BlockTable(8, 16)}
-    ex = MigrationExecutor(pools, tables)
+    ex = MigrationExecutor(pools, tables, timing=True)
     _fill(pools[0], 8)
     ex.admit(10, 0, 50)
     ex.admit(11, 0, 17)
@@ -235,6 +235,7 @@ def test_executor_plan_roundtrip():
                        bounds, topo)
     rep = ex.execute(plan)
     assert rep.bytes_moved == (4 + 2) * 16 * bpt
+    assert set(rep.device_ms) == {0} and rep.device_ms[0] > 0 and rep.copy_GBps > 0
     dst_np = pools[1].tensor.view(torch.int16).cpu().numpy()
     for rid, sb in ((10, b10), (11, b11)):
         r = ex.where(rid)

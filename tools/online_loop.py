@@ -63,6 +63,7 @@ def main():
     shapes = MINI if a.shape == "mini" else FULL
     devices = list(range(torch.cuda.device_count()))
     inner, nb = build(fx, MINI_7B if a.shape == "mini" else LLAMA2_7B, a.engine, devices, shapes)
+    inner.timing = True          # per-call device time (CUDA events) in every ExecReport
     ex = FingerprintedExecutor(inner)
     clock = Clock()
     ex.execute = clock.wrap("executor", ex.execute)
@@ -98,6 +99,9 @@ def main():
         "fingerprint_checks": sum(checked),
         "ms_per_slot": {k: 1e3 * v / n for k, v in clock.t.items()} | {"loop": 1e3 * wall / n},
         "executor_GBps_while_moving": out.bytes_moved / clock.t.get("executor", 1e-9) / 1e9,
+        "device_ms_total": round(sum(max(r.device_ms.values(), default=0.0) for r in ex.reports), 3),
+        "device_copy_GBps": round(out.bytes_moved / max(1e-9, sum(max(r.device_ms.values(), default=0.0)
+                                                                for r in ex.reports)) / 1e6, 1),
     }))
     if not parity:
         raise SystemExit("decisions differ from the reference's recorded run")
