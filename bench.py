@@ -403,21 +403,37 @@ def run_ours(args) -> int:
         ex.loc[0] = Residency(0, sb_np.copy(), tokens, pool.shape.name)
         table.set_host(0, sb_np)
         # make device bytes consistent with the residency (content is irrelevant to timing)
-        row = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        rows = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
         for i in range(args.warmup):
-            ex.compact(0, row_out=row)
+            ex.compact(0, row_out=rows[0])
         torch.cuda.synchronize()
         e2e_lat = []
+        # every step: host block lists -> H2D -> kernel -> D2H of the rewritten block-table row,
+        # and the host waits for that row; the call is stream-ordered, so the host prepares step
+        # i+1 while the GPU still copies step i (double-buffered pinned rows)
         t0 = time.perf_counter()
+        prev = None
+        e2e_ok = True
         for i in range(K):
             ts = time.perf_counter()
-            # host block lists -> H2D -> kernel -> D2H of the rewritten block-table row -> sync
-            ex.compact(0, row_out=row)
-            e2e_lat.append(time.perf_counter() - ts)
-        torch.cuda.synchronize()
+            rec = ex.compact(0, row_out=rows[i & 1], stream_ordered=True)
+            if prev is not None:
+                prev[0].done.synchronize()
+                e2e_lat.append(time.perf_counter() - prev[1])
+                e2e_ok &= bool(np.array_equal(rows[(i - 1) & 1].numpy(), prev[2]))
+            prev = (rec, ts, ex.where(0).blocks.copy())
+        prev[0].done.synchronize()
+        e2e_lat.append(time.perf_counter() - prev[1])
         e2e_s = time.perf_counter() - t0
+        torch.cuda.synchronize()
         h2d, d2h = 2 * n * 4, n * 4
-        assert np.array_equal(row.numpy(), ex.where(0).blocks)
+        assert e2e_ok and np.array_equal(rows[(K - 1) & 1].numpy(), ex.where(0).blocks)
+        # per-call latency of one synchronous call (issue -> row on the host), not pipelined
+        e2e_lat = []
+        for i in range(min(K, 30)):
+            ts = time.perf_counter()
+            ex.compact(0, row_out=rows[0])
+            e2e_lat.append(time.perf_counter() - ts)
     else:
         row = torch.empty(n, dtype=torch.int32, pin_memory=True)
         torch.cuda.synchronize()
@@ -498,7 +514,9 @@ def run_ours(args) -> int:
             "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "latency_ms_p50": round(1e3 * statistics.median(e2e_lat), 4),
-                    "path": "MigrationExecutor.compact -> kvm_compact(host block lists) -> table row D2H"
+                    "latency_definition": "one synchronous call through the API: issue -> result row on the host",
+                    "path": "MigrationExecutor.compact(stream_ordered) -> kvm_compact(host block lists) -> "
+                            "table row D2H -> host waits for the row (next step issued meanwhile)"
                     if world == 1 else "kvm_migrate(host block lists) -> kvm_wait_flag -> table row D2H"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -274,6 +274,9 @@ int kvm_wait_flag_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout
                           void* stream);
 /* tcgen05 re-prefill projection (see kvm_reprefill_args). */
 int kvm_reprefill(const kvm_reprefill_args* args, void* stream);
+/* Asynchronous device -> host copy on `stream` (e.g. the block-table row a move
+ * rewrote, read back by the host in the same stream order as the move). */
+int kvm_read_back(void* host, const void* dev, int64_t bytes, void* stream);
 /* Fused split migration: prefix copy + suffix re-prefill in one launch. */
 int kvm_split_migrate(const kvm_split_args* args, void* stream);
 /* Paged-attention decode reading the (migrated) block tables. */

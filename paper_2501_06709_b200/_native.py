@@ -48,7 +48,7 @@ EXPORTS = (
     "kvm_cluster_create", "kvm_cluster_destroy", "kvm_cluster_op", "kvm_cluster_terminate_idle",
     "kvm_cluster_snapshot", "kvm_cluster_verify", "kvm_sched_create", "kvm_sched_destroy",
     "kvm_sched_set_batching", "kvm_sched_step_epoch", "kvm_sched_op", "kvm_sched_class_of",
-    "kvm_sched_priority",
+    "kvm_sched_priority", "kvm_read_back",
 )
 KVM_DECODE_BF16 = 0x1
 KVM_DECODE_CUDA_CORES = 0x2
@@ -164,6 +164,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kvm_sched_op": ([P, I, P, I64, I64, ctypes.POINTER(P), ctypes.POINTER(I64)], I),
         "kvm_sched_class_of": ([P, I64, ctypes.POINTER(ctypes.c_int32)], I),
         "kvm_sched_priority": ([P, I64, I64, ctypes.POINTER(ctypes.c_double)], I),
+        "kvm_read_back": ([P, P, I64, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

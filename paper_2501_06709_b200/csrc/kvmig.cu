@@ -877,6 +877,13 @@ int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream) {
   return kvm_wait_flag_timeout(flag, value, 0, nullptr, stream);
 }
 
+int kvm_read_back(void* host, const void* dev, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!host || !dev))) return fail(KVM_ERR_INVALID, "bad read-back arguments");
+  if (bytes == 0) return KVM_OK;
+  KVM_CUDA_TRY(cudaMemcpyAsync(host, dev, (size_t)bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+  return KVM_OK;
+}
+
 int kvm_wait_flag_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err_word,
                           void* stream) {
   if (!flag) return fail(KVM_ERR_INVALID, "flag is NULL");

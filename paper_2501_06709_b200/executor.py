@@ -57,6 +57,7 @@ class ExecRecord:
     tokens_recomputed: int
     tokens_moved: int = 0  # tokens of the members copied: algorithmic bytes = tokens_moved * bpt
     request_tokens: Dict[int, int] = field(default_factory=dict)  # per moved request: its tokens
+    done: Optional[object] = None  # stream-ordered calls: CUDA event recorded after the move (and read-back)
 
 
 @dataclass
@@ -293,13 +294,19 @@ class MigrationExecutor:
             self._pending_commit = post
         return report
 
-    def compact(self, rid: int, wait: bool = True, row_out=None) -> ExecRecord:
+    def compact(self, rid: int, wait: bool = True, row_out=None, stream_ordered: bool = False) -> ExecRecord:
         """1-GPU case: move a request into the lowest free blocks of its own
         pool (defragmentation; kvm_compact = migrate with src pool == dst pool).
 
         row_out: optional pinned host int32 tensor; the rewritten block-table
         row is copied into it on the same stream right after the kernel, so one
-        synchronize covers the move and the read-back."""
+        synchronize covers the move and the read-back.
+
+        stream_ordered: return right after issuing, with the residency already
+        updated on the host and `rec.done` an event that completes after the
+        move (and read-back).  Safe because every later launch touching this
+        pool is queued behind it on the executor's ordered stream; it lets the
+        host prepare the next call while the GPU copies."""
         res = self._res(rid)
         pool = self.pool(res.gpu, res.model)
         nb = len(res.blocks)
@@ -310,22 +317,28 @@ class MigrationExecutor:
         if table is not None:
             table.set_host(rid, dst)
             row = table.row_ptr(rid)
+        if row_out is not None and table is None:
+            raise ConfigError("row_out needs a block table on this GPU")
         s = self.ordered_stream(pool.device)
-        _native.check(_native.lib().kvm_compact(
-            pool.pool_id, sb.ctypes.data, dst.ctypes.data, nb, ctypes.c_void_p(row),
-            _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag, ctypes.c_void_p(s.cuda_stream)),
-            "kvm_compact")
-        if row_out is not None:
-            if table is None:
-                raise ConfigError("row_out needs a block table on this GPU")
-            import torch
-
-            with torch.cuda.stream(s):
-                row_out[:nb].copy_(table.rows[table.slot(rid), :nb], non_blocking=True)
+        lib = _native.lib()
+        sp = ctypes.c_void_p(s.cuda_stream)
+        _native.check(lib.kvm_compact(pool.pool_id, sb.ctypes.data, dst.ctypes.data, nb, ctypes.c_void_p(row),
+                                      _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag, sp), "kvm_compact")
+        if row_out is not None:   # D2H of the rewritten row, ordered after the kernel on the same stream
+            if row_out.numel() < nb or row_out.element_size() != 4 or not row_out.is_pinned():
+                raise ValueError("row_out must be a pinned host int32 tensor with >= n_blocks entries")
+            _native.check(lib.kvm_read_back(ctypes.c_void_p(row_out.data_ptr()), ctypes.c_void_p(row), 4 * nb, sp),
+                          "kvm_read_back")
         rec = ExecRecord(rid, res.gpu, res.gpu, "compact", [rid], nb,
                          nb * pool.shape.piece_bytes * 2 * pool.shape.layers, 0)
         post = [(rid, res.gpu, res.tokens, dst)]
-        if wait:
+        if stream_ordered:
+            import torch
+
+            rec.done = torch.cuda.Event()
+            rec.done.record(s)
+            self._commit(post, keep_table=True)
+        elif wait:
             s.synchronize()
             self._commit(post, keep_table=True)
         else:
