@@ -199,3 +199,26 @@ def test_loop_metrics_match_reference_sim():
     assert out.deferred == m.deferred and out.forced == m.forced
     assert out.used_bytes == m.used_bytes and out.capacity_bytes == m.capacity_bytes
     assert out.peak_gpus == m.peak_gpus and out.mean_utilization == m.mean_utilization
+
+
+def test_reference_default_run_fingerprint():
+    """The reference's DEFAULT run (sim defaults: C = 120 000 B, 4 GPUs/machine,
+    100 B/token, lambda 0.5, 200 slots, seed 0) from our generator + native
+    scheduler + planner: the plan-row fingerprint recorded with the reference in
+    SURVEY.md §8c (d0331a687103bf7e: 368 requests, peak 27 GPUs, 2 200 logical
+    moves, 1 578 executed)."""
+    import hashlib
+    import json
+
+    from paper_2501_06709_b200.workload import LengthDistribution, gen_poisson
+
+    tr = gen_poisson(0.5, 200, LengthDistribution(), 0)
+    c = ocl.ClusterState(120_000, 4)
+    s = osch.MellScheduler(c, osch.PriorityConfig(), batching=True)
+    topo = Topology(gpus_per_machine=4)
+    out = run_slots(tr.tuples(), s, c, topo, load_boundaries(topo, 1.0, 0.2), bpt=100, tokens_per_slot=10,
+                    duration_slots=200)
+    fp = hashlib.sha256(json.dumps([r[:7] for r in out.plan_rows]).encode()).hexdigest()[:16]
+    assert (len(tr), out.peak_gpus, sum(out.logical_moves)) == (368, 27, 2200)
+    assert sum(1 for r in out.plan_rows if r[6] != "deferred") == 1578
+    assert fp == "d0331a687103bf7e"
