@@ -198,3 +198,86 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
         if slot > horizon + 10 ** 6:
             raise RuntimeError("slot loop failed to drain")
     return out
+
+
+# The reference's run-config schema (config.py:20-128): section -> {key: default}.
+_CONFIG_DEFAULTS = {
+    "cluster": {"capacity_bytes": 120_000, "gpus_per_machine": 4, "max_gpus": 1024,
+                "intra_bandwidth_bytes_per_s": 50e9, "inter_bandwidth_bytes_per_s": 1.25e9,
+                "prefill_tokens_per_s": 10_000.0},
+    "scheduler": {"kind": "mell", "batching": True, "weight_free_mem": 1.0, "weight_request_count": 0.25,
+                  "weight_same_machine": 0.5, "rebalance_period": 1, "imbalance_threshold": 0.25},
+    "migration": {"epoch_seconds": 1.0, "budget_fraction": 0.2, "max_defer": 3},
+    "workload": {"trace_path": None, "mean_interarrival_slots": 0.5, "duration_slots": 200,
+                 "prompt_mean_log": 4.6, "prompt_sigma_log": 0.8, "response_mean_log": 5.3,
+                 "response_sigma_log": 0.9, "scale": 1, "kv_bytes_per_token": 100},
+    "sim": {"seed": 0, "tokens_per_slot": 10, "epoch_slots": 1},
+}
+
+
+def resolve_config(doc: Optional[dict] = None) -> Dict[str, dict]:
+    """A reference run-config document (config.py's JSON schema, sections
+    cluster / scheduler / migration / workload / sim) with the reference's
+    defaults filled in; unknown sections or keys raise ConfigError, like the
+    reference's strict loader (config.py:150-186)."""
+    from .errors import ConfigError
+
+    doc = dict(doc or {})
+    version = doc.pop("schema_version", 1)
+    if version != 1:
+        raise ConfigError(f"unsupported schema_version {version}, expected 1")
+    unknown = set(doc) - set(_CONFIG_DEFAULTS)
+    if unknown:
+        raise ConfigError(f"unknown top-level keys: {sorted(unknown)}")
+    out = {}
+    for name, defaults in _CONFIG_DEFAULTS.items():
+        sec = doc.get(name, {})
+        if not isinstance(sec, dict):
+            raise ConfigError(f"section {name!r} must be an object")
+        bad = set(sec) - set(defaults)
+        if bad:
+            raise ConfigError(f"unknown keys in section {name!r}: {sorted(bad)}")
+        out[name] = {**defaults, **sec}
+    return out
+
+
+def simulate(doc: Optional[dict] = None, records: Optional[Sequence[Tuple[int, int, int, int]]] = None, *,
+             executor=None, bpt=None, models: Optional[Dict[int, str]] = None,
+             on_slot: Optional[Callable[[int, list], None]] = None) -> LoopResult:
+    """Drop-in for the Mell path of the reference's `sim.run(config, trace)`
+    (sim.py:103-268): build ClusterState + the native MellScheduler, Topology
+    and Boundaries from a reference config document, generate the Poisson trace
+    from its workload section unless `records` are given, and run the live slot
+    loop (optionally executing every plan on the GPUs through `executor`).
+    `bpt` overrides workload.kv_bytes_per_token (an int, or a per-request dict
+    for multi-LLM traces).  Returns the reference's metric series (LoopResult)."""
+    from .cluster import ClusterState
+    from .errors import ConfigError
+    from .planner import Topology, load_boundaries
+    from .scheduler import MellScheduler, PriorityConfig
+    from .workload import LengthDistribution, gen_poisson
+
+    cfg = resolve_config(doc)
+    cl, sc, mg, wl, sm = (cfg[k] for k in ("cluster", "scheduler", "migration", "workload", "sim"))
+    if sc["kind"] != "mell":
+        raise ConfigError(f"scheduler kind {sc['kind']!r}: only Mell's scheduler is provided "
+                          "(the reference's bf/wf/lb baselines are out of scope)")
+    if records is None:
+        if wl["trace_path"] is not None:
+            raise ConfigError("trace files are not read here: pass `records`")
+        dist = LengthDistribution(prompt_mean_log=wl["prompt_mean_log"], prompt_sigma_log=wl["prompt_sigma_log"],
+                                  response_mean_log=wl["response_mean_log"],
+                                  response_sigma_log=wl["response_sigma_log"], scale=wl["scale"])
+        records = gen_poisson(wl["mean_interarrival_slots"], wl["duration_slots"], dist, sm["seed"]).tuples()
+    cluster = ClusterState(cl["capacity_bytes"], gpus_per_machine=cl["gpus_per_machine"])
+    sched = MellScheduler(cluster, PriorityConfig(sc["weight_free_mem"], sc["weight_request_count"],
+                                                  sc["weight_same_machine"]), batching=sc["batching"])
+    topo = Topology(gpus_per_machine=cl["gpus_per_machine"],
+                    intra_bandwidth_bytes_per_s=cl["intra_bandwidth_bytes_per_s"],
+                    inter_bandwidth_bytes_per_s=cl["inter_bandwidth_bytes_per_s"],
+                    prefill_tokens_per_s=cl["prefill_tokens_per_s"])
+    bounds = load_boundaries(topo, mg["epoch_seconds"], mg["budget_fraction"])
+    return run_slots(records, sched, cluster, topo, bounds, bpt=wl["kv_bytes_per_token"] if bpt is None else bpt,
+                     tokens_per_slot=sm["tokens_per_slot"], epoch_slots=sm["epoch_slots"],
+                     max_defer=mg["max_defer"], duration_slots=wl["duration_slots"], executor=executor,
+                     models=models, on_slot=on_slot)

@@ -222,3 +222,43 @@ def test_reference_default_run_fingerprint():
     assert (len(tr), out.peak_gpus, sum(out.logical_moves)) == (368, 27, 2200)
     assert sum(1 for r in out.plan_rows if r[6] != "deferred") == 1578
     assert fp == "d0331a687103bf7e"
+
+
+@pytest.mark.parametrize("doc", [
+    {},
+    {"cluster": {"capacity_bytes": 200_000, "gpus_per_machine": 2}, "scheduler": {"batching": False},
+     "sim": {"epoch_slots": 3, "seed": 4}},
+    {"cluster": {"capacity_bytes": 48 << 30, "gpus_per_machine": 8, "intra_bandwidth_bytes_per_s": 900e9,
+                 "inter_bandwidth_bytes_per_s": 50e9, "prefill_tokens_per_s": 50_000.0},
+     "migration": {"epoch_seconds": 0.05}, "workload": {"scale": 10, "kv_bytes_per_token": 524288,
+                                                        "duration_slots": 120},
+     "scheduler": {"weight_request_count": 0.0}, "sim": {"seed": 2}},
+])
+def test_simulate_matches_reference_sim_run(doc):
+    """runtime.simulate(config) == kvpack.sim.run(config, gen_poisson(...)) on the
+    reference's own config schema: every metric column and the plan rows."""
+    ref = _ref_or_skip()
+    from kvpack.config import config_from_dict
+    from kvpack.sim import run as ref_run
+
+    from paper_2501_06709_b200.runtime import simulate
+
+    cfg = config_from_dict(doc)
+    w = cfg.workload
+    trace = ref.gen_poisson(w.mean_interarrival_slots, w.duration_slots, ref.LengthDistribution(scale=w.scale),
+                            cfg.sim.seed)
+    m = ref_run(cfg, trace).metrics
+    out = simulate(doc)
+    assert out.active_gpus == m.active_gpus and out.logical_moves == m.migrations
+    assert out.deferred == m.deferred and out.forced == m.forced
+    assert out.used_bytes == m.used_bytes and out.capacity_bytes == m.capacity_bytes
+
+
+def test_simulate_rejects_unknown_config():
+    from paper_2501_06709_b200.errors import ConfigError
+    from paper_2501_06709_b200.runtime import simulate
+
+    with pytest.raises(ConfigError):
+        simulate({"cluster": {"bogus": 1}})
+    with pytest.raises(ConfigError):
+        simulate({"scheduler": {"kind": "lb"}})
