@@ -303,3 +303,32 @@ def test_wait_flag_timeout_reports_instead_of_hanging():
                                                       ctypes.c_void_p(s.cuda_stream)))
     s.synchronize()   # returns after ~20 ms although the flag never reaches 5
     assert flag.cpu().tolist() == [0, 1]
+
+
+def test_compact_stream_ordered_back_to_back():
+    """compact(stream_ordered=True) returns before the copy finishes, with the
+    residency already updated; back-to-back calls stay correct because every
+    launch on the pool is queued on the executor's ordered stream, and each
+    call's rewritten table row is read back (kvm_read_back) in stream order."""
+    from paper_2501_06709_b200.executor import MigrationExecutor
+
+    pool = KVPool(SMALL, 96)
+    table = BlockTable(2, 16)
+    ex = MigrationExecutor({0: pool}, {0: table})
+    _fill(pool, 3)
+    pool.allocator.take(range(0, 96, 3))     # scatter the free blocks
+    ex.admit(5, 0, 200)
+    orig_blocks = ex.where(5).blocks.copy()
+    orig = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(orig_blocks).long().cuda()].clone()
+    rows = [torch.empty(16, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    recs, expect = [], []
+    for i in range(6):
+        recs.append(ex.compact(5, row_out=rows[i & 1], stream_ordered=True))
+        expect.append(ex.where(5).blocks.copy())
+        if i >= 1:
+            recs[i - 1].done.synchronize()
+            assert np.array_equal(rows[(i - 1) & 1].numpy()[:len(expect[i - 1])], expect[i - 1])
+    recs[-1].done.synchronize()
+    assert np.array_equal(rows[1].numpy()[:len(expect[-1])], expect[-1])
+    now = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(ex.where(5).blocks).long().cuda()]
+    assert torch.equal(now, orig)
