@@ -236,19 +236,39 @@ class MigrationExecutor:
         by_dev: Dict[int, List[Tuple[_native.Move, int, int, np.ndarray, np.ndarray]]] = {}
         keep = []  # host arrays must outlive the kvm_migrate call
         post: List[Tuple[int, int, int, np.ndarray]] = []  # (rid, dst, tokens, dst_blocks)
-        for pm in executed:
+        # phase 1: validate every move and reserve all destination blocks; nothing is
+        # launched yet, so a failure (unknown mode, missing engine, a full pool) leaves
+        # the pools and tables exactly as they were
+        work = []  # (pm, rec, [(rid, res, src_pool, dst_pool, dst_blocks)])
+        taken = []  # (pool, blocks) reserved in this call, for rollback
+        try:
+            for pm in executed:
+                mv = pm.move
+                if pm.mode not in (KV_TRANSFER, FORCED_KV_TRANSFER, TOKEN_TRANSFER):
+                    raise ValueError(f"cannot execute mode {pm.mode!r}")
+                rids = list(members_of(mv.item)) if (members_of and mv.item < 0) else [mv.item]
+                here = [r for r in rids if r in self.loc and self.loc[r].gpu == mv.src]
+                if pm.mode == TOKEN_TRANSFER and self.reprefill is None and here and mv.src != mv.dst:
+                    raise ConfigError("token_transfer planned but executor has no re-prefill engine")
+                rec = ExecRecord(mv.item, mv.src, mv.dst, pm.mode, here, 0, 0, 0)
+                items = []
+                if mv.src != mv.dst:
+                    for rid in here:
+                        res = self.loc[rid]
+                        src_pool, dst_pool = self.pool(mv.src, res.model), self.pool(mv.dst, res.model)
+                        dst_blocks = dst_pool.allocator.alloc(len(res.blocks))
+                        taken.append((dst_pool, dst_blocks))
+                        items.append((rid, res, src_pool, dst_pool, dst_blocks))
+                work.append((pm, rec, items))
+        except Exception:
+            for pool, blocks in taken:
+                pool.allocator.free(blocks)
+            raise
+        # phase 2: launch
+        for pm, rec, items in work:
             mv = pm.move
-            rids = list(members_of(mv.item)) if (members_of and mv.item < 0) else [mv.item]
-            here = [r for r in rids if r in self.loc and self.loc[r].gpu == mv.src]
-            rec = ExecRecord(mv.item, mv.src, mv.dst, pm.mode, here, 0, 0, 0)
-            if mv.src == mv.dst:
-                report.records.append(rec)
-                continue
-            for rid in here:
-                res = self.loc[rid]
-                src_pool, dst_pool = self.pool(mv.src, res.model), self.pool(mv.dst, res.model)
+            for rid, res, src_pool, dst_pool, dst_blocks in items:
                 nb = len(res.blocks)
-                dst_blocks = dst_pool.allocator.alloc(nb)
                 if pm.mode in (KV_TRANSFER, FORCED_KV_TRANSFER):
                     m = _native.Move()
                     m.src_pool, m.dst_pool, m.n_blocks = src_pool.pool_id, dst_pool.pool_id, nb
@@ -264,9 +284,7 @@ class MigrationExecutor:
                     by_dev.setdefault(src_pool.device, []).append(m)
                     rec.bytes_moved += nb * src_pool.shape.piece_bytes * 2 * src_pool.shape.layers
                     rec.tokens_moved += res.tokens
-                elif pm.mode == TOKEN_TRANSFER:
-                    if self.reprefill is None:
-                        raise ConfigError("token_transfer planned but executor has no re-prefill engine")
+                else:  # TOKEN_TRANSFER
                     self.reprefill(self, rid, mv.dst, dst_blocks, res.tokens,
                                    self.ordered_stream(dst_pool.device))
                     table = self._table(mv.dst, res.model)
@@ -276,8 +294,6 @@ class MigrationExecutor:
                             _as_i32_tensor(dst_blocks, dst_pool.device), non_blocking=False)
                     rec.tokens_recomputed += res.tokens
                     report.launches += 1
-                else:
-                    raise ValueError(f"cannot execute mode {pm.mode!r}")
                 rec.blocks += nb
                 rec.request_tokens[rid] = res.tokens
                 post.append((rid, mv.dst, res.tokens, dst_blocks))

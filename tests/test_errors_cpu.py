@@ -88,3 +88,19 @@ def test_residency_without_model_uses_the_single_model():
     ex.loc[7] = Residency(0, np.arange(2, dtype=np.int32), 20)
     assert ex.pool_of(7) is ex.pool(0)
     assert ex._table(0, ex.loc[7].model) == "T0"
+
+
+def test_execute_is_all_or_nothing_when_a_pool_is_full():
+    """A plan whose later move cannot get destination blocks raises before any
+    launch and leaves every pool, residency and launch list untouched."""
+    ex = _ex()
+    ex.admit(1, 0, 100)                # 7 blocks on GPU 0
+    ex.admit(2, 0, 60)                 # 4 blocks on GPU 0
+    ex.admit(3, 1, 16 * 25)            # 25 of GPU 1's 32 blocks
+    free0, free1 = ex.pools[0]["mini"].allocator.n_free, ex.pools[1]["mini"].allocator.n_free
+    plan = [PlannedMove(PendingMove(2, 0, 1, 0, 60), KV_TRANSFER),     # fits (4 <= 7 free)
+            PlannedMove(PendingMove(1, 0, 1, 0, 100), KV_TRANSFER)]    # does not (7 > 3 left)
+    with pytest.raises(RequestTooLarge):
+        ex.execute(plan)
+    assert ex.pools[0]["mini"].allocator.n_free == free0 and ex.pools[1]["mini"].allocator.n_free == free1
+    assert ex.where(1).gpu == 0 and ex.where(2).gpu == 0 and ex.launched == []
