@@ -14,7 +14,8 @@ from .errors import (ConfigError, KvmCudaError, KvmUnsupported, NativeLibraryMis
                      RequestTooLarge)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libkvmig.so")
+# KVM_LIB_PATH: load another build of the library (A/B experiments with kernel variants)
+LIB_PATH = os.environ.get("KVM_LIB_PATH") or os.path.join(HERE, "_lib", "libkvmig.so")
 
 KVM_OK = 0
 KVM_ERR_INVALID = -1

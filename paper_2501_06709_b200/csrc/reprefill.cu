@@ -419,7 +419,10 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
 // through a warp-private shared-memory tile before writing 64-byte token rows
 // into the paged pool.
 namespace pair {
-constexpr int BM = 256, BN = 256, BK = 64, STAGES = 6;
+#ifndef KVM_PAIR_STAGES
+#define KVM_PAIR_STAGES 6
+#endif
+constexpr int BM = 256, BN = 256, BK = 64, STAGES = KVM_PAIR_STAGES;
 constexpr int A_BYTES = 128 * BK * 2;                 // this CTA's 128 weight rows
 constexpr int B_BYTES = 128 * BK * 2;                 // this CTA's half of the token tile (box rows)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;        // 32 KiB
