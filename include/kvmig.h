@@ -367,6 +367,8 @@ int kvm_plan_hybrid(const kvm_pending* moves, int n, const kvm_plan_params* para
 #define KVM_CL_SET_NEXT_ACTIVATION_SEQ 21 /* next_activation_seq = a       */
 #define KVM_CL_VERSION 22          /* mutation counter (snapshot cache key) */
 #define KVM_CL_CLASSIFY 23         /* classify_request(a, b)        :72  */
+#define KVM_CL_VERSION_ADDR 24     /* ret = address of the uint64 mutation counter (valid while the
+                                      cluster lives), so a host can poll it without a call */
 /* kvm_sched_op ops: MellScheduler public operations */
 #define KVM_SCHED_ALLOCATE 0      /* ids[0], size   scheduler.py:641 */
 #define KVM_SCHED_DEPART 1        /* ids[0]         scheduler.py:684 */

@@ -148,7 +148,7 @@ _OPS = {name: i for i, name in enumerate((
     "ACTIVATE_GPU", "TERMINATE_GPU", "PLACE", "UNPLACE", "GPU_OF", "SET_SIZE", "PUT_SIZE", "DEL_SIZE",
     "NEW_GROUP", "GROUP_ADD", "GROUP_REMOVE", "DEL_GROUP", "ITEM_SIZE", "ITEM_CLASS", "USED_BYTES",
     "GPU_CLASS", "GPU_FAMILY", "LATEST_OF_FAMILY", "CHECK_CAPACITY", "ITEM_OF_REQUEST",
-    "SET_ACTIVATION_SEQ", "SET_NEXT_ACTIVATION_SEQ", "VERSION", "CLASSIFY"))}
+    "SET_ACTIVATION_SEQ", "SET_NEXT_ACTIVATION_SEQ", "VERSION", "CLASSIFY", "VERSION_ADDR"))}
 
 
 def _native_op(name: str) -> int:
@@ -213,6 +213,8 @@ class ClusterState:
         self._ret = ctypes.c_int64()
         self._cache: Optional[_Snapshot] = None
         self._sizes_view = _Sizes(self)
+        # the native mutation counter, read in place (no call per view access)
+        self._ver = ctypes.c_uint64.from_address(self._op(_OPS["VERSION_ADDR"]))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -232,7 +234,7 @@ class ClusterState:
         return self._ret.value
 
     def _version(self) -> int:
-        return self._op(_OPS["VERSION"])
+        return self._ver.value
 
     def _snap(self) -> _Snapshot:
         v = self._version()

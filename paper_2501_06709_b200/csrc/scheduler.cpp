@@ -1574,6 +1574,7 @@ int kvm_cluster_op(kvm_cluster* h, int op, int64_t a, int64_t b, int64_t* ret) {
       case KVM_CL_SET_NEXT_ACTIVATION_SEQ: c.next_seq = a; ++c.version; break;
       case KVM_CL_VERSION: r = (int64_t)c.version; break;
       case KVM_CL_CLASSIFY: r = classify(a, b); break;
+      case KVM_CL_VERSION_ADDR: r = (int64_t)(uintptr_t)&c.version; break;
       default: raise(KVM_ERR_INVALID, "unknown cluster op " + std::to_string(op));
     }
     if (ret) *ret = r;
