@@ -523,9 +523,24 @@ __device__ __forceinline__ void decode_pair(const Params& p, int t, int& l, int&
   mt = r / p.n_tiles;
   nt = r - mt * p.n_tiles;
 }
-__device__ __forceinline__ int tile_n(const Params& p, int nt) {  // MMA N of a token tile (multiple of 16)
-  const int left = min(BN, p.rows - nt * BN);
-  return (left + 15) & ~15;
+// Token tiles are balanced: the suffix's ceil(rows/16) 16-token units are dealt
+// evenly over the n_tiles tiles (e.g. 1 360 tokens -> 240 + 5 x 224 rather than
+// 5 x 256 + 80): a narrow N still reads the full 256-row A operand per MMA, so
+// one 80-wide tile costs ~2.4x its share (measured 5.41 ms for 1 280 tokens,
+// 6.23 ms for 1 360).
+struct TokenTile {
+  int start;  // first token of the tile
+  int n_mma;  // MMA N (multiple of 16, <= 256)
+  int n_tok;  // valid tokens (<= n_mma)
+};
+__device__ __forceinline__ TokenTile token_tile(const Params& p, int nt) {
+  const int units = (p.rows + 15) >> 4;
+  const int base = units / p.n_tiles, rem = units - base * p.n_tiles;
+  TokenTile tt;
+  tt.start = 16 * (nt * base + min(nt, rem));
+  tt.n_mma = 16 * (base + (nt < rem ? 1 : 0));
+  tt.n_tok = min(tt.n_mma, p.rows - tt.start);
+  return tt;
 }
 
 template <bool kCopy>
@@ -604,7 +619,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
         if (t >= p.total_tiles) break;
         int l, mt, nt;
         decode_pair(p, t, l, mt, nt);
-        const int half = tile_n(p, nt) >> 1;
+        const TokenTile tt = token_tile(p, nt);
+        const int half = tt.n_mma >> 1;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -612,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
           if (rank == 0) mbar_expect_tx(full + stage, 2 * STAGE_BYTES);
           const uint32_t bar = mapa(smem_u32(full + stage), 0);
           tma_3d_pair(&p.tmap_w, bar, sa, kb * BK, mt * BM + (int)rank * 128, l);
-          tma_2d_pair(&p.tmap_x, bar, sb, kb * BK, nt * BN + (int)rank * half);
+          tma_2d_pair(&p.tmap_x, bar, sb, kb * BK, tt.start + (int)rank * half);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -630,7 +646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
       for (int t = tq.next(true); t < p.total_tiles; t = tq.next(true)) {
         int l, mt, nt;
         decode_pair(p, t, l, mt, nt);
-        const uint32_t id = idesc(tile_n(p, nt));
+        const uint32_t id = idesc(token_tile(p, nt).n_mma);
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -680,7 +696,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const int f0 = mt * BM + (int)rank * 128 + q * 32;  // this warp's 32 features
-      const int n_tok = min(BN, p.rows - nt * BN);
+      const TokenTile tt = token_tile(p, nt);
+      const int n_tok = tt.n_tok;
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
       // destination of features [f0, f0 + 32) for a token: Q (dense) or the K / V row in the pool
       int kind = -1;  // 0: Q, 1: K, 2: V
@@ -706,9 +723,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int tr = 8 * i + (lane >> 2);          // token row of the 32 x 32 block
-          const int tok_i = nt * BN + c * 32 + tr;      // token index within the suffix
+          const int tok_i = tt.start + c * 32 + tr;     // token index within the suffix
           const uint4 v = *reinterpret_cast<const uint4*>(tile + tr * 32 + (lane & 3) * 8);
-          if (tok_i < p.rows) {
+          if (c * 32 + tr < n_tok) {  // columns past the tile's tokens hold stale TMEM
             uint8_t* dst;
             if (kind == 0) {
               dst = reinterpret_cast<uint8_t*>(p.q_out + ((int64_t)l * p.rows + tok_i) * p.q_cols + fcol);
