@@ -22,7 +22,8 @@ def main():
     ap.add_argument("--rows", type=int, default=1360)
     ap.add_argument("--shape", default="llama2-13b")
     ap.add_argument("--kv-only", action="store_true")
-    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--no-cublas", action="store_true")
     a = ap.parse_args()
@@ -49,22 +50,33 @@ def main():
         torch.cuda.synchronize()
         return ev[0].elapsed_time(ev[1]) / a.iters
 
-    with torch.cuda.stream(s):
-        ms = timeit(lambda: reprefill(pool, x, w, blocks, stream=s))
-        ms1 = timeit(lambda: reprefill(pool, x, w, blocks, stream=s, single_cta=True))
-        out = {"kernel": "reprefill_pair_kernel (tcgen05 cta_group::2)", "shape": a.shape, "rows": rows,
-               "kv_only": a.kv_only, "flops": flops, "ms": round(ms, 4),
-               "tflops": round(flops / ms / 1e9, 1),
-               "single_cta_ms": round(ms1, 4), "single_cta_tflops": round(flops / ms1 / 1e9, 1)}
-        if not a.no_cublas:
-            y = torch.empty(rows, w.shape[1], dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(rows, w.shape[1], dtype=torch.bfloat16, device="cuda")
 
-            def cublas():
-                for l in range(shape.layers):
-                    torch.matmul(x, w[l].t(), out=y)
-            ms2 = timeit(cublas)
-            out["cublas_ms"] = round(ms2, 4)
-            out["cublas_tflops"] = round(flops / ms2 / 1e9, 1)
+    def cublas():
+        for l in range(shape.layers):
+            torch.matmul(x, w[l].t(), out=y)
+
+    arms = {"pair": lambda: reprefill(pool, x, w, blocks, stream=s),
+            "single": lambda: reprefill(pool, x, w, blocks, stream=s, single_cta=True)}
+    if not a.no_cublas:
+        arms["cublas"] = cublas
+    # interleaved rounds (pair, single, cuBLAS, pair, ...) so every arm sees the same
+    # thermal / power state; the median round per arm is reported
+    samples = {k: [] for k in arms}
+    with torch.cuda.stream(s):
+        for _ in range(a.rounds):
+            for k, fn in arms.items():
+                samples[k].append(timeit(fn))
+    med = {k: sorted(v)[len(v) // 2] for k, v in samples.items()}
+    ms, ms1 = med["pair"], med["single"]
+    out = {"kernel": "reprefill_pair_kernel (tcgen05 cta_group::2)", "shape": a.shape, "rows": rows,
+           "kv_only": a.kv_only, "flops": flops, "ms": round(ms, 4),
+           "tflops": round(flops / ms / 1e9, 1),
+           "single_cta_ms": round(ms1, 4), "single_cta_tflops": round(flops / ms1 / 1e9, 1),
+           "rounds": a.rounds, "iters_per_round": a.iters}
+    if "cublas" in med:
+        out["cublas_ms"] = round(med["cublas"], 4)
+        out["cublas_tflops"] = round(flops / med["cublas"] / 1e9, 1)
     print(json.dumps(out))
 
 
