@@ -48,6 +48,81 @@ NVLINK_PEAK_GBS = 900.0        # nominal per direction per GPU
 NVLINK_MEASURED_GBS = 770.0    # B200_PROFILING.md: measured peer copy per direction
 
 
+def _kernel_extras(device: int) -> dict:
+    """Fresh measurements of the path's other kernels on the same box, reported
+    beside the headline (not part of the timed region): K3 re-prefill on the
+    CTA-pair tcgen05 kernel (configs[2]'s 13B suffix of 1 360 tokens, QKV, 40
+    layers) and K5 paged decode over a 7B 4k-token cache (32 layers), each with
+    its roofline fraction against MEASURED_PEAKS.json."""
+    import torch
+
+    from paper_2501_06709_b200.attention import paged_decode
+    from paper_2501_06709_b200.kvcache import SHAPES, KVPool
+    from paper_2501_06709_b200.reprefill import reprefill, reprefill_flops, synthetic_hidden, synthetic_weights
+
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        tflops_peak, tsrc = float(pk["bf16_tflops_sustained"]), "measured (MEASURED_PEAKS.json bf16 sustained)"
+        hbm_peak = float(pk["hbm_gbs"])
+    except Exception:
+        tflops_peak, tsrc, hbm_peak = 2250.0, "fallback (nominal dense bf16)", 6650.0
+    st = torch.cuda.Stream(device=device)
+
+    def timed(fn, reps=5, iters=3):
+        st.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(st):
+            for _ in range(2):
+                fn()
+            ms = []
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(iters):
+                    fn()
+                e1.record(st)
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1) / iters)
+        return statistics.median(ms)
+
+    out = {}
+    try:
+        sh, rows = SHAPES["llama2-13b"], 1360
+        nblk = (rows + 15) // 16
+        pool = KVPool(sh, nblk + 4, device=device, dtype=torch.bfloat16)
+        blocks = torch.arange(nblk, dtype=torch.int32, device=f"cuda:{device}")
+        x, w = synthetic_hidden(sh, rows, device), synthetic_weights(sh, device, with_q=True)
+        ms = timed(lambda: reprefill(pool, x, w, blocks, stream=st))
+        tf = reprefill_flops(sh, rows, with_q=True) / ms / 1e9
+        out["reprefill_13b_s1360"] = {"kernel": "reprefill_pair_kernel (tcgen05 cta_group::2)", "ms": round(ms, 4),
+                                      "achieved": round(tf, 1), "peak": tflops_peak, "unit": "TFLOP/s",
+                                      "frac": round(tf / tflops_peak, 4), "peak_source": tsrc}
+        del pool, x, w
+    except Exception as e:  # reported, never fatal for the headline
+        out["reprefill_13b_s1360"] = {"error": str(e)[:300]}
+    try:
+        sh, seq = SHAPES["llama2-7b"], 4096
+        nblk = seq // 16
+        pool = KVPool(sh, nblk + 8, device=device)
+        pool.tensor.normal_()
+        g = torch.Generator().manual_seed(0)
+        table = torch.randperm(nblk + 8, generator=g)[:nblk].to(torch.int32).view(1, nblk).to(f"cuda:{device}")
+        lens = torch.full((1,), seq, dtype=torch.int32, device=f"cuda:{device}")
+        q = torch.randn(sh.layers, 1, sh.q_heads, 128, device=f"cuda:{device}").half()
+        o = torch.empty_like(q)
+        ms = timed(lambda: paged_decode(pool, q, table, lens, o, max_seq_len=seq, stream=st), iters=10)
+        gbs = 2 * seq * sh.kv_heads * 128 * 2 * sh.layers / ms / 1e6
+        out["decode_7b_4k_32l"] = {"kernel": "decode_gqa_kernel (mma.sync)", "ms": round(ms, 4),
+                                   "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                                   "frac": round(gbs / hbm_peak, 4),
+                                   "note": "read-only stream vs the read+write copy peak"}
+        del pool, q, o
+    except Exception as e:
+        out["decode_7b_4k_32l"] = {"error": str(e)[:300]}
+    torch.cuda.empty_cache()
+    return out
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -521,6 +596,8 @@ def run_ours(args) -> int:
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
+        if world == 1 and not args.no_extras:
+            line["kernels"] = _kernel_extras(device)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -542,6 +619,8 @@ def main(argv=None) -> int:
                     help="stream KV through L2 with an evict-first policy (KVM_F_L2_EVICT_FIRST)")
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the re-prefill / decode measurements reported beside the headline")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -48,6 +48,9 @@ def test_gpu_arm_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * 32 * 4 and e["d2h_bytes_per_step"] == 32 * 4
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    k = d["kernels"]   # fresh re-prefill / decode measurements beside the headline
+    assert k["reprefill_13b_s1360"]["unit"] == "TFLOP/s" and 0.3 < k["reprefill_13b_s1360"]["frac"] < 1.5
+    assert k["decode_7b_4k_32l"]["unit"] == "GB/s" and 0.3 < k["decode_7b_4k_32l"]["frac"] < 1.5
 
 
 @pytest.mark.gpu
