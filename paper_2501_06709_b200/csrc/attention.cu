@@ -427,6 +427,9 @@ __global__ void __launch_bounds__(WARPS * 32) decode_gqa_kernel(const __grid_con
 
 template <typename T>
 __global__ void __launch_bounds__(D) decode_combine_kernel(const __grid_constant__ Params p) {
+  // launched as a programmatic dependent of the split kernel: its launch and
+  // prologue overlap the split kernel's tail; wait here for its partials
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int qh = blockIdx.x, lb = blockIdx.y, d = threadIdx.x;
   const int64_t base = ((int64_t)lb * p.q_heads + qh) * p.splits;
   float M = -CUDART_INF_F;
@@ -449,18 +452,30 @@ struct Workspace {
 static Workspace g_ws[64];
 static std::mutex g_ws_mu;
 
+template <typename T>
+static int launch_combine(const Params& p, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.q_heads, p.n_layers * p.batch);
+  cfg.blockDim = dim3(D);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KVM_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_combine_kernel<T>, p));
+  count_launch();
+  return KVM_OK;
+}
+
 template <typename T, int G>
 static int launch_g(const Params& p, cudaStream_t st) {
   dim3 grid(p.splits, p.kv_heads, p.n_layers * p.batch);
   decode_split_kernel<T, G><<<grid, WARPS * 32, 0, st>>>(p);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
-  if (p.splits > 1) {
-    dim3 g2(p.q_heads, p.n_layers * p.batch);
-    decode_combine_kernel<T><<<g2, D, 0, st>>>(p);
-    KVM_CUDA_TRY(cudaGetLastError());
-    count_launch();
-  }
+  if (p.splits > 1) return launch_combine<T>(p, st);
   return KVM_OK;
 }
 
@@ -476,12 +491,7 @@ static int launch_gqa(const Params& p, int G, cudaStream_t st) {
   decode_gqa_kernel<T><<<grid, WARPS * 32, GQA_SMEM, st>>>(p, G);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
-  if (p.splits > 1) {
-    dim3 g2(p.q_heads, p.n_layers * p.batch);
-    decode_combine_kernel<T><<<g2, D, 0, st>>>(p);
-    KVM_CUDA_TRY(cudaGetLastError());
-    count_launch();
-  }
+  if (p.splits > 1) return launch_combine<T>(p, st);
   return KVM_OK;
 }
 
