@@ -122,12 +122,20 @@ typedef struct kvm_reprefill_args {
   const int32_t* dst_blocks; /* device, n_dst_blocks entries */
   uint32_t* done_flag;    /* optional, set to done_value when all layers landed */
   uint32_t done_value;
-  int32_t flags;          /* 0 or KVM_REPREFILL_SINGLE_CTA */
+  int32_t flags;          /* 0 | KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE */
+  float rope_theta;       /* read only with KVM_REPREFILL_ROPE: the rotary base (Llama: 10000) */
 } kvm_reprefill_args;
 /* kvm_reprefill engine: default = CTA-pair kernel (tcgen05 cta_group::2, features
  * on M, tokens on N, 256 x 256 tiles); this flag selects the single-CTA kernel
  * (M = 128 tokens, N = 256 features), which is also the split kernel's GEMM. */
 #define KVM_REPREFILL_SINGLE_CTA 0x1
+/* Rotary position embedding fused into the epilogue, so the pool holds
+ * post-RoPE K (what a Llama KV cache holds) and q_out post-RoPE Q: per head of
+ * 128 dims, position p = tok0 + t, i < 64, theta_i = rope_theta^(-2i/128):
+ *   y[i] = x[i] cos(p theta_i) - x[i+64] sin(p theta_i),
+ *   y[i+64] = x[i+64] cos(p theta_i) + x[i] sin(p theta_i)   (HF "rotate_half").
+ * V is not rotated.  Needs head_dim 128. */
+#define KVM_REPREFILL_ROPE 0x2
 
 /* Adaptive split migration in ONE kernel on the destination GPU (extension of
  * the reference's all-or-nothing choice, migration.py:155-169): the first
@@ -153,7 +161,8 @@ typedef struct kvm_split_args {
   int32_t* dst_table_row; /* optional */
   uint32_t* done_flag;    /* optional */
   uint32_t done_value;
-  int32_t flags;          /* 0 or KVM_REPREFILL_SINGLE_CTA (GEMM engine) */
+  int32_t flags;          /* 0 | KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE */
+  float rope_theta;       /* read only with KVM_REPREFILL_ROPE */
 } kvm_split_args;
 
 /* Paged-attention decode over a pool (the consumer of a migrated cache):

@@ -34,6 +34,7 @@ KVM_F_ENGINE_BULK = 0x2
 KVM_F_L2_EVICT_FIRST = 0x4
 KVM_MAX_MOVES = 96
 KVM_REPREFILL_SINGLE_CTA = 0x1
+KVM_REPREFILL_ROPE = 0x2
 
 
 def KVM_F_CTAS_PER_SM(n: int) -> int:
@@ -75,7 +76,7 @@ class ReprefillArgs(ctypes.Structure):
                 ("tok0", ctypes.c_int32), ("n_dst_blocks", ctypes.c_int32),
                 ("x", ctypes.c_void_p), ("w", ctypes.c_void_p), ("q_out", ctypes.c_void_p),
                 ("dst_blocks", ctypes.c_void_p), ("done_flag", ctypes.c_void_p),
-                ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32)]
+                ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32), ("rope_theta", ctypes.c_float)]
 
 
 class SplitArgs(ctypes.Structure):
@@ -83,7 +84,8 @@ class SplitArgs(ctypes.Structure):
                 ("prefix_blocks", ctypes.c_int32), ("d_model", ctypes.c_int32), ("q_cols", ctypes.c_int32),
                 ("src_blocks", ctypes.c_void_p), ("dst_blocks", ctypes.c_void_p), ("x", ctypes.c_void_p),
                 ("w", ctypes.c_void_p), ("q_out", ctypes.c_void_p), ("dst_table_row", ctypes.c_void_p),
-                ("done_flag", ctypes.c_void_p), ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32)]
+                ("done_flag", ctypes.c_void_p), ("done_value", ctypes.c_uint32), ("flags", ctypes.c_int32),
+                ("rope_theta", ctypes.c_float)]
 
 
 class DecodeArgs(ctypes.Structure):

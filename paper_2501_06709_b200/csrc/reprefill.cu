@@ -59,6 +59,7 @@ struct Params {
   uint32_t* done_flag;
   uint32_t* ctr;
   uint32_t* tile_ctr;   // pair kernel: dynamic tile counter (self-resetting)
+  const float2* rope;   // KVM_REPREFILL_ROPE: (cos, sin) per [token t][i < 64] of the suffix, else NULL
   int64_t plane_bytes;  // num_blocks * piece_bytes
   int64_t piece_bytes;
   int32_t rows, n_out, d_model, layers, q_cols, kvd, tok0, block_tokens, n_dst_blocks;
@@ -155,6 +156,13 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Rotary embedding of one element pair (HF rotate_half): lo' = lo c - hi s, hi' = hi c + lo s.
+__device__ __forceinline__ void rope_pair(uint32_t& lo, uint32_t& hi, float2 cs) {
+  const float a = __uint_as_float(lo), b = __uint_as_float(hi);
+  lo = __float_as_uint(a * cs.x - b * cs.y);
+  hi = __float_as_uint(b * cs.x + a * cs.y);
 }
 
 __device__ __forceinline__ void decode(const Params& p, int t, int& l, int& nt, int& mt) {
@@ -339,13 +347,10 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
           kv_row[kv] = p.pool + ((int64_t)l * 2 + kv) * p.plane_bytes + (int64_t)blk * p.piece_bytes + slot_off;
       }
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        TMEM_LD_32x32b_X32(taddr + c * 32, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // bf16 store of 32 consecutive output columns of this thread's token row
+      auto store32 = [&](int c, const uint32_t* r) {
         const int col = nt * BN + c * 32;
-        if (!row_ok || col >= p.n_out) continue;
+        if (!row_ok || col >= p.n_out) return;
         uint4 v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
         }
         uint4* dst;
         if (col < p.q_cols) {
-          if (!p.q_out) continue;
+          if (!p.q_out) return;
           dst = reinterpret_cast<uint4*>(p.q_out + ((int64_t)l * p.rows + row) * p.q_cols + col);
         } else {
           const int kc = col - p.q_cols;
@@ -365,6 +370,34 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) dst[j] = v[j];
+      };
+      if (!p.rope) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          TMEM_LD_32x32b_X32(taddr + c * 32, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          store32(c, r);
+        }
+      } else {
+        // RoPE: the tile's 256 columns are two 128-dim heads; column chunk c (dims
+        // (c%4)*32..) pairs with chunk c+2 (dims +64) of the same head.  V heads are
+        // stored unrotated.
+#pragma unroll 1
+        for (int pc = 0; pc < BN / 32; pc += (pc % 4 == 1 ? 3 : 1)) {  // 0, 1, 4, 5
+          uint32_t ra[32], rb[32];
+          TMEM_LD_32x32b_X32(taddr + pc * 32, ra);
+          TMEM_LD_32x32b_X32(taddr + (pc + 2) * 32, rb);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const int col = nt * BN + pc * 32;
+          if (row_ok && col < p.q_cols + p.kvd) {  // Q or K: rotate by the token's position
+            const float2* cs = p.rope + (int64_t)row * 64 + (pc % 4) * 32;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) rope_pair(ra[k], rb[k], __ldg(cs + k));
+          }
+          store32(pc, ra);
+          store32(pc + 2, rb);
+        }
       }
       tc_fence_before();
       mbar_arrive(tempty + acc);
@@ -426,7 +459,9 @@ constexpr int BM = 256, BN = 256, BK = 64, STAGES = KVM_PAIR_STAGES;
 constexpr int A_BYTES = 128 * BK * 2;                 // this CTA's 128 weight rows
 constexpr int B_BYTES = 128 * BK * 2;                 // this CTA's half of the token tile (box rows)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;        // 32 KiB
-constexpr int EPI_BYTES = 4 * 32 * 32 * 2;            // 4 warps x [32 tokens][32 features] bf16
+constexpr int EPI_BF16 = 32 * 32 * 2;                // per warp: [32 tokens][32 features] bf16 (transpose)
+constexpr int EPI_F32 = 32 * 32 * 4;                 // per warp: fp32 exchange tile (RoPE partner)
+constexpr int EPI_BYTES = 4 * (EPI_BF16 + EPI_F32);
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 1024;
 constexpr uint32_t TMEM_COLS = 512;                   // two 128 x 256 fp32 accumulators per CTA
 
@@ -679,7 +714,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
     // ---------------- epilogue: TMEM -> bf16 -> smem transpose -> paged pool ----------------
     const int q = warp & 3;
     bool copying = kCopy;
-    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(epi + q * 32 * 32 * 2);  // [32 tokens][32 features]
+    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(epi + q * EPI_BF16);  // [32 tokens][32 features]
+    float* xch = reinterpret_cast<float*>(epi + 4 * EPI_BF16);                    // 4 x [32 tokens][32 features]
     const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -717,6 +753,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
         TMEM_LD_32x32b_X32(taddr + c * 32, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (kind < 0) continue;
+        if (p.rope && kind <= 1) {
+          // RoPE on Q / K: this CTA's 128 features are one head; warp q holds dims
+          // q*32.., its rotary partner (dims +-64) is warp q^2 -> exchange through smem.
+          // kind is uniform over the 4 epilogue warps, so the named barrier is too.
+          float* mine = xch + q * 1024;
+          const float* other = xch + (q ^ 2) * 1024;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mine[j * 32 + lane] = __uint_as_float(r[j]);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const int i = (q & 1) * 32 + lane;  // rotary frequency index of this lane's dim
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int tok_i = tt.start + c * 32 + j;
+            const float2 cs = tok_i < p.rows ? __ldg(p.rope + (int64_t)tok_i * 64 + i) : make_float2(1.f, 0.f);
+            const float x = __uint_as_float(r[j]), y = other[j * 32 + lane];
+            r[j] = __float_as_uint(q < 2 ? x * cs.x - y * cs.y : x * cs.x + y * cs.y);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // partner has read `mine`
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) tile[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]));
         __syncwarp();
@@ -779,6 +834,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
   }
 }
 }  // namespace pair
+
+// (cos, sin) of position tok0 + t times theta^(-2i/128), i < 64, computed in double
+__global__ void rope_table_kernel(float2* tab, int rows, int tok0, double log_theta) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * 64) return;
+  const int t = idx >> 6, i = idx & 63;
+  const double ang = (double)(tok0 + t) * exp(-log_theta * (double)(2 * i) / 128.0);
+  double sn, cs;
+  sincos(ang, &sn, &cs);
+  tab[idx] = make_float2((float)cs, (float)sn);
+}
 
 // ---------------------------------------------------------------------------
 // host side
@@ -946,6 +1012,19 @@ static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
   return KVM_OK;
 }
 
+// KVM_REPREFILL_ROPE: a stream-ordered (cos, sin) table for the suffix's positions,
+// freed (stream-ordered) after the GEMM that reads it.
+static int rope_table(Params& p, float theta, cudaStream_t stream, float2** out) {
+  *out = nullptr;
+  if (p.rows <= 0) return KVM_OK;
+  const size_t n = (size_t)p.rows * 64;
+  KVM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(out), n * sizeof(float2), stream));
+  rope_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(*out, p.rows, p.tok0, log((double)theta));
+  KVM_CUDA_TRY(cudaGetLastError());
+  p.rope = *out;
+  return KVM_OK;
+}
+
 struct DevScope {
   int prev = -1, dev;
   explicit DevScope(int d) : dev(d) {
@@ -981,7 +1060,9 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a->x || !a->w || !a->dst_blocks) return fail(KVM_ERR_INVALID, "NULL x/w/dst_blocks");
   if ((int64_t)(a->tok0 + a->rows) > (int64_t)a->n_dst_blocks * d.block_tokens)
     return fail(KVM_ERR_INVALID, "dst_blocks do not cover tok0 + rows tokens");
-  if (a->flags & ~KVM_REPREFILL_SINGLE_CTA) return fail(KVM_ERR_INVALID, "unknown flags");
+  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE)) return fail(KVM_ERR_INVALID, "unknown flags");
+  if ((a->flags & KVM_REPREFILL_ROPE) && (d.head_dim != 128 || !(a->rope_theta > 1.f)))
+    return fail(KVM_ERR_CONFIG, "KVM_REPREFILL_ROPE needs head_dim 128 and rope_theta > 1");
   if (reinterpret_cast<uintptr_t>(a->x) % 16 || reinterpret_cast<uintptr_t>(a->w) % 16)
     return fail(KVM_ERR_INVALID, "x and w must be 16-byte aligned");
   DevScope ds(pool->device);
@@ -994,8 +1075,12 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (rc) return rc;
   p.done_flag = a->done_flag;
   p.done_value = a->done_value;
-  if (pair_kernel) return launch_pair(p, pool->device, false, static_cast<cudaStream_t>(stream));
-  return launch_gemm(p, pool->device, false, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float2* tab = nullptr;
+  if ((a->flags & KVM_REPREFILL_ROPE) && (rc = rope_table(p, a->rope_theta, st, &tab))) return rc;
+  rc = pair_kernel ? launch_pair(p, pool->device, false, st) : launch_gemm(p, pool->device, false, st);
+  if (tab) cudaFreeAsync(tab, st);
+  return rc;
 }
 
 extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
@@ -1022,7 +1107,9 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
     return fail(KVM_ERR_CONFIG, "kv_heads*head_dim and q_cols must be multiples of 32");
   if (!a->dst_blocks || (a->prefix_blocks && !a->src_blocks) || (suffix && (!a->x || !a->w)))
     return fail(KVM_ERR_INVALID, "NULL pointer argument");
-  if (a->flags & ~KVM_REPREFILL_SINGLE_CTA) return fail(KVM_ERR_INVALID, "unknown flags");
+  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE)) return fail(KVM_ERR_INVALID, "unknown flags");
+  if ((a->flags & KVM_REPREFILL_ROPE) && (d.head_dim != 128 || !(a->rope_theta > 1.f)))
+    return fail(KVM_ERR_CONFIG, "KVM_REPREFILL_ROPE needs head_dim 128 and rope_theta > 1");
   if (a->tokens == 0) return KVM_OK;
   DevScope ds(dst->device);
   if (!is_sm100(dst->device)) return fail(KVM_ERR_UNSUPPORTED, "kvm_split_migrate needs an sm_100 (B200) device");
@@ -1042,6 +1129,10 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   p.c_nblocks = a->prefix_blocks;
   p.c_upp = (int32_t)((dst->piece_bytes + CUNIT - 1) / CUNIT);
   p.c_units = (int64_t)2 * d.layers * a->prefix_blocks * p.c_upp;
-  if (pair_kernel) return launch_pair(p, dst->device, p.c_units > 0, static_cast<cudaStream_t>(stream));
-  return launch_gemm(p, dst->device, p.c_units > 0, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float2* tab = nullptr;
+  if ((a->flags & KVM_REPREFILL_ROPE) && (rc = rope_table(p, a->rope_theta, st, &tab))) return rc;
+  rc = pair_kernel ? launch_pair(p, dst->device, p.c_units > 0, st) : launch_gemm(p, dst->device, p.c_units > 0, st);
+  if (tab) cudaFreeAsync(tab, st);
+  return rc;
 }

@@ -45,13 +45,17 @@ def synthetic_hidden(shape: ModelShape, rows: int, device: int, seed: int = 2):
 
 
 def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=None,
-              done_flag: int = 0, done_value: int = 1, single_cta: bool = False) -> None:
+              done_flag: int = 0, done_value: int = 1, single_cta: bool = False,
+              rope_theta: Optional[float] = None) -> None:
     """Launch kvm_reprefill: K/V of tokens [tok0, tok0 + rows) into `dst_blocks`.
 
     x: bf16 [rows][d_model] (device), w: bf16 [layers][n_out][d_model] with
     n_out = q_cols + 2 * kv_cols, dst_blocks: int32 device tensor covering the
     token range, q_out: optional bf16 [layers][rows][q_cols].  single_cta
     selects the single-CTA kernel instead of the default CTA-pair one.
+    rope_theta: apply rotary position embedding (HF rotate_half, positions
+    tok0 + t) to Q and K in the epilogue, so the pool holds post-RoPE K as a
+    Llama KV cache does (head_dim 128).
     """
     import torch
 
@@ -79,7 +83,9 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
     a.q_out = q_out.data_ptr() if q_out is not None else None
     a.dst_blocks = dst_blocks.data_ptr()
     a.done_flag, a.done_value = done_flag or None, done_value
-    a.flags = _native.KVM_REPREFILL_SINGLE_CTA if single_cta else 0
+    a.flags = (_native.KVM_REPREFILL_SINGLE_CTA if single_cta else 0) | (
+        _native.KVM_REPREFILL_ROPE if rope_theta else 0)
+    a.rope_theta = float(rope_theta or 0.0)
     s = stream if stream is not None else torch.cuda.current_stream(pool.device)
     _native.check(_native.lib().kvm_reprefill(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),
                   "kvm_reprefill")

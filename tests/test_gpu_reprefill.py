@@ -164,3 +164,52 @@ def test_reprefill_full_shapes_pair_kernel(shape_name, rows, tok0):
                                    atol=ATOL, rtol=RTOL)
         torch.testing.assert_close(pool.tensor[l, 1, blk, slot].reshape(rows, kvd).float(), ref[:, qc + kvd:],
                                    atol=ATOL, rtol=RTOL)
+
+
+def _rope_ref(y, positions, theta, q_cols, kv_cols):
+    """HF Llama rotate_half RoPE on the Q and K columns of y [L, rows, n_out] (fp32),
+    angles in float64; V untouched."""
+    y = y.clone()
+    i = torch.arange(64, dtype=torch.float64, device=y.device)
+    ang = positions.to(torch.float64)[:, None] * theta ** (-2.0 * i / 128.0)
+    c, s = torch.cos(ang).float(), torch.sin(ang).float()          # [rows, 64]
+    for lo, hi in ((0, q_cols), (q_cols, q_cols + kv_cols)):
+        seg = y[:, :, lo:hi].reshape(y.shape[0], y.shape[1], -1, 128)
+        a, b = seg[..., :64].clone(), seg[..., 64:].clone()
+        seg[..., :64] = a * c[None, :, None, :] - b * s[None, :, None, :]
+        seg[..., 64:] = b * c[None, :, None, :] + a * s[None, :, None, :]
+        y[:, :, lo:hi] = seg.reshape(y.shape[0], y.shape[1], -1)
+    return y
+
+
+@pytest.mark.parametrize("single_cta", [False, True])
+@pytest.mark.parametrize("rows,tok0", [(1, 0), (77, 5), (300, 4000), (513, 16)])
+def test_reprefill_rope(rows, tok0, single_cta):
+    """KVM_REPREFILL_ROPE: K in the pool and Q are post-RoPE (positions tok0 + t),
+    V is not rotated; both engines."""
+    shape = ModelShape("rope", layers=2, kv_heads=2, head_dim=128, q_heads=4, d_model=256)
+    nblk = (tok0 + rows + 15) // 16
+    nb = nblk + 6
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    before = pool.tensor.view(torch.int16).clone()
+    blocks = torch.randperm(nb, generator=torch.Generator().manual_seed(rows))[:nblk].to(torch.int32).cuda()
+    x = synthetic_hidden(shape, rows, 0, seed=rows + 3)
+    w = synthetic_weights(shape, 0, with_q=True, seed=rows + 4)
+    q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda")
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q, single_cta=single_cta, rope_theta=10000.0)
+    torch.cuda.synchronize()
+    pos = torch.arange(tok0, tok0 + rows, device="cuda")
+    ref = _rope_ref(_ref(x, w), pos, 10000.0, shape.q_cols, shape.kv_cols)
+    _check(shape, pool, blocks, tok0, rows, ref, q, before)
+
+
+def test_reprefill_rope_needs_head_dim_128():
+    from paper_2501_06709_b200.errors import ConfigError
+
+    shape = ModelShape("rope64", layers=1, kv_heads=2, head_dim=64, q_heads=2, d_model=128)
+    pool = KVPool(shape, 4, dtype=torch.bfloat16)
+    x = synthetic_hidden(shape, 16, 0)
+    w = synthetic_weights(shape, 0, with_q=False)
+    with pytest.raises(ConfigError):
+        reprefill(pool, x, w, torch.arange(1, dtype=torch.int32, device="cuda"), rope_theta=10000.0)

@@ -123,3 +123,36 @@ def test_executor_split_move():
                        pools[0].tensor[:, :, torch.from_numpy(sb[:pre]).long().cuda()].view(torch.int16))
     assert np.array_equal(tables[1].rows[tables[1].slot(3), :len(r.blocks)].cpu().numpy(), r.blocks)
     assert pools[0].allocator.n_free == 64
+
+
+@pytest.mark.parametrize("single_cta", [False, True])
+def test_fused_split_with_rope(single_cta):
+    """The fused split migration with RoPE in the re-prefill epilogue: prefix
+    bit-exact, suffix K post-RoPE at positions prefix_tokens + t."""
+    from paper_2501_06709_b200.split import split_migrate_fused
+    from test_gpu_reprefill import _rope_ref
+
+    shape = ModelShape("spr", layers=3, kv_heads=2, head_dim=128, q_heads=4, d_model=256)
+    tokens, suffix = 1000, 232
+    plan = make_split(tokens, suffix)
+    nb = plan.total_blocks + 10
+    src, dst = KVPool(shape, nb, dtype=torch.bfloat16), KVPool(shape, nb, dtype=torch.bfloat16)
+    src.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(5))[:plan.total_blocks].to(torch.int32).cuda()
+    db = torch.from_numpy(dst.allocator.alloc(plan.total_blocks)).cuda()
+    x = synthetic_hidden(shape, suffix, 0, seed=6)
+    w = synthetic_weights(shape, 0, with_q=True, seed=7)
+    split_migrate_fused(src, dst, sb, db, plan, x, w, single_cta=single_cta, rope_theta=500000.0)
+    torch.cuda.synchronize()
+    pre = plan.prefix_blocks
+    assert torch.equal(dst.tensor[:, :, db[:pre].long()].view(torch.int16),
+                       src.tensor[:, :, sb[:pre].long()].view(torch.int16))
+    toks = torch.arange(plan.prefix_tokens, tokens, device="cuda")
+    ref = _rope_ref(torch.einsum("tk,lnk->ltn", x.float(), w.float()), toks, 500000.0, shape.q_cols, shape.kv_cols)
+    blk, slot = db.long()[toks // 16], toks % 16
+    kvd, qc = shape.kv_cols, shape.q_cols
+    for l in range(shape.layers):
+        torch.testing.assert_close(dst.tensor[l, 0, blk, slot].reshape(suffix, kvd).float(), ref[l, :, qc:qc + kvd],
+                                   atol=1e-2, rtol=1.6e-2)
+        torch.testing.assert_close(dst.tensor[l, 1, blk, slot].reshape(suffix, kvd).float(), ref[l, :, qc + kvd:],
+                                   atol=1e-2, rtol=1.6e-2)
