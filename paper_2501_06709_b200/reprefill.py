@@ -96,10 +96,11 @@ class ReprefillEngine:
     the destination from its (synthetic, seeded) hidden states.  One set of
     synthetic weights per (device, model shape)."""
 
-    def __init__(self, shapes, devices, with_q: bool = False, seed: int = 3):
+    def __init__(self, shapes, devices, with_q: bool = False, seed: int = 3, rope_theta: Optional[float] = None):
         shapes = [shapes] if isinstance(shapes, ModelShape) else list(shapes)
         self.shapes = {s.name: s for s in shapes}
         self.with_q = with_q
+        self.rope_theta = rope_theta   # post-RoPE K in the pool (KVM_REPREFILL_ROPE)
         self.weights = {(d, s.name): synthetic_weights(s, d, with_q=with_q, seed=seed)
                         for d in set(devices) for s in shapes}
 
@@ -115,7 +116,8 @@ class ReprefillEngine:
             x = self.hidden(pool.shape, rid, tokens, dev)
             blocks = torch.from_numpy(np.ascontiguousarray(dst_blocks, dtype=np.int32)).to(f"cuda:{dev}",
                                                                                           non_blocking=False)
-            reprefill(pool, x, self.weights[(dev, pool.shape.name)], blocks, tok0=0, stream=stream)
+            reprefill(pool, x, self.weights[(dev, pool.shape.name)], blocks, tok0=0, stream=stream,
+                      rope_theta=self.rope_theta)
             # keep the temporaries alive until the stream has consumed them
             x.record_stream(stream)
             blocks.record_stream(stream)
