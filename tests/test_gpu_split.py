@@ -156,3 +156,41 @@ def test_fused_split_with_rope(single_cta):
                                    atol=1e-2, rtol=1.6e-2)
         torch.testing.assert_close(dst.tensor[l, 1, blk, slot].reshape(suffix, kvd).float(), ref[l, :, qc + kvd:],
                                    atol=1e-2, rtol=1.6e-2)
+
+
+@pytest.mark.parametrize("single_cta", [False, True])
+def test_split_migrated_cache_decodes_like_the_original(single_cta):
+    """End to end through the consumer: the source cache is prefilled by the same
+    projection (+RoPE) for all n tokens; a split migration copies the prefix and
+    recomputes the suffix on the destination; paged decode over the migrated
+    cache must equal decode over the source.  The recomputed rows are the same
+    GEMM on the same inputs with the same per-element accumulation order, so
+    the migrated cache is BIT-IDENTICAL to the original (and so is decode)."""
+    from paper_2501_06709_b200.attention import paged_decode
+    from paper_2501_06709_b200.reprefill import reprefill
+    from paper_2501_06709_b200.split import split_migrate_fused
+
+    shape = ModelShape("e2e", layers=2, kv_heads=2, head_dim=128, q_heads=4, d_model=256)
+    n, suffix = 1000, 232
+    plan = make_split(n, suffix)
+    nb = plan.total_blocks + 8
+    src, dst = KVPool(shape, nb, dtype=torch.bfloat16), KVPool(shape, nb, dtype=torch.bfloat16)
+    dst.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(11))[:plan.total_blocks].to(torch.int32).cuda()
+    db = torch.from_numpy(dst.allocator.alloc(plan.total_blocks)).cuda()
+    x = synthetic_hidden(shape, n, 0, seed=12)
+    w = synthetic_weights(shape, 0, with_q=False, seed=13)
+    reprefill(src, x, w, sb, tok0=0, rope_theta=10000.0, single_cta=single_cta)   # the original prefill
+    xs = x[plan.prefix_tokens:].contiguous()
+    split_migrate_fused(src, dst, sb, db, plan, xs, w, single_cta=single_cta, rope_theta=10000.0)
+    torch.cuda.synchronize()
+    q = torch.randn(shape.layers, 1, shape.q_heads, 128, device="cuda").to(torch.bfloat16)
+    lens = torch.tensor([n], dtype=torch.int32, device="cuda")
+    a = paged_decode(src, q, sb[None].contiguous(), lens)
+    b = paged_decode(dst, q, db[None].contiguous(), lens)
+    torch.cuda.synchronize()
+    toks = torch.arange(n, device="cuda")   # every token slot of the request (the last block is partial)
+    got = dst.tensor[:, :, db.long()[toks // 16], toks % 16].view(torch.int16)
+    exp = src.tensor[:, :, sb.long()[toks // 16], toks % 16].view(torch.int16)
+    assert torch.equal(got, exp)
+    assert torch.equal(b.view(torch.int16), a.view(torch.int16))
