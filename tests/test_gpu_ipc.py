@@ -119,3 +119,71 @@ def test_two_process_ipc_push(engine):
         p.join(timeout=60)
     for rank, ok, err in res:
         assert ok, f"rank {rank} failed:\n{err}"
+
+
+def _split_worker(rank, world, port, result_q):
+    """Rank 0 owns the source pool; rank 1 imports it through CUDA IPC and runs the
+    fused split migration on its own GPU: the prefix is PULLED from the peer
+    pool by the re-prefill GEMM's idle warps, the suffix recomputed locally."""
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2501_06709_b200.dist import exchange_objects
+    from paper_2501_06709_b200.kvcache import KVPool, ModelShape
+    from paper_2501_06709_b200.reprefill import synthetic_hidden, synthetic_weights
+    from paper_2501_06709_b200.split import make_split, split_migrate_fused
+
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        shape = ModelShape("ipcs", layers=3, kv_heads=2, head_dim=128, q_heads=4, d_model=256)
+        plan = make_split(600, 88)
+        nb = plan.total_blocks + 6
+        pool = KVPool(shape, nb, device=0, dtype=torch.bfloat16)
+        pool.tensor.view(torch.int16).copy_(torch.randint(-2 ** 15, 2 ** 15, pool.view_shape, device="cuda:0",
+                                                          dtype=torch.int16,
+                                                          generator=torch.Generator(device="cuda:0")
+                                                          .manual_seed(50 + rank)))
+        torch.cuda.synchronize()
+        sb = torch.randperm(nb, generator=torch.Generator().manual_seed(3))[:plan.total_blocks].to(torch.int32)
+        info = exchange_objects((pool.ipc_handle(), pool.tensor.view(torch.int16).cpu() if rank == 0 else None))
+        ok = True
+        if rank == 1:
+            src = KVPool.from_ipc(shape, nb, 0, *info[0][0], dtype=torch.bfloat16)
+            db = torch.from_numpy(pool.allocator.alloc(plan.total_blocks)).cuda()
+            x = synthetic_hidden(shape, plan.suffix, 0, seed=8)
+            w = synthetic_weights(shape, 0, with_q=False, seed=9)
+            split_migrate_fused(src, pool, sb.cuda(), db, plan, x, w)
+            torch.cuda.synchronize()
+            pre = plan.prefix_blocks
+            got = pool.tensor.view(torch.int16)[:, :, db[:pre].long()].cpu()
+            ok = bool(torch.equal(got, info[0][1][:, :, sb[:pre].long()]))
+            toks = torch.arange(plan.prefix_tokens, 600, device="cuda")
+            ref = torch.einsum("tk,lnk->ltn", x.float(), w.float())
+            k = pool.tensor[:, 0, db.long()[toks // 16], toks % 16].reshape(shape.layers, plan.suffix, -1).float()
+            ok = ok and bool(torch.allclose(k, ref[:, :, :shape.kv_cols], atol=1e-2, rtol=1.6e-2))
+        dist.barrier()   # rank 0 keeps its pool alive until rank 1 has pulled
+        result_q.put((rank, ok, ""))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        result_q.put((rank, False, traceback.format_exc()))
+
+
+def test_two_process_split_pull():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, err in res:
+        assert ok, f"rank {rank} failed:\n{err}"
