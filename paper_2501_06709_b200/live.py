@@ -62,6 +62,7 @@ class LiveMigration:
         self.stats = LiveStats()
         self._t0 = time.perf_counter()
         self._keep = []
+        self._last = None   # event after the latest launched copy
         self._table = executor._table(dst_gpu, res.model)
 
     def _res(self) -> Residency:
@@ -92,6 +93,20 @@ class LiveMigration:
         s = self.ex.ordered_stream(self.src_pool.device)
         _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | self.flags,
                                                 ctypes.c_void_p(s.cuda_stream)), "kvm_migrate (live)")
+        import torch
+
+        self._last = torch.cuda.Event()
+        self._last.record(s)
+
+    def precopy_done(self) -> bool:
+        """Have all pre-copy rounds launched so far landed?  (Non-blocking: the
+        serving loop keeps decoding until this is true, then pauses.)"""
+        return self._last is None or self._last.query()
+
+    def drain(self) -> None:
+        """Wait (decode still running) until the launched pre-copy rounds landed."""
+        if self._last is not None:
+            self._last.synchronize()
 
     def precopy(self, after=None) -> int:
         """Asynchronously copy every block that became full since the last

@@ -4,7 +4,9 @@
 
 Both on one B200 (two pools).  Stop-and-copy: the request is paused for one
 full kvm_migrate of all its blocks.  Live: full blocks are pre-copied while
-(mock) decode keeps appending; the pause covers only the tail copy.  Times
+(mock) decode keeps appending; once the launched rounds have landed
+(`LiveMigration.drain`, decode still running) the request pauses and only the
+tail is copied.  Times
 are host wall clock around the paused section (what a serving loop sees),
 median over reps.
 """
@@ -63,7 +65,8 @@ def main():
                 lm.precopy(after=ev)
         ev.record(dec)
         dec.synchronize()
-        st = lm.finish(after=ev)
+        lm.drain()                    # decode keeps running until the pre-copy rounds landed ...
+        st = lm.finish(after=ev)      # ... then pause: only the tail is copied
         ex.release(rid)
         if rep:  # first rep warms up
             stop.append(t1 - t0)
