@@ -25,7 +25,7 @@ from __future__ import annotations
 import ctypes
 import time
 from dataclasses import dataclass, field
-from typing import List
+from typing import List, Optional
 
 import numpy as np
 
@@ -39,7 +39,8 @@ class LiveStats:
     rounds: int = 0
     blocks_precopied: int = 0
     blocks_stopcopied: int = 0
-    downtime_s: float = 0.0      # host wall time of finish(): pause -> switched
+    downtime_s: float = 0.0      # host wall time of finish(): pause -> switched (-> issued, stream-ordered)
+    done: Optional[object] = None  # stream-ordered finish: CUDA event after the tail copy + table rewrite
     total_s: float = 0.0
     round_blocks: List[int] = field(default_factory=list)
 
@@ -125,10 +126,17 @@ class LiveMigration:
             self.stats.round_blocks.append(n)
         return n
 
-    def finish(self, after=None) -> LiveStats:
+    def finish(self, after=None, stream_ordered: bool = False) -> LiveStats:
         """Pause point (decode stopped): copy the tail incl. the partial last
         block, switch residency, free the source blocks.  The destination
-        block-table row was filled piecewise by the copy kernels themselves."""
+        block-table row was filled piecewise by the copy kernels themselves.
+
+        stream_ordered: do not wait on the host; `stats.done` is an event the
+        destination's decode stream waits on (`wait_event`), so the GPU goes from
+        the last source decode step to the tail copy to the first destination
+        decode step without a host round trip."""
+        import torch
+
         t0 = time.perf_counter()
         if after is not None:
             self.ex.stream(self.src_pool.device).wait_event(after)
@@ -137,7 +145,11 @@ class LiveMigration:
         tail = n_all - self.copied
         self._copy(self.copied, n_all)
         self.copied = n_all
-        self.ex.stream(self.src_pool.device).synchronize()
+        if stream_ordered:
+            self.stats.done = torch.cuda.Event(enable_timing=True)
+            self.stats.done.record(self.ex.stream(self.src_pool.device))
+        else:
+            self.ex.stream(self.src_pool.device).synchronize()
         self.ex._commit([(self.rid, self.dst_gpu, res.tokens, self.dst_blocks)])
         t1 = time.perf_counter()
         self.stats.blocks_stopcopied = tail

@@ -29,8 +29,9 @@ def _decode_write(ex, rid, tok, stream):
         pool.tensor.view(torch.int16)[:, :, blk, slot] = v[:, :, None, None]
 
 
+@pytest.mark.parametrize("stream_ordered", [False, True])
 @pytest.mark.parametrize("prompt,decode_steps,precopy_every", [(100, 200, 16), (33, 50, 5), (512, 0, 1)])
-def test_live_migration_consistent(prompt, decode_steps, precopy_every):
+def test_live_migration_consistent(prompt, decode_steps, precopy_every, stream_ordered):
     pools = {0: KVPool(SHAPE, 128), 1: KVPool(SHAPE, 128)}
     tables = {0: BlockTable(4, 64), 1: BlockTable(4, 64)}
     ex = MigrationExecutor(pools, tables)
@@ -52,7 +53,9 @@ def test_live_migration_consistent(prompt, decode_steps, precopy_every):
     ev.record(dec)
     lm.precopy(after=ev)
     ev.record(dec)
-    st = lm.finish(after=ev)
+    st = lm.finish(after=ev, stream_ordered=stream_ordered)
+    if stream_ordered:   # the destination's decode stream would wait on this event
+        torch.cuda.current_stream().wait_event(st.done)
     assert ex.where(rid).gpu == 1
     assert st.blocks_stopcopied <= 2 or decode_steps == 0
     r = ex.where(rid)
