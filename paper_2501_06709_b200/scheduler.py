@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass, field
-from typing import Dict, FrozenSet, List, Optional, Sequence, Set, Tuple
+from typing import Dict, List, Optional, Sequence, Set, Tuple
 
 from . import _native
 from .cluster import (NONE, ClusterState, ItemId, SizeClass, class_of_code, classify_request,  # noqa: F401

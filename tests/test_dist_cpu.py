@@ -5,7 +5,6 @@ max-over-ranks timing reduction."""
 import os
 import socket
 
-import pytest
 
 from paper_2501_06709_b200.dist import RankInfo, ring_pairs
 

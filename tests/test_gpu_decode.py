@@ -4,7 +4,6 @@ the destination after a migration is bit-identical to decoding on the source
 before it."""
 import ctypes
 
-import numpy as np
 import pytest
 import torch
 
