@@ -613,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);      // both: multicast commit
-      mbar_init(tempty + a, 256);   // leader: 128 epilogue threads of each CTA
+      mbar_init(tempty + a, 8);     // leader: one elected lane per epilogue warp of each CTA
     }
     for (int i = 0; i < TQ; ++i) {
       mbar_init(tq.full + i, 1);
@@ -796,7 +796,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
         __syncwarp();
       }
       tc_fence_before();
-      arrive_remote(tempty_leader + (uint32_t)(acc * 8));
+      __syncwarp();  // every lane's TMEM reads of this accumulator are done
+      if (lane == 0) arrive_remote(tempty_leader + (uint32_t)(acc * 8));
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
