@@ -106,6 +106,7 @@ class MigrationExecutor:
 
         self.timing = timing
         self._events: Dict[int, list] = {}
+        self._pending: List[Tuple[list, bool]] = []   # wait=False calls awaiting commit()
         if engine not in ENGINES:
             raise ConfigError(f"engine must be one of {sorted(ENGINES)}")
         if not pools:
@@ -247,6 +248,8 @@ class MigrationExecutor:
                 if pm.mode not in (KV_TRANSFER, FORCED_KV_TRANSFER, TOKEN_TRANSFER):
                     raise ValueError(f"cannot execute mode {pm.mode!r}")
                 rids = list(members_of(mv.item)) if (members_of and mv.item < 0) else [mv.item]
+                if self._pending:
+                    self._check_not_pending(rids)
                 here = [r for r in rids if r in self.loc and self.loc[r].gpu == mv.src]
                 if pm.mode == TOKEN_TRANSFER and self.reprefill is None and here and mv.src != mv.dst:
                     raise ConfigError("token_transfer planned but executor has no re-prefill engine")
@@ -307,7 +310,7 @@ class MigrationExecutor:
             self.synchronize()
             self._commit(post)
         else:
-            self._pending_commit = post
+            self._pending.append((post, False))
         return report
 
     def compact(self, rid: int, wait: bool = True, row_out=None, stream_ordered: bool = False) -> ExecRecord:
@@ -323,6 +326,8 @@ class MigrationExecutor:
         move (and read-back).  Safe because every later launch touching this
         pool is queued behind it on the executor's ordered stream; it lets the
         host prepare the next call while the GPU copies."""
+        if self._pending:
+            self._check_not_pending([rid])
         res = self._res(rid)
         pool = self.pool(res.gpu, res.model)
         nb = len(res.blocks)
@@ -358,7 +363,7 @@ class MigrationExecutor:
             s.synchronize()
             self._commit(post, keep_table=True)
         else:
-            self._pending_commit = post
+            self._pending.append((post, True))
         return rec
 
     def split_move(self, rid: int, dst_gpu: int, suffix: Optional[int] = None, *, link_bytes_per_s: float = 770e9,
@@ -410,10 +415,18 @@ class MigrationExecutor:
                           plan.prefix_tokens, {rid: res.tokens})
 
     def commit(self) -> None:
-        """Finish a wait=False execute(): await streams, then free sources."""
+        """Finish every wait=False execute()/compact(): await streams, then free
+        the sources and switch residencies (in call order)."""
         self.synchronize()
-        self._commit(getattr(self, "_pending_commit", []))
-        self._pending_commit = []
+        pending, self._pending = self._pending, []
+        for post, keep_table in pending:
+            self._commit(post, keep_table=keep_table)
+
+    def _check_not_pending(self, rids) -> None:
+        busy = {rid for post, _ in self._pending for rid, *_ in post}
+        hit = busy.intersection(rids)
+        if hit:
+            raise ValueError(f"requests {sorted(hit)} have an uncommitted move: call commit() first")
 
     # -- internals ---------------------------------------------------------------
     def _launch_migrate(self, dev: int, moves: List[_native.Move]) -> None:

@@ -104,3 +104,18 @@ def test_execute_is_all_or_nothing_when_a_pool_is_full():
         ex.execute(plan)
     assert ex.pools[0]["mini"].allocator.n_free == free0 and ex.pools[1]["mini"].allocator.n_free == free1
     assert ex.where(1).gpu == 0 and ex.where(2).gpu == 0 and ex.launched == []
+
+
+def test_deferred_commits_accumulate_and_guard():
+    """Several wait=False executes before commit(): all are committed in order;
+    a request with an uncommitted move cannot be moved again."""
+    ex = _ex()
+    ex.admit(1, 0, 40)
+    ex.admit(2, 0, 40)
+    ex.execute([PlannedMove(PendingMove(1, 0, 1, 0, 40), KV_TRANSFER)], wait=False)
+    ex.execute([PlannedMove(PendingMove(2, 0, 1, 0, 40), KV_TRANSFER)], wait=False)
+    with pytest.raises(ValueError):
+        ex.execute([PlannedMove(PendingMove(1, 0, 1, 0, 40), KV_TRANSFER)], wait=False)
+    ex.commit()
+    assert ex.where(1).gpu == 1 and ex.where(2).gpu == 1
+    assert ex.pools[0]["mini"].allocator.n_free == 32

@@ -34,7 +34,7 @@ for i in range(K):
     rec = ex.compact(0, wait=False, row_out=row)
     t1 = time.perf_counter()
     ex.stream(0).synchronize()
-    ex._commit(ex._pending_commit, keep_table=True)
+    ex.commit()
     t2 = time.perf_counter()
     t_launch += t1 - t0
     t_total += t2 - t0
@@ -43,7 +43,7 @@ s = ex.stream(0)
 ev0.record(s)
 for i in range(K):
     ex.compact(0, wait=False)
-    ex._commit(ex._pending_commit, keep_table=True)
+    ex.commit()
 ev1.record(s)
 torch.cuda.synchronize()
 print({"host_issue_us": 1e6 * t_launch / K, "step_us": 1e6 * t_total / K,
