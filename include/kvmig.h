@@ -122,7 +122,7 @@ typedef struct kvm_reprefill_args {
   const int32_t* dst_blocks; /* device, n_dst_blocks entries */
   uint32_t* done_flag;    /* optional, set to done_value when all layers landed */
   uint32_t done_value;
-  int32_t flags;          /* 0 | KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE */
+  int32_t flags;          /* KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER */
   float rope_theta;       /* read only with KVM_REPREFILL_ROPE: the rotary base (Llama: 10000) */
 } kvm_reprefill_args;
 /* kvm_reprefill engine: default = CTA-pair kernel (tcgen05 cta_group::2, features
@@ -136,6 +136,10 @@ typedef struct kvm_reprefill_args {
  *   y[i+64] = x[i+64] cos(p theta_i) + x[i] sin(p theta_i)   (HF "rotate_half").
  * V is not rotated.  Needs head_dim 128. */
 #define KVM_REPREFILL_ROPE 0x2
+/* x holds per-layer hidden states, bf16 [layers][rows][d_model] (the input of
+ * each layer's projection, as a model forward produces them); default: one
+ * [rows][d_model] for every layer. */
+#define KVM_REPREFILL_X_PER_LAYER 0x4
 
 /* Adaptive split migration in ONE kernel on the destination GPU (extension of
  * the reference's all-or-nothing choice, migration.py:155-169): the first
@@ -161,7 +165,7 @@ typedef struct kvm_split_args {
   int32_t* dst_table_row; /* optional */
   uint32_t* done_flag;    /* optional */
   uint32_t done_value;
-  int32_t flags;          /* 0 | KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE */
+  int32_t flags;          /* KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER */
   float rope_theta;       /* read only with KVM_REPREFILL_ROPE */
 } kvm_split_args;
 

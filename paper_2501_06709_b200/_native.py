@@ -35,6 +35,7 @@ KVM_F_L2_EVICT_FIRST = 0x4
 KVM_MAX_MOVES = 96
 KVM_REPREFILL_SINGLE_CTA = 0x1
 KVM_REPREFILL_ROPE = 0x2
+KVM_REPREFILL_X_PER_LAYER = 0x4
 
 
 def KVM_F_CTAS_PER_SM(n: int) -> int:

@@ -60,6 +60,7 @@ struct Params {
   uint32_t* ctr;
   uint32_t* tile_ctr;   // pair kernel: dynamic tile counter (self-resetting)
   const float2* rope;   // KVM_REPREFILL_ROPE: (cos, sin) per [token t][i < 64] of the suffix, else NULL
+  int32_t x_per_layer;  // KVM_REPREFILL_X_PER_LAYER: tmap_x is 3D [layers][rows][d_model]
   int64_t plane_bytes;  // num_blocks * piece_bytes
   int64_t piece_bytes;
   int32_t rows, n_out, d_model, layers, q_cols, kvd, tok0, block_tokens, n_dst_blocks;
@@ -273,7 +274,10 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           mbar_expect_tx(full + stage, STAGE_BYTES);
-          tma_2d(&p.tmap_x, full + stage, sa, kb * BK, mt * BM);
+          if (p.x_per_layer)
+            tma_3d(&p.tmap_x, full + stage, sa, kb * BK, mt * BM, l);
+          else
+            tma_2d(&p.tmap_x, full + stage, sa, kb * BK, mt * BM);
           tma_3d(&p.tmap_w, full + stage, sb, kb * BK, nt * BN, l);
           if (++stage == STAGES) {
             stage = 0;
@@ -663,7 +667,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
           if (rank == 0) mbar_expect_tx(full + stage, 2 * STAGE_BYTES);
           const uint32_t bar = mapa(smem_u32(full + stage), 0);
           tma_3d_pair(&p.tmap_w, bar, sa, kb * BK, mt * BM + (int)rank * 128, l);
-          tma_2d_pair(&p.tmap_x, bar, sb, kb * BK, tt.start + (int)rank * half);
+          if (p.x_per_layer)
+            tma_3d_pair(&p.tmap_x, bar, sb, kb * BK, tt.start + (int)rank * half, l);
+          else
+            tma_2d_pair(&p.tmap_x, bar, sb, kb * BK, tt.start + (int)rank * half);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -875,7 +882,7 @@ struct DevCtr {
 // Encode X / W tensor maps and the GEMM geometry.  Returns KVM_OK or an error code.
 static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
                              int n_dst_blocks, const void* x, const void* w, void* q_out,
-                             const int32_t* dst_blocks, bool pair = false);
+                             const int32_t* dst_blocks, bool pair = false, bool x_per_layer = false);
 // Launch on the pool's device (current device already set); grid = min(work, SMs).
 static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream);
 // CTA-pair kernel: grid = 2 x min(work, co-resident clusters).
@@ -894,20 +901,22 @@ namespace rp {
 
 static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
                              int n_dst_blocks, const void* x, const void* w, void* q_out,
-                             const int32_t* dst_blocks, bool pair) {
+                             const int32_t* dst_blocks, bool pair, bool x_per_layer) {
   const kvm_pool_desc& d = pool->desc;
   const int kvd = d.kv_heads * d.head_dim;
   EncodeTiled enc = encode_fn();
   if (!enc) return fail(KVM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   const int n_out = q_cols + 2 * kvd;
   if (rows > 0) {
-    cuuint64_t dims[2] = {(cuuint64_t)d_model, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)d_model * 2};
-    cuuint32_t box[2] = {BK, BM};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(&p.tmap_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // x: [rows][d_model], or [layers][rows][d_model] with per-layer hidden states
+    cuuint64_t dims[3] = {(cuuint64_t)d_model, (cuuint64_t)rows, (cuuint64_t)d.layers};
+    cuuint64_t strides[2] = {(cuuint64_t)d_model * 2, (cuuint64_t)d_model * 2 * rows};
+    cuuint32_t box[3] = {BK, BM, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&p.tmap_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x_per_layer ? 3 : 2, const_cast<void*>(x), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    p.x_per_layer = x_per_layer ? 1 : 0;
     if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuTensorMapEncodeTiled(x) failed: " + std::to_string((int)r));
     cuuint64_t wd[3] = {(cuuint64_t)d_model, (cuuint64_t)n_out, (cuuint64_t)d.layers};
     cuuint64_t ws[2] = {(cuuint64_t)d_model * 2, (cuuint64_t)d_model * 2 * n_out};
@@ -1061,7 +1070,8 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a->x || !a->w || !a->dst_blocks) return fail(KVM_ERR_INVALID, "NULL x/w/dst_blocks");
   if ((int64_t)(a->tok0 + a->rows) > (int64_t)a->n_dst_blocks * d.block_tokens)
     return fail(KVM_ERR_INVALID, "dst_blocks do not cover tok0 + rows tokens");
-  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE)) return fail(KVM_ERR_INVALID, "unknown flags");
+  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER))
+    return fail(KVM_ERR_INVALID, "unknown flags");
   if ((a->flags & KVM_REPREFILL_ROPE) && (d.head_dim != 128 || !(a->rope_theta > 1.f)))
     return fail(KVM_ERR_CONFIG, "KVM_REPREFILL_ROPE needs head_dim 128 and rope_theta > 1");
   if (reinterpret_cast<uintptr_t>(a->x) % 16 || reinterpret_cast<uintptr_t>(a->w) % 16)
@@ -1072,7 +1082,7 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   memset(&p, 0, sizeof(p));
   const bool pair_kernel = !(a->flags & KVM_REPREFILL_SINGLE_CTA);
   int rc = build_gemm_params(p, pool, a->rows, a->d_model, a->q_cols, a->tok0, a->n_dst_blocks, a->x, a->w,
-                             a->q_out, a->dst_blocks, pair_kernel);
+                             a->q_out, a->dst_blocks, pair_kernel, (a->flags & KVM_REPREFILL_X_PER_LAYER) != 0);
   if (rc) return rc;
   p.done_flag = a->done_flag;
   p.done_value = a->done_value;
@@ -1108,7 +1118,8 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
     return fail(KVM_ERR_CONFIG, "kv_heads*head_dim and q_cols must be multiples of 32");
   if (!a->dst_blocks || (a->prefix_blocks && !a->src_blocks) || (suffix && (!a->x || !a->w)))
     return fail(KVM_ERR_INVALID, "NULL pointer argument");
-  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE)) return fail(KVM_ERR_INVALID, "unknown flags");
+  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER))
+    return fail(KVM_ERR_INVALID, "unknown flags");
   if ((a->flags & KVM_REPREFILL_ROPE) && (d.head_dim != 128 || !(a->rope_theta > 1.f)))
     return fail(KVM_ERR_CONFIG, "KVM_REPREFILL_ROPE needs head_dim 128 and rope_theta > 1");
   if (a->tokens == 0) return KVM_OK;
@@ -1118,7 +1129,7 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   memset(&p, 0, sizeof(p));
   const bool pair_kernel = !(a->flags & KVM_REPREFILL_SINGLE_CTA);
   int rc = build_gemm_params(p, dst, suffix, a->d_model, a->q_cols, a->prefix_blocks * bt, n_blocks, a->x, a->w,
-                             a->q_out, a->dst_blocks, pair_kernel);
+                             a->q_out, a->dst_blocks, pair_kernel, (a->flags & KVM_REPREFILL_X_PER_LAYER) != 0);
   if (rc) return rc;
   p.done_flag = a->done_flag;
   p.done_value = a->done_value;

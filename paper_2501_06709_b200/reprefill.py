@@ -49,7 +49,8 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
               rope_theta: Optional[float] = None) -> None:
     """Launch kvm_reprefill: K/V of tokens [tok0, tok0 + rows) into `dst_blocks`.
 
-    x: bf16 [rows][d_model] (device), w: bf16 [layers][n_out][d_model] with
+    x: bf16 [rows][d_model] (device) fed to every layer, or [layers][rows][d_model]
+    per-layer hidden states (KVM_REPREFILL_X_PER_LAYER), w: bf16 [layers][n_out][d_model] with
     n_out = q_cols + 2 * kv_cols, dst_blocks: int32 device tensor covering the
     token range, q_out: optional bf16 [layers][rows][q_cols].  single_cta
     selects the single-CTA kernel instead of the default CTA-pair one.
@@ -66,7 +67,10 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
         raise ConfigError("re-prefill writes bf16 K/V: pool dtype must be bfloat16")
     if not (x.is_contiguous() and w.is_contiguous()):
         raise ValueError("x and w must be contiguous")
-    rows, d_model = x.shape
+    per_layer = x.dim() == 3
+    if per_layer and x.shape[0] != shape.layers:
+        raise ConfigError(f"per-layer x must be [layers={shape.layers}][rows][d_model]")
+    rows, d_model = x.shape[-2:]
     if w.shape[0] != shape.layers or w.shape[2] != d_model:
         raise ConfigError(f"w must be [layers={shape.layers}][n_out][d_model={d_model}]")
     q_cols = w.shape[1] - 2 * shape.kv_cols
@@ -84,7 +88,7 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
     a.dst_blocks = dst_blocks.data_ptr()
     a.done_flag, a.done_value = done_flag or None, done_value
     a.flags = (_native.KVM_REPREFILL_SINGLE_CTA if single_cta else 0) | (
-        _native.KVM_REPREFILL_ROPE if rope_theta else 0)
+        _native.KVM_REPREFILL_ROPE if rope_theta else 0) | (_native.KVM_REPREFILL_X_PER_LAYER if per_layer else 0)
     a.rope_theta = float(rope_theta or 0.0)
     s = stream if stream is not None else torch.cuda.current_stream(pool.device)
     _native.check(_native.lib().kvm_reprefill(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),

@@ -113,8 +113,10 @@ def split_migrate_fused(src: KVPool, dst: KVPool, src_blocks_dev, dst_blocks_dev
     an IPC-imported peer pool: the prefix is then pulled over NVLink)."""
     import torch
 
-    if plan.suffix and (x_suffix is None or x_suffix.shape[0] != plan.suffix):
-        raise ValueError("x_suffix must have `suffix` rows")
+    per_layer = x_suffix is not None and x_suffix.dim() == 3   # [layers][suffix][d_model]
+    if plan.suffix and (x_suffix is None or x_suffix.shape[-2] != plan.suffix
+                        or (per_layer and x_suffix.shape[0] != dst.shape.layers)):
+        raise ValueError("x_suffix must be [suffix][d_model] or [layers][suffix][d_model]")
     q_cols = w.shape[1] - 2 * dst.shape.kv_cols
     a = _native.SplitArgs()
     a.src_pool, a.dst_pool, a.tokens, a.prefix_blocks = src.pool_id, dst.pool_id, plan.tokens, plan.prefix_blocks
@@ -125,7 +127,7 @@ def split_migrate_fused(src: KVPool, dst: KVPool, src_blocks_dev, dst_blocks_dev
     a.q_out = None
     a.dst_table_row, a.done_flag, a.done_value = table_row or None, done_flag or None, done_value
     a.flags = (_native.KVM_REPREFILL_SINGLE_CTA if single_cta else 0) | (   # GEMM engine (default: CTA pair)
-        _native.KVM_REPREFILL_ROPE if rope_theta else 0)
+        _native.KVM_REPREFILL_ROPE if rope_theta else 0) | (_native.KVM_REPREFILL_X_PER_LAYER if per_layer else 0)
     a.rope_theta = float(rope_theta or 0.0)
     s = stream if stream is not None else torch.cuda.current_stream(dst.device)
     _native.check(_native.lib().kvm_split_migrate(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),

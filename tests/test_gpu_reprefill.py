@@ -213,3 +213,62 @@ def test_reprefill_rope_needs_head_dim_128():
     w = synthetic_weights(shape, 0, with_q=False)
     with pytest.raises(ConfigError):
         reprefill(pool, x, w, torch.arange(1, dtype=torch.int32, device="cuda"), rope_theta=10000.0)
+
+
+@pytest.mark.parametrize("single_cta", [False, True])
+@pytest.mark.parametrize("rows,tok0,rope", [(1, 0, False), (300, 21, False), (1000, 3, True), (513, 4000, True)])
+def test_reprefill_per_layer_hidden(rows, tok0, rope, single_cta):
+    """KVM_REPREFILL_X_PER_LAYER: x is [layers][rows][d_model] and layer l's
+    K/V/Q come from x[l] (a model forward's per-layer inputs)."""
+    shape = ModelShape("xl", layers=4, kv_heads=2, head_dim=128, q_heads=4, d_model=256)
+    nblk = (tok0 + rows + 15) // 16
+    nb = nblk + 5
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    before = pool.tensor.view(torch.int16).clone()
+    blocks = torch.randperm(nb, generator=torch.Generator().manual_seed(rows + 1))[:nblk].to(torch.int32).cuda()
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    x = torch.randn(shape.layers, rows, shape.d_model, generator=g, device="cuda").to(torch.bfloat16)
+    w = synthetic_weights(shape, 0, with_q=True, seed=rows + 2)
+    q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda")
+    theta = 10000.0 if rope else None
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q, single_cta=single_cta, rope_theta=theta)
+    torch.cuda.synchronize()
+    ref = torch.einsum("ltk,lnk->ltn", x.float(), w.float())
+    if rope:
+        ref = _rope_ref(ref, torch.arange(tok0, tok0 + rows, device="cuda"), theta, shape.q_cols, shape.kv_cols)
+    _check(shape, pool, blocks, tok0, rows, ref, q, before)
+
+
+def test_reprefill_per_layer_13b_sampled():
+    """Per-layer x at the 13B balanced-split size (pair kernel), sampled layers."""
+    shape = LLAMA2_13B
+    rows, tok0 = 1360, 8192 - 1360
+    nblk = 8192 // 16
+    pool = KVPool(shape, nblk + 4, dtype=torch.bfloat16)
+    blocks = torch.randperm(nblk + 4, generator=torch.Generator().manual_seed(5))[:nblk].to(torch.int32).cuda()
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.randn(shape.layers, rows, shape.d_model, generator=g, device="cuda").to(torch.bfloat16)
+    w = synthetic_weights(shape, 0, with_q=True, seed=7)
+    reprefill(pool, x, w, blocks, tok0=tok0)
+    torch.cuda.synchronize()
+    kvd, qc = shape.kv_cols, shape.q_cols
+    toks = torch.arange(tok0, tok0 + rows, device="cuda")
+    blk, slot = blocks.long()[toks // 16], toks % 16
+    for l in (0, 1, 22, 39):
+        ref = x[l].float() @ w[l].float().t()
+        torch.testing.assert_close(pool.tensor[l, 0, blk, slot].reshape(rows, kvd).float(), ref[:, qc:qc + kvd],
+                                   atol=ATOL, rtol=RTOL)
+        torch.testing.assert_close(pool.tensor[l, 1, blk, slot].reshape(rows, kvd).float(), ref[:, qc + kvd:],
+                                   atol=ATOL, rtol=RTOL)
+
+
+def test_reprefill_per_layer_wrong_layers():
+    from paper_2501_06709_b200.errors import ConfigError
+
+    shape = ModelShape("xl2", layers=2, kv_heads=2, head_dim=64, q_heads=2, d_model=128)
+    pool = KVPool(shape, 4, dtype=torch.bfloat16)
+    x = torch.zeros(3, 16, 128, dtype=torch.bfloat16, device="cuda")
+    w = synthetic_weights(shape, 0, with_q=False)
+    with pytest.raises(ConfigError):
+        reprefill(pool, x, w, torch.arange(1, dtype=torch.int32, device="cuda"))

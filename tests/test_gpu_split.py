@@ -158,14 +158,16 @@ def test_fused_split_with_rope(single_cta):
                                    atol=1e-2, rtol=1.6e-2)
 
 
+@pytest.mark.parametrize("per_layer", [False, True])
 @pytest.mark.parametrize("single_cta", [False, True])
-def test_split_migrated_cache_decodes_like_the_original(single_cta):
+def test_split_migrated_cache_decodes_like_the_original(single_cta, per_layer):
     """End to end through the consumer: the source cache is prefilled by the same
     projection (+RoPE) for all n tokens; a split migration copies the prefix and
     recomputes the suffix on the destination; paged decode over the migrated
     cache must equal decode over the source.  The recomputed rows are the same
     GEMM on the same inputs with the same per-element accumulation order, so
-    the migrated cache is BIT-IDENTICAL to the original (and so is decode)."""
+    the migrated cache is BIT-IDENTICAL to the original (and so is decode).
+    per_layer: every layer has its own hidden states (KVM_REPREFILL_X_PER_LAYER)."""
     from paper_2501_06709_b200.attention import paged_decode
     from paper_2501_06709_b200.reprefill import reprefill
     from paper_2501_06709_b200.split import split_migrate_fused
@@ -178,10 +180,14 @@ def test_split_migrated_cache_decodes_like_the_original(single_cta):
     dst.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
     sb = torch.randperm(nb, generator=torch.Generator().manual_seed(11))[:plan.total_blocks].to(torch.int32).cuda()
     db = torch.from_numpy(dst.allocator.alloc(plan.total_blocks)).cuda()
-    x = synthetic_hidden(shape, n, 0, seed=12)
+    if per_layer:
+        g = torch.Generator(device="cuda").manual_seed(12)
+        x = torch.randn(shape.layers, n, shape.d_model, generator=g, device="cuda").to(torch.bfloat16)
+    else:
+        x = synthetic_hidden(shape, n, 0, seed=12)
     w = synthetic_weights(shape, 0, with_q=False, seed=13)
     reprefill(src, x, w, sb, tok0=0, rope_theta=10000.0, single_cta=single_cta)   # the original prefill
-    xs = x[plan.prefix_tokens:].contiguous()
+    xs = x[..., plan.prefix_tokens:, :].contiguous()
     split_migrate_fused(src, dst, sb, db, plan, xs, w, single_cta=single_cta, rope_theta=10000.0)
     torch.cuda.synchronize()
     q = torch.randn(shape.layers, 1, shape.q_heads, 128, device="cuda").to(torch.bfloat16)
