@@ -65,6 +65,15 @@ extern "C" {
 #define KVM_F_L2_EVICT_FIRST 0x4 /* stream the KV through L2 with an evict-first
                                     cache policy (keeps a co-running kernel's
                                     working set, e.g. re-prefill weights, in L2) */
+#define KVM_F_SYS_SCOPE 0x8       /* publish table rows / flags at system scope even
+                                    when every written pointer is this GPU's own
+                                    memory: set it when a PEER GPU or the host
+                                    polls a flag that lives here.  Without it the
+                                    scope is derived per move: .gpu if the dst
+                                    pool, table row and flags are all memory of
+                                    the launching GPU, else .sys.  Moves with no
+                                    table row and no flags do no completion
+                                    accounting at all (stream order publishes). */
 /* Cap the copy kernel at n CTAs per SM (bits 8..15; 0 = occupancy maximum), so
  * it can share SMs with a concurrently running persistent kernel (e.g. the
  * re-prefill GEMM of a split move on the same GPU). */

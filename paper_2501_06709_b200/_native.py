@@ -32,6 +32,7 @@ KVM_NONE = -(2 ** 63)
 KVM_F_BLOCKS_ON_HOST = 0x1
 KVM_F_ENGINE_BULK = 0x2
 KVM_F_L2_EVICT_FIRST = 0x4
+KVM_F_SYS_SCOPE = 0x8
 KVM_MAX_MOVES = 96
 KVM_REPREFILL_SINGLE_CTA = 0x1
 KVM_REPREFILL_ROPE = 0x2

@@ -43,6 +43,7 @@
 #include <deque>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "kvmig_common.cuh"
@@ -84,6 +85,33 @@ const Pool* get_pool(int id) {
   return &g_pools[id];  // entries are never erased, only marked dead
 }
 
+// IPC-imported mappings [begin, end): memory of another process (and maybe GPU).
+static std::mutex g_ipc_mu;
+static std::vector<std::pair<uintptr_t, uintptr_t>> g_ipc_maps;
+static bool ipc_imported(const void* ptr) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(ptr);
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (const auto& m : g_ipc_maps)
+    if (a >= m.first && a < m.second) return true;
+  return false;
+}
+
+// Allocation containing `ptr`, via the driver API (no -lcuda link dependency).
+static int address_range(const void* ptr, CUdeviceptr* base, size_t* size) {
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    KVM_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn) return fail(KVM_ERR_UNSUPPORTED, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUresult r = get_range(base, size, reinterpret_cast<CUdeviceptr>(ptr));
+  if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuMemGetAddressRange failed: " + std::to_string((int)r));
+  return KVM_OK;
+}
+
 static int g_sm_count[64] = {0};
 int sm_count(int device) {
   if (device < 0 || device >= 64) return 148;
@@ -120,15 +148,40 @@ struct DevMove {
   int32_t n_blocks;
   int32_t layers;
   uint32_t done_value;
-  int32_t _pad;
+  int16_t sys_scope;         // 1: a completion observer may be off this GPU -> .sys fences
+  int16_t track;             // 0: no table row / flags -> no completion accounting at all
 };
 
-struct MigrateParams {
+// Kernel parameter block, sized per launch class.  kMoves moves; with
+// kInline > 0 the block lists of move 0 may travel inline (src at blocks[i],
+// dst at blocks[kInline + i]; marked by src_blocks == NULL), so a small move
+// with host-side lists needs no staging copy.  A one-move launch passes ~1.2
+// KiB of parameters instead of ~11 KiB.
+template <int kMoves, int kInline>
+struct MigrateParamsT {
+  static constexpr int kInlineBlocks = kInline;
   int32_t n_moves;
   int32_t per_layer_flush;   // 1: flush at (move, layer) granularity
   int64_t total_tiles;
-  DevMove m[KVM_MAX_MOVES];
+  DevMove m[kMoves];
+  int32_t blocks[kInline > 0 ? 2 * kInline : 1];
 };
+constexpr int kSmallInline = 128;
+using BatchParams = MigrateParamsT<KVM_MAX_MOVES, 0>;
+using SmallParams = MigrateParamsT<1, kSmallInline>;
+
+template <class P>
+__device__ __forceinline__ int64_t src_block(const P& p, const DevMove& mv, int i) {
+  if constexpr (P::kInlineBlocks > 0)
+    if (mv.src_blocks == nullptr) return p.blocks[i];
+  return __ldg(mv.src_blocks + i);
+}
+template <class P>
+__device__ __forceinline__ int64_t dst_block(const P& p, const DevMove& mv, int i) {
+  if constexpr (P::kInlineBlocks > 0)
+    if (mv.src_blocks == nullptr) return p.blocks[P::kInlineBlocks + i];
+  return __ldg(mv.dst_blocks + i);
+}
 
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
@@ -168,7 +221,8 @@ struct TileRef {
   int len;
 };
 
-__device__ __forceinline__ TileRef decode_tile(const MigrateParams& p, int64_t t, int& cur) {
+template <class P>
+__device__ __forceinline__ TileRef decode_tile(const P& p, int64_t t, int& cur) {
   while (cur + 1 < p.n_moves && t >= p.m[cur + 1].tile_begin) ++cur;
   const DevMove& mv = p.m[cur];
   const int32_t local = (int32_t)(t - mv.tile_begin);
@@ -177,8 +231,8 @@ __device__ __forceinline__ TileRef decode_tile(const MigrateParams& p, int64_t t
   const int32_t r = local - plane * per_plane;
   const int32_t bi = r / mv.tpp;
   const int32_t ti = r - bi * mv.tpp;
-  const int64_t sb = __ldg(mv.src_blocks + bi);
-  const int64_t db = __ldg(mv.dst_blocks + bi);
+  const int64_t sb = src_block(p, mv, bi);
+  const int64_t db = dst_block(p, mv, bi);
   const int64_t off = (int64_t)ti * kTileBytes;
   TileRef tr;
   tr.move = cur;
@@ -192,20 +246,25 @@ __device__ __forceinline__ TileRef decode_tile(const MigrateParams& p, int64_t t
 // Called by ONE thread after the CTA's stores for `key` are ordered before it
 // (bar.sync / bulk wait_group + this fence).  Returns 1 if this call completed
 // the whole move (caller then runs finalize_move with the CTA / warp).
-__device__ __forceinline__ int account(const MigrateParams& p, int move, int layer, int ntiles) {
+// Moves without a table row or flags (track == 0) skip this entirely: stream
+// order alone publishes their bytes.
+template <class P>
+__device__ __forceinline__ int account(const P& p, int move, int layer, int ntiles) {
   const DevMove& mv = p.m[move];
-  fence_acq_rel_sys();
+  if (!mv.track) return 0;
+  const bool sys = mv.sys_scope != 0;
+  fence_acq_rel(sys);
   const uint32_t per_layer = 2u * (uint32_t)mv.n_blocks * (uint32_t)mv.tpp;
   if (p.per_layer_flush) {
     uint32_t old = atomicAdd(mv.ctr + layer, (uint32_t)ntiles);
     if (old + (uint32_t)ntiles == per_layer) {
       mv.ctr[layer] = 0;  // self-reset: nobody else touches it this launch
-      fence_acq_rel_sys();
-      if (mv.layer_flags) st_release_sys_u32(mv.layer_flags + layer, mv.done_value);
+      fence_acq_rel(sys);
+      if (mv.layer_flags) st_release_u32(mv.layer_flags + layer, mv.done_value, sys);
       uint32_t o2 = atomicAdd(mv.ctr + mv.layers, 1u);
       if (o2 + 1 == (uint32_t)mv.layers) {
         mv.ctr[mv.layers] = 0;
-        fence_acq_rel_sys();
+        fence_acq_rel(sys);
         return 1;
       }
     }
@@ -214,7 +273,7 @@ __device__ __forceinline__ int account(const MigrateParams& p, int move, int lay
     uint32_t old = atomicAdd(mv.ctr + mv.layers, (uint32_t)ntiles);
     if (old + (uint32_t)ntiles == total) {
       mv.ctr[mv.layers] = 0;
-      fence_acq_rel_sys();
+      fence_acq_rel(sys);
       return 1;
     }
   }
@@ -224,22 +283,22 @@ __device__ __forceinline__ int account(const MigrateParams& p, int move, int lay
 // Block-table rewrite + done flag; executed by `nthr` cooperating threads,
 // `tid` in [0, nthr).  sync() must order all threads' table stores before the
 // single release store of the flag.
-template <bool kCta>
-__device__ __forceinline__ void finalize_move(const DevMove& mv, int tid, int nthr) {
+template <bool kCta, class P>
+__device__ __forceinline__ void finalize_move(const P& p, const DevMove& mv, int tid, int nthr) {
   if (mv.table_row) {
-    for (int i = tid; i < mv.n_blocks; i += nthr) mv.table_row[i] = __ldg(mv.dst_blocks + i);
+    for (int i = tid; i < mv.n_blocks; i += nthr) mv.table_row[i] = (int32_t)dst_block(p, mv, i);
   }
   if (kCta) __syncthreads(); else __syncwarp();
   if (tid == 0) {
-    fence_acq_rel_sys();
-    if (mv.done_flag) st_release_sys_u32(mv.done_flag, mv.done_value);
+    fence_acq_rel(mv.sys_scope != 0);
+    if (mv.done_flag) st_release_u32(mv.done_flag, mv.done_value, mv.sys_scope != 0);
   }
 }
 
 // ------------------------- LDG/STG engine ----------------------------------
-template <bool kEvictFirst>
+template <bool kEvictFirst, class P>
 __global__ void __launch_bounds__(kLdgThreads)
-    migrate_ldg_kernel(const __grid_constant__ MigrateParams p) {
+    migrate_ldg_kernel(const __grid_constant__ P p) {
   __shared__ int s_done;
   const uint64_t pol = kEvictFirst ? l2_evict_first_policy() : 0;
   int cur = 0;
@@ -253,7 +312,7 @@ __global__ void __launch_bounds__(kLdgThreads)
         __syncthreads();
         if (tid == 0) s_done = account(p, key_move, key_layer, key_n);
         __syncthreads();
-        if (s_done) finalize_move<true>(p.m[key_move], tid, kLdgThreads);
+        if (s_done) finalize_move<true>(p, p.m[key_move], tid, kLdgThreads);
       }
       key_move = tr.move;
       key_layer = lay;
@@ -287,13 +346,14 @@ __global__ void __launch_bounds__(kLdgThreads)
     __syncthreads();
     if (tid == 0) s_done = account(p, key_move, key_layer, key_n);
     __syncthreads();
-    if (s_done) finalize_move<true>(p.m[key_move], tid, kLdgThreads);
+    if (s_done) finalize_move<true>(p, p.m[key_move], tid, kLdgThreads);
   }
 }
 
 // ------------------------- bulk-copy (TMA unit) engine ---------------------
-constexpr int kBulkStages = 4;
-constexpr int kBulkLag = 2;   // loads in flight; stages - lag stores in flight
+constexpr int kBulkStages = 4;        // batch launches (1 CTA/SM)
+constexpr int kBulkStagesSmall = 2;   // one-move launches: 3 CTAs/SM, one tile each
+constexpr int bulk_smem_bytes(int stages) { return stages * kTileBytes + 64; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -353,9 +413,12 @@ __device__ __forceinline__ void bulk_wait_all() {
 }
 
 // One warp per CTA; lane 0 drives the bulk unit, the warp cooperates on the
-// block-table rewrite.  Dynamic smem: kBulkStages * kTileBytes + barriers.
-template <bool kEvictFirst>
-__global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant__ MigrateParams p) {
+// block-table rewrite.  Dynamic smem: kStages * kTileBytes + barriers.
+// kStages / 2 loads in flight, the other half of the stages drain stores.
+template <bool kEvictFirst, class P, int kStages>
+__global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant__ P p) {
+  constexpr int kBulkStages = kStages;
+  constexpr int kBulkLag = kStages / 2;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint64_t pol = kEvictFirst ? l2_evict_first_policy() : 0;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBulkStages * kTileBytes);
@@ -392,7 +455,7 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
             done = account(p, key_move, key_layer, key_n);
           }
           done = __shfl_sync(0xffffffffu, done, 0);
-          if (done) finalize_move<false>(p.m[key_move], lane, 32);
+          if (done) finalize_move<false>(p, p.m[key_move], lane, 32);
         }
         key_move = mv;
         key_layer = ly;
@@ -427,20 +490,22 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
       done = account(p, key_move, key_layer, key_n);
     }
     done = __shfl_sync(0xffffffffu, done, 0);
-    if (done) finalize_move<false>(p.m[key_move], lane, 32);
+    if (done) finalize_move<false>(p, p.m[key_move], lane, 32);
   }
 }
 
 // Moves with zero blocks: publish their (empty) completion without a copy.
-__global__ void finalize_empty_kernel(const __grid_constant__ MigrateParams p) {
+template <class P>
+__global__ void finalize_empty_kernel(const __grid_constant__ P p) {
   for (int m = 0; m < p.n_moves; ++m) {
     const DevMove& mv = p.m[m];
     if (mv.n_blocks != 0) continue;
     if (threadIdx.x == 0) {
-      fence_acq_rel_sys();
+      const bool sys = mv.sys_scope != 0;
+      fence_acq_rel(sys);
       if (mv.layer_flags)
-        for (int l = 0; l < mv.layers; ++l) st_release_sys_u32(mv.layer_flags + l, mv.done_value);
-      if (mv.done_flag) st_release_sys_u32(mv.done_flag, mv.done_value);
+        for (int l = 0; l < mv.layers; ++l) st_release_u32(mv.layer_flags + l, mv.done_value, sys);
+      if (mv.done_flag) st_release_u32(mv.done_flag, mv.done_value, sys);
     }
   }
 }
@@ -486,7 +551,8 @@ struct DevState {
   Slot slots[kSlots];
   int next = 0;
   int ldg_grid = 0;
-  int bulk_grid = 0;
+  int bulk_grid = 0;        // kBulkStages CTAs
+  int bulk_grid_small = 0;  // kBulkStagesSmall CTAs
 };
 static DevState g_dev[64];
 static std::mutex g_dev_mu[64];
@@ -496,16 +562,24 @@ static int dev_init(int device, DevState& ds) {
   for (int i = 0; i < kSlots; ++i)
     KVM_CUDA_TRY(cudaEventCreateWithFlags(&ds.slots[i].ev, cudaEventDisableTiming));
   int occ = 0;
-  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, migrate_ldg_kernel<false>, kLdgThreads, 0));
+  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, migrate_ldg_kernel<false, BatchParams>,
+                                                             kLdgThreads, 0));
   ds.ldg_grid = sm_count(device) * std::max(occ, 1);
-  const size_t bulk_smem = kBulkStages * kTileBytes + 64;
-  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)bulk_smem));
-  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)bulk_smem));
-  int occb = 0;
-  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occb, migrate_bulk_kernel<false>, 32, bulk_smem));
+  const int big = bulk_smem_bytes(kBulkStages), small = bulk_smem_bytes(kBulkStagesSmall);
+  const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<false, BatchParams, kBulkStages>, attr, big));
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<true, BatchParams, kBulkStages>, attr, big));
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<false, SmallParams, kBulkStagesSmall>, attr, small));
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<false, SmallParams, kBulkStages>, attr, big));
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<true, SmallParams, kBulkStages>, attr, big));
+  KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<true, SmallParams, kBulkStagesSmall>, attr, small));
+  int occb = 0, occs = 0;
+  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occb, migrate_bulk_kernel<false, BatchParams, kBulkStages>, 32, big));
+  KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occs, migrate_bulk_kernel<false, SmallParams, kBulkStagesSmall>, 32, small));
   ds.bulk_grid = sm_count(device) * std::max(occb, 1);
+  ds.bulk_grid_small = sm_count(device) * std::max(occs, 1);
   ds.init = true;
   return KVM_OK;
 }
@@ -562,24 +636,73 @@ static int validate_blocks_host(const int32_t* b, int n, int nb, const char* wha
   return KVM_OK;
 }
 
-static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t stream) {
-  const Pool* sp0 = get_pool(moves[0].src_pool);
-  if (!sp0) return KVM_ERR_NOT_FOUND;
-  const int device = sp0->device;
-  std::lock_guard<std::mutex> lk(g_dev_mu[device]);
-  DeviceGuard dg(device);
-  DevState& ds = g_dev[device];
-  int rc = dev_init(device, ds);
-  if (rc) return rc;
+// Is `ptr` memory of `device` itself (not host, managed, a peer or an IPC
+// import)?  Decides the completion scope of a move's table row / flags.
+static bool local_device_ptr(const void* ptr, int device) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice && a.device == device && !ipc_imported(ptr);
+}
 
-  static MigrateParams p;  // large; guarded by g_dev_mu[device] (one device at a time per call)
-  static std::mutex p_mu;
-  std::lock_guard<std::mutex> lkp(p_mu);
+template <class P>
+static int launch_copy(const P& p, int64_t tiles, bool any_empty, int flags, int device, const DevState& ds,
+                       cudaStream_t stream) {
+  constexpr bool kSmall = std::is_same<P, SmallParams>::value;
+  if (tiles > 0) {
+    const int cap = (flags >> 8) & 0xff;
+    const int nsm = sm_count(device);
+    // A move that fits in one tile per CTA of the 2-stage kernel (3 CTAs/SM)
+    // gets it: more SMs' worth of bulk units for a latency-bound copy.  Larger
+    // moves keep the 4-stage pipeline (1 CTA/SM), which streams better.
+    const bool shallow = kSmall && tiles <= ds.bulk_grid_small && !cap;
+    if ((flags & KVM_F_ENGINE_BULK) && shallow) {
+      const int grid = (int)tiles;
+      const int smem = bulk_smem_bytes(kBulkStagesSmall);
+      if (flags & KVM_F_L2_EVICT_FIRST)
+        migrate_bulk_kernel<true, P, kBulkStagesSmall><<<grid, 32, smem, stream>>>(p);
+      else
+        migrate_bulk_kernel<false, P, kBulkStagesSmall><<<grid, 32, smem, stream>>>(p);
+    } else if (flags & KVM_F_ENGINE_BULK) {
+      const int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.bulk_grid, cap * nsm) : ds.bulk_grid);
+      const int smem = bulk_smem_bytes(kBulkStages);
+      if (flags & KVM_F_L2_EVICT_FIRST)
+        migrate_bulk_kernel<true, P, kBulkStages><<<grid, 32, smem, stream>>>(p);
+      else
+        migrate_bulk_kernel<false, P, kBulkStages><<<grid, 32, smem, stream>>>(p);
+    } else {
+      const int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.ldg_grid, cap * nsm) : ds.ldg_grid);
+      if (flags & KVM_F_L2_EVICT_FIRST)
+        migrate_ldg_kernel<true, P><<<grid, kLdgThreads, 0, stream>>>(p);
+      else
+        migrate_ldg_kernel<false, P><<<grid, kLdgThreads, 0, stream>>>(p);
+    }
+    KVM_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  }
+  if (any_empty) {
+    finalize_empty_kernel<P><<<1, 32, 0, stream>>>(p);
+    KVM_CUDA_TRY(cudaGetLastError());
+    count_launch();
+  }
+  return KVM_OK;
+}
+
+// Validate, fill the parameter block, stage what must be staged, launch.
+template <class P>
+static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaStream_t stream, int device,
+                           DevState& ds) {
   memset(&p, 0, sizeof(p));
   p.n_moves = n;
-  bool any_layer_flags = false;
+  bool any_layer_flags = false, any_track = false, any_empty = false;
+  const bool on_host = (flags & KVM_F_BLOCKS_ON_HOST) != 0;
+  // one host-listed move that fits: its lists ride in the parameters
+  const bool inline_lists = P::kInlineBlocks > 0 && on_host && n == 1 && moves[0].n_blocks <= P::kInlineBlocks;
   size_t host_bytes = 0, ctrs = 0;
   int64_t tiles = 0;
+  int rc;
   for (int i = 0; i < n; ++i) {
     const kvm_move& mv = moves[i];
     const Pool* sp = get_pool(mv.src_pool);
@@ -595,15 +718,27 @@ static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t s
     if (mv.n_blocks < 0) return fail(KVM_ERR_INVALID, "n_blocks < 0");
     if (mv.n_blocks > 0 && (!mv.src_blocks || !mv.dst_blocks))
       return fail(KVM_ERR_INVALID, "NULL block list");
-    if (flags & KVM_F_BLOCKS_ON_HOST) {
+    if (on_host) {
       if ((rc = validate_blocks_host(mv.src_blocks, mv.n_blocks, a.num_blocks, "src_blocks"))) return rc;
       if ((rc = validate_blocks_host(mv.dst_blocks, mv.n_blocks, b.num_blocks, "dst_blocks"))) return rc;
-      host_bytes += 2 * sizeof(int32_t) * (size_t)mv.n_blocks;
-      host_bytes = (host_bytes + 15) & ~size_t(15);
+      if (!inline_lists) {
+        host_bytes += 2 * sizeof(int32_t) * (size_t)mv.n_blocks;
+        host_bytes = (host_bytes + 15) & ~size_t(15);
+      }
+    }
+    DevMove& d = p.m[i];
+    d.track = (mv.dst_table_row || mv.done_flag || mv.layer_flags) ? 1 : 0;
+    if (d.track) {
+      bool local = !(flags & KVM_F_SYS_SCOPE) && dp->device == device && !dp->remote;
+      if (local && mv.dst_table_row) local = local_device_ptr(mv.dst_table_row, device);
+      if (local && mv.done_flag) local = local_device_ptr(mv.done_flag, device);
+      if (local && mv.layer_flags) local = local_device_ptr(mv.layer_flags, device);
+      d.sys_scope = local ? 0 : 1;
+      ctrs += (size_t)a.layers + 1;
+      any_track = true;
     }
     if (mv.layer_flags) any_layer_flags = true;
-    ctrs += (size_t)a.layers + 1;
-    DevMove& d = p.m[i];
+    any_empty |= (mv.n_blocks == 0);
     d.src = sp->base;
     d.dst = dp->base;
     d.table_row = mv.dst_table_row;
@@ -622,16 +757,25 @@ static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t s
   p.total_tiles = tiles;
   p.per_layer_flush = any_layer_flags ? 1 : 0;
 
+  // A staging slot is needed only for host lists that are not inline and for
+  // completion counters; an untracked inline move is parameters only.
   Slot* slot = nullptr;
-  if ((rc = slot_acquire(ds, host_bytes, ctrs, &slot))) return rc;
-  // stage host block lists and counters
+  if (host_bytes > 0 || any_track)
+    if ((rc = slot_acquire(ds, host_bytes, ctrs, &slot))) return rc;
   size_t off = 0, coff = 0;
   for (int i = 0; i < n; ++i) {
     DevMove& d = p.m[i];
     const kvm_move& mv = moves[i];
-    d.ctr = slot->ctr + coff;
-    coff += (size_t)d.layers + 1;
-    if (flags & KVM_F_BLOCKS_ON_HOST) {
+    if (d.track) {
+      d.ctr = slot->ctr + coff;
+      coff += (size_t)d.layers + 1;
+    }
+    if (inline_lists) {
+      memcpy(p.blocks, mv.src_blocks, sizeof(int32_t) * mv.n_blocks);
+      memcpy(p.blocks + P::kInlineBlocks, mv.dst_blocks, sizeof(int32_t) * mv.n_blocks);
+      d.src_blocks = nullptr;   // marks the inline lists
+      d.dst_blocks = nullptr;
+    } else if (on_host) {
       uint8_t* h = static_cast<uint8_t*>(slot->host) + off;
       memcpy(h, mv.src_blocks, sizeof(int32_t) * mv.n_blocks);
       memcpy(h + sizeof(int32_t) * mv.n_blocks, mv.dst_blocks, sizeof(int32_t) * mv.n_blocks);
@@ -644,38 +788,32 @@ static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t s
       d.dst_blocks = mv.dst_blocks;
     }
   }
-  if ((flags & KVM_F_BLOCKS_ON_HOST) && off > 0)
-    KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
-
-  bool any_empty = false;
-  for (int i = 0; i < n; ++i) any_empty |= (moves[i].n_blocks == 0);
-  if (tiles > 0) {
-    const int cap = (flags >> 8) & 0xff;
-    const int nsm = sm_count(device);
-    if (flags & KVM_F_ENGINE_BULK) {
-      int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.bulk_grid, cap * nsm) : ds.bulk_grid);
-      if (flags & KVM_F_L2_EVICT_FIRST)
-        migrate_bulk_kernel<true><<<grid, 32, kBulkStages * kTileBytes + 64, stream>>>(p);
-      else
-        migrate_bulk_kernel<false><<<grid, 32, kBulkStages * kTileBytes + 64, stream>>>(p);
-    } else {
-      int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.ldg_grid, cap * nsm) : ds.ldg_grid);
-      if (flags & KVM_F_L2_EVICT_FIRST)
-        migrate_ldg_kernel<true><<<grid, kLdgThreads, 0, stream>>>(p);
-      else
-        migrate_ldg_kernel<false><<<grid, kLdgThreads, 0, stream>>>(p);
-    }
-    KVM_CUDA_TRY(cudaGetLastError());
-    count_launch();
+  if (off > 0) KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
+  if ((rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream))) return rc;
+  if (slot) {
+    KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
+    slot->pending = true;
   }
-  if (any_empty) {
-    finalize_empty_kernel<<<1, 32, 0, stream>>>(p);
-    KVM_CUDA_TRY(cudaGetLastError());
-    count_launch();
-  }
-  KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
-  slot->pending = true;
   return KVM_OK;
+}
+
+static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t stream) {
+  const Pool* sp0 = get_pool(moves[0].src_pool);
+  if (!sp0) return KVM_ERR_NOT_FOUND;
+  const int device = sp0->device;
+  std::lock_guard<std::mutex> lk(g_dev_mu[device]);
+  DeviceGuard dg(device);
+  DevState& ds = g_dev[device];
+  int rc = dev_init(device, ds);
+  if (rc) return rc;
+  if (n == 1) {
+    SmallParams p;   // ~1.2 KiB
+    return migrate_batch_t(p, moves, n, flags, stream, device, ds);
+  }
+  static BatchParams p;  // ~11 KiB; guarded by p_mu
+  static std::mutex p_mu;
+  std::lock_guard<std::mutex> lkp(p_mu);
+  return migrate_batch_t(p, moves, n, flags, stream, device, ds);
 }
 
 }  // namespace kvm
@@ -766,6 +904,15 @@ int kvm_pool_register(int device, void* base, const kvm_pool_desc* desc) {
   p.piece_bytes = piece;
   p.plane_bytes = piece * desc->num_blocks;
   p.token_bytes = (int64_t)desc->kv_heads * desc->head_dim * desc->elem_bytes;
+  {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, base) != cudaSuccess) {
+      cudaGetLastError();
+      p.remote = true;
+    } else {
+      p.remote = pa.type != cudaMemoryTypeDevice || pa.device != device || ipc_imported(base);
+    }
+  }
   std::lock_guard<std::mutex> lk(g_mu);
   g_pools.push_back(p);
   return (int)g_pools.size() - 1;
@@ -789,20 +936,10 @@ int kvm_pool_piece_bytes(int pool, int64_t* out) {
 
 int kvm_ipc_export(const void* ptr, void* handle64, int64_t* offset_out) {
   if (!ptr || !handle64 || !offset_out) return fail(KVM_ERR_INVALID, "NULL argument");
-  // Find the allocation base with the driver API (no -lcuda link dependency).
-  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
-  static GetRange get_range = nullptr;
-  if (!get_range) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    KVM_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
-    if (!fn) return fail(KVM_ERR_UNSUPPORTED, "cuMemGetAddressRange unavailable");
-    get_range = reinterpret_cast<GetRange>(fn);
-  }
   CUdeviceptr base = 0;
   size_t size = 0;
-  CUresult r = get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr));
-  if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuMemGetAddressRange failed: " + std::to_string((int)r));
+  int rc = address_range(ptr, &base, &size);
+  if (rc) return rc;
   cudaIpcMemHandle_t h;
   KVM_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
@@ -818,13 +955,28 @@ int kvm_ipc_import(int device, const void* handle64, int64_t offset, void** ptr_
   memcpy(&h, handle64, 64);
   void* base = nullptr;
   KVM_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  CUdeviceptr rb = 0;
+  size_t size = 0;
+  if (address_range(base, &rb, &size) == KVM_OK) {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    g_ipc_maps.push_back({(uintptr_t)base, (uintptr_t)base + size});
+  }
   *ptr_out = static_cast<uint8_t*>(base) + offset;
   return KVM_OK;
 }
 
 int kvm_ipc_close(void* mapped_ptr, int64_t offset) {
   if (!mapped_ptr) return fail(KVM_ERR_INVALID, "NULL argument");
-  KVM_CUDA_TRY(cudaIpcCloseMemHandle(static_cast<uint8_t*>(mapped_ptr) - offset));
+  void* base = static_cast<uint8_t*>(mapped_ptr) - offset;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (size_t i = 0; i < g_ipc_maps.size(); ++i)
+      if (g_ipc_maps[i].first == (uintptr_t)base) {
+        g_ipc_maps.erase(g_ipc_maps.begin() + i);
+        break;
+      }
+  }
+  KVM_CUDA_TRY(cudaIpcCloseMemHandle(base));
   return KVM_OK;
 }
 
@@ -832,7 +984,8 @@ int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream) {
   if (n_moves < 0) return fail(KVM_ERR_INVALID, "n_moves < 0");
   if (n_moves == 0) return KVM_OK;
   if (!moves) return fail(KVM_ERR_INVALID, "moves is NULL");
-  if (flags & ~(KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK | KVM_F_L2_EVICT_FIRST | KVM_F_CTAS_PER_SM(0xff)))
+  if (flags & ~(KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK | KVM_F_L2_EVICT_FIRST | KVM_F_SYS_SCOPE |
+                KVM_F_CTAS_PER_SM(0xff)))
     return fail(KVM_ERR_INVALID, "unknown flags");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < n_moves; i += KVM_MAX_MOVES) {

@@ -28,6 +28,7 @@ struct Pool {
   int64_t piece_bytes = 0;  // block_tokens * kv_heads * head_dim * elem_bytes
   int64_t plane_bytes = 0;  // num_blocks * piece_bytes  (one (layer, K|V) plane)
   int64_t token_bytes = 0;  // kv_heads * head_dim * elem_bytes (one token row)
+  bool remote = false;      // memory lives off `device` (IPC import / peer mapping)
 };
 
 // Look up a registered pool; returns nullptr (and sets the error) if unknown.
@@ -46,6 +47,20 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
 }
 __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+// Scope-selected variants: `sys` when an observer of the completion stores
+// may sit off this GPU (peer GPU, host); .gpu is ~4 us cheaper per fence.
+__device__ __forceinline__ void fence_acq_rel(bool sys) {
+  if (sys)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 }  // namespace kvm

@@ -332,3 +332,48 @@ def test_compact_stream_ordered_back_to_back():
     assert np.array_equal(rows[1].numpy()[:len(expect[-1])], expect[-1])
     now = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(ex.where(5).blocks).long().cuda()]
     assert torch.equal(now, orig)
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 300])
+@pytest.mark.parametrize("consumers", ["none", "device", "host_flag", "sys_scope"])
+def test_single_move_launch_class(engine, n, consumers):
+    """One-move launches use the small parameter block: host lists of <= 128
+    blocks ride inline (no staging copy), larger ones are staged; moves with no
+    table row / flags skip completion accounting; completion stores are .gpu
+    scope when every written pointer is this GPU's memory, .sys for a flag in
+    pinned host memory or with KVM_F_SYS_SCOPE.  Bytes, row and flags exact."""
+    nb = 2 * n + 8
+    src, dst = KVPool(SMALL, nb), KVPool(SMALL, nb)
+    _fill(src, n)
+    _fill(dst, n + 1)
+    rng = np.random.default_rng(n)
+    sb = rng.permutation(nb)[:n].astype(np.int32)
+    dst.allocator.take(rng.permutation(nb)[:3])
+    db = dst.allocator.alloc(n)
+    exp = dst.tensor.view(torch.int16).cpu().numpy()
+    row_exp = orc.migrate(src.tensor.view(torch.int16).cpu().numpy(), _desc(src), exp, _desc(dst), sb, db)
+    table = BlockTable(2, n + 4)
+    lflags = torch.zeros(SMALL.layers, dtype=torch.int32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    flags = _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine]
+    if consumers == "none":
+        m = _move(src, dst, sb, db)
+    elif consumers == "host_flag":
+        flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+        m = _move(src, dst, sb, db, table.row_ptr(1), flag.data_ptr(), lflags.data_ptr(), value=7)
+    else:
+        m = _move(src, dst, sb, db, table.row_ptr(1), flag.data_ptr(), lflags.data_ptr(), value=7)
+        if consumers == "sys_scope":
+            flags |= _native.KVM_F_SYS_SCOPE
+    _run([m], flags)
+    assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
+    if consumers != "none":
+        assert np.array_equal(table.rows[table.slot(1), :n].cpu().numpy(), row_exp)
+        assert flag.item() == 7
+        assert lflags.cpu().tolist() == [7] * SMALL.layers
+    # back to back on one stream, alternating inline / staged: no slot reuse hazard
+    for k in range(40):
+        _native.check(_native.lib().kvm_migrate(ctypes.byref(_move(src, dst, sb, db)), 1, flags, _stream()))
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
