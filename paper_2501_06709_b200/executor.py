@@ -68,6 +68,10 @@ class ExecReport:
     # the first launch of this call to the last (CUDA events on the executor's
     # stream), in ms
     device_ms: Dict[int, float] = field(default_factory=dict)
+    # stream_ordered execute(): destination device -> event after its incoming
+    # moves landed; source device -> event after its launches
+    done: Dict[int, object] = field(default_factory=dict)
+    src_done: Dict[int, object] = field(default_factory=dict)
 
     @property
     def copy_GBps(self) -> Optional[float]:
@@ -224,11 +228,21 @@ class MigrationExecutor:
 
     # -- execution ---------------------------------------------------------------
     def execute(self, plan, members_of: Optional[Callable[[int], Sequence[int]]] = None,
-                wait: bool = True) -> ExecReport:
+                wait: bool = True, stream_ordered: bool = False) -> ExecReport:
         """Carry out `plan.executed` (or a list of PlannedMove) in plan order.
 
         members_of(item) -> request ids of a group item (negative id); the
         default treats every item as a single request.
+
+        stream_ordered: return right after issuing, with residencies already
+        switched on the host.  Each destination GPU's executor stream waits
+        (cudaStreamWaitEvent, no host round trip) on the copy launched on every
+        source GPU that feeds it, and `report.done[dst_device]` / `rec.done`
+        is an event after which the destination's blocks and table row are
+        final: a decode stream `wait_event`s on it.  Freed source blocks may
+        be reallocated by the host at once; launches that reuse them must be
+        queued behind the move (the executor's own streams are; a caller's
+        stream waits on `report.src_done[src_device]`).
         """
         executed: List[PlannedMove] = plan.executed if isinstance(plan, MigrationPlan) else [
             p for p in plan if p.mode != "deferred"]
@@ -304,7 +318,10 @@ class MigrationExecutor:
         for dev, moves in by_dev.items():
             self._launch_migrate(dev, moves)
             report.launches += 1
-        if wait:
+        if stream_ordered:
+            self._order_across_devices(report, work)
+            self._commit(post)
+        elif wait:
             if self.timing:
                 self._close_timing(report)
             self.synchronize()
@@ -312,6 +329,32 @@ class MigrationExecutor:
         else:
             self._pending.append((post, False))
         return report
+
+    def _order_across_devices(self, report: "ExecReport", work) -> None:
+        """Stream-ordered completion: one event per source device after its
+        launches; each destination device's stream waits on the events of the
+        sources that feed it, then records its own done event."""
+        import torch
+
+        feeds: Dict[int, set] = {}
+        for pm, rec, items in work:
+            for rid, res, src_pool, dst_pool, dst_blocks in items:
+                feeds.setdefault(dst_pool.device, set()).add(src_pool.device)
+        for dev in sorted({d for srcs in feeds.values() for d in srcs}):
+            ev = torch.cuda.Event()
+            ev.record(self.stream(dev))
+            report.src_done[dev] = ev
+        for dst, srcs in sorted(feeds.items()):
+            s = self.stream(dst)
+            for src in sorted(srcs):
+                if src != dst:
+                    s.wait_event(report.src_done[src])
+            ev = torch.cuda.Event(enable_timing=self.timing)
+            ev.record(s)
+            report.done[dst] = ev
+        for pm, rec, items in work:
+            if items:
+                rec.done = report.done[items[0][3].device]
 
     def compact(self, rid: int, wait: bool = True, row_out=None, stream_ordered: bool = False) -> ExecRecord:
         """1-GPU case: move a request into the lowest free blocks of its own

@@ -377,3 +377,42 @@ def test_single_move_launch_class(engine, n, consumers):
         _native.check(_native.lib().kvm_migrate(ctypes.byref(_move(src, dst, sb, db)), 1, flags, _stream()))
     torch.cuda.synchronize()
     assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
+
+
+def test_executor_stream_ordered_chain():
+    """execute(stream_ordered=True): no host wait; residencies switch at issue,
+    so the same request can be moved again at once (0 -> 1 -> 2); a consumer
+    stream that waits on `report.done` sees the final bytes and table row."""
+    from paper_2501_06709_b200.executor import MigrationExecutor
+    from paper_2501_06709_b200.planner import KV_TRANSFER, PendingMove, PlannedMove
+
+    pools = {g: KVPool(SMALL, 64) for g in range(3)}
+    tables = {g: BlockTable(8, 16) for g in range(3)}
+    ex = MigrationExecutor(pools, tables)
+    _fill(pools[0], 21)
+    ex.admit(5, 0, 70)
+    ex.admit(6, 0, 33)
+    src_np = pools[0].tensor.view(torch.int16).cpu().numpy()
+    b5, b6 = ex.where(5).blocks.copy(), ex.where(6).blocks.copy()
+    bpt = SMALL.kv_bytes_per_token
+    r1 = ex.execute([PlannedMove(PendingMove(5, 0, 1, 70 * bpt, 70), KV_TRANSFER),
+                     PlannedMove(PendingMove(6, 0, 2, 33 * bpt, 33), KV_TRANSFER)], stream_ordered=True)
+    assert ex.where(5).gpu == 1 and ex.where(6).gpu == 2
+    assert set(r1.src_done) == {0} and set(r1.done) == {0}   # all logical GPUs share cuda:0
+    assert r1.records[0].done is r1.done[0]
+    # the freed source blocks are reused at once by a new request, written on the executor's stream
+    ex.admit(7, 0, 16 * 7)
+    with torch.cuda.stream(ex.stream(0)):
+        pools[0].tensor[:, :, ex.where(7).blocks.tolist()] = 0
+    r2 = ex.execute([PlannedMove(PendingMove(5, 1, 2, 70 * bpt, 70), KV_TRANSFER)], stream_ordered=True)
+    consumer = torch.cuda.Stream()
+    consumer.wait_event(r2.done[0])
+    with torch.cuda.stream(consumer):
+        got5 = pools[2].tensor[:, :, ex.where(5).blocks.tolist()].clone()
+        got6 = pools[2].tensor[:, :, ex.where(6).blocks.tolist()].clone()
+        row5 = tables[2].rows[tables[2].slot(5), :len(b5)].clone()
+    consumer.synchronize()
+    assert np.array_equal(got5.view(torch.int16).cpu().numpy(), src_np[:, :, b5])
+    assert np.array_equal(got6.view(torch.int16).cpu().numpy(), src_np[:, :, b6])
+    assert np.array_equal(row5.cpu().numpy(), ex.where(5).blocks)
+    assert pools[1].allocator.n_free == 64
