@@ -28,6 +28,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <string>
 #include <type_traits>
@@ -445,12 +446,33 @@ __global__ void __launch_bounds__(D) decode_combine_kernel(const __grid_constant
   static_cast<T*>(p.out)[((int64_t)lb * p.q_heads + qh) * D + d] = static_cast<T>(L > 0.f ? A / L : 0.f);
 }
 
+// Split-K partials, one workspace per (device, stream): decode calls on
+// different streams of one GPU may run concurrently; calls on one stream are
+// ordered by it.  `last` (recorded after each use) is waited on by the next
+// use, which only matters if a destroyed stream's handle is reused while its
+// work is still queued.  Idle workspaces beyond kMaxWorkspaces are freed.
 struct Workspace {
   float* ptr = nullptr;
   size_t floats = 0;
+  cudaEvent_t last = nullptr;
 };
-static Workspace g_ws[64];
+static std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
 static std::mutex g_ws_mu;
+constexpr size_t kMaxWorkspaces = 16;
+
+static void trim_workspaces(int device) {
+  for (auto it = g_ws.begin(); it != g_ws.end() && g_ws.size() > kMaxWorkspaces;) {
+    Workspace& w = it->second;
+    if (it->first.first == device && (!w.last || cudaEventQuery(w.last) == cudaSuccess)) {
+      if (w.ptr) cudaFree(w.ptr);
+      if (w.last) cudaEventDestroy(w.last);
+      it = g_ws.erase(it);
+    } else {
+      cudaGetLastError();   // cudaErrorNotReady from the query is not an error
+      ++it;
+    }
+  }
+}
 
 template <typename T>
 static int launch_combine(const Params& p, cudaStream_t st) {
@@ -576,27 +598,37 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
   cudaGetDevice(&cur);
   if (cur != pool->device) cudaSetDevice(pool->device);
   int rc = KVM_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::unique_lock<std::mutex> lk(g_ws_mu, std::defer_lock);
+  Workspace* w = nullptr;
   if (p.splits > 1) {
     const size_t slots = (size_t)a->n_layers * a->batch * a->q_heads * p.splits;
     const size_t need = slots * (D + 2);
-    std::lock_guard<std::mutex> lk(g_ws_mu);
-    Workspace& w = g_ws[pool->device];
-    if (w.floats < need) {
-      if (w.ptr) cudaFree(w.ptr);  // implicit device sync: only on growth
-      w.ptr = nullptr;
-      w.floats = 0;
-      cudaError_t e = cudaMalloc(&w.ptr, need * sizeof(float));
-      if (e != cudaSuccess) rc = cuda_fail(e, "decode workspace");
-      else w.floats = need;
+    lk.lock();
+    if (g_ws.size() >= kMaxWorkspaces) trim_workspaces(pool->device);
+    w = &g_ws[{pool->device, st}];
+    cudaError_t e = cudaSuccess;
+    if (!w->last) e = cudaEventCreateWithFlags(&w->last, cudaEventDisableTiming);
+    else e = cudaStreamWaitEvent(st, w->last, 0);
+    if (e == cudaSuccess && w->floats < need) {
+      if (w->ptr) cudaFree(w->ptr);  // implicit device sync: only on growth
+      w->ptr = nullptr;
+      w->floats = 0;
+      e = cudaMalloc(&w->ptr, need * sizeof(float));
+      if (e == cudaSuccess) w->floats = need;
     }
-    p.ws_acc = w.ptr;
-    p.ws_ml = w.ptr + slots * D;
+    if (e != cudaSuccess) rc = cuda_fail(e, "decode workspace");
+    p.ws_acc = w->ptr;
+    p.ws_ml = w->ptr + slots * D;
   }
   const bool tensor_path = !(a->flags & KVM_DECODE_CUDA_CORES);
   if (!rc)
-    rc = (a->flags & KVM_DECODE_BF16)
-             ? launch_t<__nv_bfloat16>(p, G, static_cast<cudaStream_t>(stream), tensor_path)
-             : launch_t<__half>(p, G, static_cast<cudaStream_t>(stream), tensor_path);
+    rc = (a->flags & KVM_DECODE_BF16) ? launch_t<__nv_bfloat16>(p, G, st, tensor_path)
+                                      : launch_t<__half>(p, G, st, tensor_path);
+  if (!rc && w) {
+    cudaError_t e = cudaEventRecord(w->last, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "decode workspace event");
+  }
   if (cur != pool->device) cudaSetDevice(cur);
   return rc;
 }

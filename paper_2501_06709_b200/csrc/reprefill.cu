@@ -877,7 +877,25 @@ struct DevCtr {
   uint32_t* ctr = nullptr;  // 64 self-resetting completion counters (one per in-flight launch) + 64 tile counters
   uint32_t next = 0;
   bool attr = false;
+  cudaEvent_t used[64] = {};  // after the launch that last took slot i: a reuse waits on it (device side)
 };
+
+// Take the next counter slot for a launch on `stream`: if the launch that
+// held it may still be queued (another stream, 64 launches ago), the new one
+// waits for it on the device.  Called with g_rp_mu held.
+static int take_ctr_slot(DevCtr& dc, cudaStream_t stream, int* slot) {
+  if (!dc.ctr) {
+    KVM_CUDA_TRY(cudaMalloc(&dc.ctr, 128 * sizeof(uint32_t)));
+    KVM_CUDA_TRY(cudaMemset(dc.ctr, 0, 128 * sizeof(uint32_t)));
+  }
+  const int i = (int)(dc.next++ % 64);
+  if (!dc.used[i])
+    KVM_CUDA_TRY(cudaEventCreateWithFlags(&dc.used[i], cudaEventDisableTiming));
+  else
+    KVM_CUDA_TRY(cudaStreamWaitEvent(stream, dc.used[i], 0));
+  *slot = i;
+  return KVM_OK;
+}
 
 // Encode X / W tensor maps and the GEMM geometry.  Returns KVM_OK or an error code.
 static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
@@ -958,10 +976,6 @@ static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model,
 static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(g_rp_mu);
   DevCtr& dc = g_ctr[dev];
-  if (!dc.ctr) {
-    KVM_CUDA_TRY(cudaMalloc(&dc.ctr, 128 * sizeof(uint32_t)));
-    KVM_CUDA_TRY(cudaMemset(dc.ctr, 0, 128 * sizeof(uint32_t)));
-  }
   if (!dc.attr) {
     KVM_CUDA_TRY(cudaFuncSetAttribute(reprefill_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM_BYTES));
@@ -969,7 +983,10 @@ static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
                                       SMEM_BYTES));
     dc.attr = true;
   }
-  p.ctr = dc.ctr + (dc.next++ % 64);
+  int slot = 0;
+  int rc = take_ctr_slot(dc, stream, &slot);
+  if (rc) return rc;
+  p.ctr = dc.ctr + slot;
   int64_t work = p.total_tiles;
   if (copy) work = std::max<int64_t>(work, (p.c_units + 1) / 2);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sm_count(dev)));
@@ -979,6 +996,7 @@ static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
     reprefill_kernel<false><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
+  KVM_CUDA_TRY(cudaEventRecord(dc.used[slot], stream));
   return KVM_OK;
 }
 
@@ -987,10 +1005,6 @@ static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
   static int clusters[64] = {};
   std::lock_guard<std::mutex> lk(g_rp_mu);
   DevCtr& dc = g_ctr[dev];
-  if (!dc.ctr) {
-    KVM_CUDA_TRY(cudaMalloc(&dc.ctr, 128 * sizeof(uint32_t)));
-    KVM_CUDA_TRY(cudaMemset(dc.ctr, 0, 128 * sizeof(uint32_t)));
-  }
   if (!attr[dev]) {
     KVM_CUDA_TRY(cudaFuncSetAttribute(pair::reprefill_pair_kernel<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES));
@@ -1008,8 +1022,11 @@ static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
     clusters[dev] = n;
     attr[dev] = true;
   }
-  p.tile_ctr = dc.ctr + 64 + (dc.next % 64);
-  p.ctr = dc.ctr + (dc.next++ % 64);
+  int slot = 0;
+  int rc = take_ctr_slot(dc, stream, &slot);
+  if (rc) return rc;
+  p.tile_ctr = dc.ctr + 64 + slot;
+  p.ctr = dc.ctr + slot;
   int64_t work = p.total_tiles;
   if (copy) work = std::max<int64_t>(work, (p.c_units + 3) / 4);  // ~4 copy warps per cluster
   const int grid = 2 * (int)std::max<int64_t>(1, std::min<int64_t>(work, clusters[dev]));
@@ -1019,6 +1036,7 @@ static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
     pair::reprefill_pair_kernel<false><<<grid, THREADS, pair::SMEM_BYTES, stream>>>(p);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
+  KVM_CUDA_TRY(cudaEventRecord(dc.used[slot], stream));
   return KVM_OK;
 }
 

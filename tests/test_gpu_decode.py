@@ -70,3 +70,33 @@ def test_decode_after_migration_is_bit_identical():
     after = paged_decode(dst, q, table.rows[table.slot(0)][None].contiguous(), lens)   # the rewritten row
     torch.cuda.synchronize()
     assert torch.equal(before.view(torch.int16), after.view(torch.int16))
+
+
+def test_decode_concurrent_streams_have_private_workspaces():
+    """Split-K decode on several streams of one GPU at once (each call's
+    partials in its own per-stream workspace): every stream's outputs equal the
+    same calls run one at a time, bit for bit."""
+    shape = ModelShape("dws", layers=4, kv_heads=2, head_dim=128, q_heads=8, d_model=256)
+    seq = 6000   # long enough for many splits
+    nb = 4 * ((seq + 15) // 16) + 8
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    _fill_normal(pool, 5)
+    maxb = (seq + 15) // 16
+    perm = torch.randperm(nb, generator=torch.Generator().manual_seed(6))[:4 * maxb].to(torch.int32)
+    tables = perm.view(4, maxb).contiguous().cuda()
+    lens = torch.tensor([seq, seq - 100, 4000, seq], dtype=torch.int32, device="cuda")
+    qs = [torch.randn(4, 4, 8, 128, generator=torch.Generator(device="cuda").manual_seed(10 + i),
+                      device="cuda").to(torch.bfloat16) for i in range(4)]
+    expect = [paged_decode(pool, q, tables, lens, max_seq_len=seq) for q in qs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in qs]
+    for s in streams:
+        s.wait_stream(torch.cuda.current_stream())
+    outs = [torch.empty_like(q) for q in qs]
+    for rep in range(20):
+        for s, q, o in zip(streams, qs, outs):
+            paged_decode(pool, q, tables, lens, out=o, max_seq_len=seq, stream=s)
+    for s in streams:
+        s.synchronize()
+    for o, e in zip(outs, expect):
+        assert torch.equal(o.view(torch.int16), e.view(torch.int16))

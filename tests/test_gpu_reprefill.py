@@ -272,3 +272,31 @@ def test_reprefill_per_layer_wrong_layers():
     w = synthetic_weights(shape, 0, with_q=False)
     with pytest.raises(ConfigError):
         reprefill(pool, x, w, torch.arange(1, dtype=torch.int32, device="cuda"))
+
+
+def test_reprefill_many_launches_on_two_streams():
+    """150 re-prefill launches alternating between two streams (more than the
+    64 completion / tile counter slots, so slots are reused while the other
+    stream may still hold them): every result matches fp32."""
+    shape = ModelShape("two", layers=2, kv_heads=2, head_dim=64, q_heads=2, d_model=128)
+    rows = 40
+    nblk = (rows + 15) // 16
+    pools = [KVPool(shape, nblk + 2, dtype=torch.bfloat16) for _ in range(2)]
+    blocks = torch.arange(nblk, dtype=torch.int32, device="cuda")
+    xs = [synthetic_hidden(shape, rows, 0, seed=30 + i) for i in range(2)]
+    w = synthetic_weights(shape, 0, with_q=False, seed=32)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for s in streams:
+        s.wait_stream(torch.cuda.current_stream())
+    for k in range(150):
+        i = k % 2
+        reprefill(pools[i], xs[i], w, blocks, stream=streams[i], single_cta=(k % 3 == 0))
+    torch.cuda.synchronize()
+    kvd = shape.kv_cols
+    toks = torch.arange(rows, device="cuda")
+    for i in range(2):
+        ref = _ref(xs[i], w)
+        for l in range(shape.layers):
+            t = pools[i].tensor
+            k_ = t[l, 0, blocks.long()[toks // 16], toks % 16].reshape(rows, kvd).float()
+            torch.testing.assert_close(k_, ref[l, :, :kvd], atol=ATOL, rtol=RTOL)
