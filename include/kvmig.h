@@ -261,6 +261,18 @@ int kvm_can_access_peer(int dev, int peer, int* out);
 /* --- pools ----------------------------------------------------------------- */
 /* Register a borrowed device allocation as a pool; returns pool id >= 0. */
 int kvm_pool_register(int device, void* base, const kvm_pool_desc* desc);
+/* Register a pool laid out by another engine: one base pointer per layer
+ * (host array of desc->layers device pointers), and the piece of (layer l,
+ * K|V kv, block b) -- block_tokens x kv_heads x head_dim contiguous elements --
+ * at layer_bases[l] + kv * kv_stride + b * block_stride (bytes).  vLLM's
+ * per-layer caches are this: FlashAttention backend [2][blocks][16][H][D]
+ * (kv_stride = blocks * piece, block_stride = piece), FlashInfer backend
+ * [blocks][2][16][H][D] (kv_stride = piece, block_stride = 2 * piece).
+ * kvm_migrate / kvm_compact accept any mix of native and strided pools with
+ * the same piece size (pieces are copied as opaque bytes); decode, re-prefill
+ * and split need native pools (KVM_ERR_UNSUPPORTED otherwise). */
+int kvm_pool_register_strided(int device, const kvm_pool_desc* desc, void* const* layer_bases, int64_t kv_stride,
+                              int64_t block_stride);
 int kvm_pool_unregister(int pool);
 int kvm_pool_piece_bytes(int pool, int64_t* out);
 int kvm_pool_bytes(const kvm_pool_desc* desc, int64_t* out);

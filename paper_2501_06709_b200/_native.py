@@ -45,7 +45,7 @@ def KVM_F_CTAS_PER_SM(n: int) -> int:
 # Every symbol include/kvmig.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "kvm_version", "kvm_last_error", "kvm_device_count", "kvm_init", "kvm_can_access_peer",
-    "kvm_pool_register", "kvm_pool_unregister", "kvm_pool_piece_bytes", "kvm_pool_bytes",
+    "kvm_pool_register", "kvm_pool_register_strided", "kvm_pool_unregister", "kvm_pool_piece_bytes", "kvm_pool_bytes",
     "kvm_ipc_export", "kvm_ipc_import", "kvm_ipc_close",
     "kvm_migrate", "kvm_compact", "kvm_wait_flag", "kvm_reprefill", "kvm_paged_decode",
     "kvm_plan_hybrid", "kvm_wait_flag_timeout", "kvm_split_migrate", "kvm_launch_count",
@@ -140,6 +140,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kvm_init": ([I], I),
         "kvm_can_access_peer": ([I, I, ctypes.POINTER(I)], I),
         "kvm_pool_register": ([I, P, ctypes.POINTER(PoolDesc)], I),
+        "kvm_pool_register_strided": ([I, ctypes.POINTER(PoolDesc), ctypes.POINTER(P), I64, I64], I),
         "kvm_pool_unregister": ([I], I),
         "kvm_pool_piece_bytes": ([I, ctypes.POINTER(I64)], I),
         "kvm_pool_bytes": ([ctypes.POINTER(PoolDesc), ctypes.POINTER(I64)], I),

@@ -539,6 +539,7 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
   if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
   const Pool* pool = get_pool(a->pool);
   if (!pool) return KVM_ERR_NOT_FOUND;
+  if (pool->strided) return fail(KVM_ERR_UNSUPPORTED, "paged decode needs a native pool (not a strided one)");
   const kvm_pool_desc& d = pool->desc;
   if (d.head_dim != D) return fail(KVM_ERR_UNSUPPORTED, "kvm_paged_decode supports head_dim 128");
   if (d.elem_bytes != 2 || d.block_tokens != 16) return fail(KVM_ERR_UNSUPPORTED, "needs 16-bit KV, 16-token blocks");

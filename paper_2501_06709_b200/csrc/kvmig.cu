@@ -140,8 +140,10 @@ struct DevMove {
   uint32_t* done_flag;       // nullable
   uint32_t* layer_flags;     // nullable
   uint32_t* ctr;             // [layers + 1] self-resetting counters
-  int64_t src_plane;         // bytes per (layer, K|V) plane in src pool
-  int64_t dst_plane;
+  const uint8_t* const* src_layers;  // strided src pool: per-layer bases (device), else NULL
+  uint8_t* const* dst_layers;
+  int64_t src_layer_stride, src_kv_stride, src_block_stride;   // bytes (Pool fields)
+  int64_t dst_layer_stride, dst_kv_stride, dst_block_stride;
   int64_t tile_begin;        // first global tile index of this move
   int32_t piece;             // bytes per piece (same for src and dst)
   int32_t tpp;               // tiles per piece
@@ -237,8 +239,18 @@ __device__ __forceinline__ TileRef decode_tile(const P& p, int64_t t, int& cur) 
   TileRef tr;
   tr.move = cur;
   tr.layer = plane >> 1;
-  tr.src = mv.src + plane * mv.src_plane + sb * mv.piece + off;
-  tr.dst = mv.dst + plane * mv.dst_plane + db * mv.piece + off;
+  const int kv = plane & 1;
+  // layer base: native pools by stride, strided (foreign-layout) pools through their pointer array
+  const uint8_t* sl =
+      mv.src_layers
+          ? reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(mv.src_layers) + tr.layer))
+          : mv.src + tr.layer * mv.src_layer_stride;
+  uint8_t* dl =
+      mv.dst_layers
+          ? reinterpret_cast<uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(mv.dst_layers) + tr.layer))
+          : mv.dst + tr.layer * mv.dst_layer_stride;
+  tr.src = sl + kv * mv.src_kv_stride + sb * mv.src_block_stride + off;
+  tr.dst = dl + kv * mv.dst_kv_stride + db * mv.dst_block_stride + off;
   tr.len = min((int64_t)kTileBytes, (int64_t)mv.piece - off);
   return tr;
 }
@@ -741,11 +753,17 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
     any_empty |= (mv.n_blocks == 0);
     d.src = sp->base;
     d.dst = dp->base;
+    d.src_layers = sp->layers;
+    d.dst_layers = dp->layers;
+    d.src_layer_stride = sp->layer_stride;
+    d.src_kv_stride = sp->kv_stride;
+    d.src_block_stride = sp->block_stride;
+    d.dst_layer_stride = dp->layer_stride;
+    d.dst_kv_stride = dp->kv_stride;
+    d.dst_block_stride = dp->block_stride;
     d.table_row = mv.dst_table_row;
     d.done_flag = mv.done_flag;
     d.layer_flags = mv.layer_flags;
-    d.src_plane = sp->plane_bytes;
-    d.dst_plane = dp->plane_bytes;
     d.piece = (int32_t)sp->piece_bytes;
     d.tpp = (int32_t)((sp->piece_bytes + kTileBytes - 1) / kTileBytes);
     d.n_blocks = mv.n_blocks;
@@ -904,6 +922,9 @@ int kvm_pool_register(int device, void* base, const kvm_pool_desc* desc) {
   p.piece_bytes = piece;
   p.plane_bytes = piece * desc->num_blocks;
   p.token_bytes = (int64_t)desc->kv_heads * desc->head_dim * desc->elem_bytes;
+  p.layer_stride = 2 * p.plane_bytes;
+  p.kv_stride = p.plane_bytes;
+  p.block_stride = piece;
   {
     cudaPointerAttributes pa;
     if (cudaPointerGetAttributes(&pa, base) != cudaSuccess) {
@@ -918,11 +939,68 @@ int kvm_pool_register(int device, void* base, const kvm_pool_desc* desc) {
   return (int)g_pools.size() - 1;
 }
 
+int kvm_pool_register_strided(int device, const kvm_pool_desc* desc, void* const* layer_bases, int64_t kv_stride,
+                              int64_t block_stride) {
+  int64_t total = 0;
+  int rc = kvm_pool_bytes(desc, &total);
+  if (rc) return rc;
+  if (!layer_bases) return fail(KVM_ERR_INVALID, "layer_bases is NULL");
+  const int64_t piece = (int64_t)desc->block_tokens * desc->kv_heads * desc->head_dim * desc->elem_bytes;
+  if (piece % 16) return fail(KVM_ERR_CONFIG, "piece bytes must be a multiple of 16");
+  if (piece > (int64_t)1 << 30) return fail(KVM_ERR_CONFIG, "piece too large");
+  if (kv_stride <= 0 || block_stride <= 0 || kv_stride % 16 || block_stride % 16)
+    return fail(KVM_ERR_INVALID, "strides must be positive multiples of 16 bytes");
+  // the 2 x num_blocks pieces of a layer must not overlap
+  const int64_t nb = desc->num_blocks;
+  const bool kv_outer = kv_stride >= block_stride;
+  if (kv_outer ? (block_stride < piece || kv_stride < nb * block_stride)
+               : (kv_stride < piece || block_stride < 2 * kv_stride))
+    return fail(KVM_ERR_INVALID, "strides make pieces of one layer overlap");
+  for (int l = 0; l < desc->layers; ++l) {
+    if (!layer_bases[l]) return fail(KVM_ERR_INVALID, "layer base " + std::to_string(l) + " is NULL");
+    if (reinterpret_cast<uintptr_t>(layer_bases[l]) % 16)
+      return fail(KVM_ERR_INVALID, "layer bases must be 16-byte aligned");
+  }
+  int ndev = 0;
+  KVM_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(KVM_ERR_INVALID, "bad device " + std::to_string(device));
+  Pool p;
+  p.live = true;
+  p.device = device;
+  p.base = static_cast<uint8_t*>(layer_bases[0]);
+  p.desc = *desc;
+  p.piece_bytes = piece;
+  p.plane_bytes = 0;   // no single plane: not usable by decode / re-prefill / split
+  p.token_bytes = (int64_t)desc->kv_heads * desc->head_dim * desc->elem_bytes;
+  p.strided = true;
+  p.kv_stride = kv_stride;
+  p.block_stride = block_stride;
+  p.remote = false;
+  for (int l = 0; l < desc->layers; ++l) {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, layer_bases[l]) != cudaSuccess) {
+      cudaGetLastError();
+      p.remote = true;
+    } else if (pa.type != cudaMemoryTypeDevice || pa.device != device || ipc_imported(layer_bases[l])) {
+      p.remote = true;
+    }
+  }
+  {
+    DeviceGuard dg(device);
+    KVM_CUDA_TRY(cudaMalloc(&p.layers, sizeof(uint8_t*) * desc->layers));
+    KVM_CUDA_TRY(cudaMemcpy(p.layers, layer_bases, sizeof(uint8_t*) * desc->layers, cudaMemcpyHostToDevice));
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_pools.push_back(p);
+  return (int)g_pools.size() - 1;
+}
+
 int kvm_pool_unregister(int pool) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (pool < 0 || pool >= (int)g_pools.size() || !g_pools[pool].live)
     return fail(KVM_ERR_NOT_FOUND, "unknown pool id " + std::to_string(pool));
   g_pools[pool].live = false;
+  // the layer-pointer array is left allocated: a launch queued before this call may still read it
   return KVM_OK;
 }
 

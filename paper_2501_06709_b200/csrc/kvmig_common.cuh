@@ -29,6 +29,12 @@ struct Pool {
   int64_t plane_bytes = 0;  // num_blocks * piece_bytes  (one (layer, K|V) plane)
   int64_t token_bytes = 0;  // kv_heads * head_dim * elem_bytes (one token row)
   bool remote = false;      // memory lives off `device` (IPC import / peer mapping)
+  // Piece (l, kv, b) at layer_base(l) + kv * kv_stride + b * block_stride, with
+  // layer_base(l) = base + l * layer_stride for a native pool, or layers[l]
+  // (device array) for a strided pool registered by another engine.
+  bool strided = false;
+  uint8_t** layers = nullptr;  // device: desc.layers base pointers (strided pools)
+  int64_t layer_stride = 0, kv_stride = 0, block_stride = 0;
 };
 
 // Look up a registered pool; returns nullptr (and sets the error) if unknown.

@@ -1077,6 +1077,7 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
   const Pool* pool = get_pool(a->dst_pool);
   if (!pool) return KVM_ERR_NOT_FOUND;
+  if (pool->strided) return fail(KVM_ERR_UNSUPPORTED, "re-prefill needs a native pool (not a strided one)");
   const kvm_pool_desc& d = pool->desc;
   if (d.elem_bytes != 2) return fail(KVM_ERR_CONFIG, "re-prefill writes bf16 KV: pool elem_bytes must be 2");
   const int kvd = d.kv_heads * d.head_dim;
@@ -1117,6 +1118,8 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   const Pool* dst = get_pool(a->dst_pool);
   const Pool* src = dst ? get_pool(a->src_pool) : nullptr;
   if (!dst || !src) return KVM_ERR_NOT_FOUND;
+  if (src->strided || dst->strided)
+    return fail(KVM_ERR_UNSUPPORTED, "split migration needs native pools (not strided ones)");
   const kvm_pool_desc &sd = src->desc, &d = dst->desc;
   if (sd.layers != d.layers || sd.kv_heads != d.kv_heads || sd.head_dim != d.head_dim ||
       sd.block_tokens != d.block_tokens || sd.elem_bytes != d.elem_bytes)

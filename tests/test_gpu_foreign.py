@@ -1,0 +1,149 @@
+"""Strided (foreign-layout) pools: vLLM per-layer KV caches registered as they
+are and migrated to/from native pools and each other (kvm_pool_register_strided).
+
+Copy is identity, so the oracle is the piece-for-piece equality of the int16
+views: every destination piece (l, kv, dst_blocks[i]) equals the source piece
+(l, kv, src_blocks[i]), the destination table row lists dst_blocks, and no
+other destination byte changes.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2501_06709_b200 import _native
+from paper_2501_06709_b200.foreign import StridedKVPool, vllm_cache_shape
+from paper_2501_06709_b200.kvcache import BlockTable, KVPool, ModelShape
+
+pytestmark = pytest.mark.gpu
+SHAPE = ModelShape("fx", layers=3, kv_heads=4, head_dim=64, q_heads=4, d_model=256)   # 8 KiB pieces
+ENGINES = {"ldg": 0, "bulk": _native.KVM_F_ENGINE_BULK}
+
+
+def _vllm(layout, nb, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    caches = [torch.randint(-2 ** 15, 2 ** 15, vllm_cache_shape(layout, nb, 16, SHAPE.kv_heads, SHAPE.head_dim),
+                            generator=g, device="cuda", dtype=torch.int16).view(torch.float16)
+              for _ in range(SHAPE.layers)]
+    return StridedKVPool.from_vllm(caches, layout, name="fx"), caches
+
+
+def _native_pool(nb, seed):
+    p = KVPool(SHAPE, nb)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    p.tensor.view(torch.int16).copy_(torch.randint(-2 ** 15, 2 ** 15, p.view_shape, generator=g, device="cuda",
+                                                   dtype=torch.int16))
+    return p
+
+
+def _piece(pool, l, kv, b):
+    if isinstance(pool, StridedKVPool):
+        return pool.piece(l, kv, b)
+    return pool.tensor[l, kv, b]
+
+
+def _snapshot(pool):
+    nb = pool.num_blocks
+    return torch.stack([torch.stack([torch.stack([_piece(pool, l, kv, b).view(torch.int16) for b in range(nb)])
+                                     for kv in range(2)]) for l in range(SHAPE.layers)]).cpu()
+
+
+def _make(kind, nb, seed):
+    if kind == "native":
+        return _native_pool(nb, seed), None
+    return _vllm(kind, nb, seed)
+
+
+@pytest.mark.parametrize("engine", ["bulk", "ldg"])
+@pytest.mark.parametrize("src_kind,dst_kind", [("flash_attn", "native"), ("native", "flashinfer"),
+                                               ("flash_attn", "flashinfer"), ("flashinfer", "flash_attn"),
+                                               ("flash_attn", "flash_attn")])
+@pytest.mark.parametrize("n", [1, 37, 200])
+def test_migrate_between_layouts(engine, src_kind, dst_kind, n):
+    nb = 2 * n + 11
+    src, _keep_s = _make(src_kind, nb, 1)
+    dst, _keep_d = _make(dst_kind, nb, 2)
+    rng = np.random.default_rng(n)
+    sb = rng.permutation(nb)[:n].astype(np.int32)
+    dst.allocator.take(rng.permutation(nb)[:5])
+    db = dst.allocator.alloc(n).astype(np.int32)
+    before_src, before_dst = _snapshot(src), _snapshot(dst)
+    table = BlockTable(2, n + 3)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    m = _native.Move()
+    m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, n, 3
+    m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
+    m.dst_table_row, m.done_flag = table.row_ptr(1), flag.data_ptr()
+    _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine],
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    exp = before_dst.clone()
+    exp[:, :, torch.from_numpy(db).long()] = before_src[:, :, torch.from_numpy(sb).long()]
+    assert torch.equal(_snapshot(dst), exp)
+    assert torch.equal(_snapshot(src), before_src)
+    assert np.array_equal(table.rows[table.slot(1), :n].cpu().numpy(), db)
+    assert flag.item() == 3
+
+
+def test_compact_inside_a_vllm_cache_and_batch_of_moves():
+    """kvm_compact on a strided pool, and one batched launch mixing native and
+    strided pools (96+ moves, split internally)."""
+    src, _k1 = _vllm("flashinfer", 300, 5)
+    before = _snapshot(src)
+    sb = np.arange(0, 40, dtype=np.int32)
+    db = np.arange(200, 240, dtype=np.int32)
+    _native.check(_native.lib().kvm_compact(src.pool_id, sb.ctypes.data, db.ctypes.data, 40, None,
+                                            _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    exp = before.clone()
+    exp[:, :, 200:240] = before[:, :, 0:40]
+    assert torch.equal(_snapshot(src), exp)
+    natives = [_native_pool(8, 10 + i) for i in range(2)]
+    fa, _k2 = _vllm("flash_attn", 400, 7)
+    snap = [_snapshot(p) for p in natives]
+    moves, keep = [], []
+    for i in range(130):
+        p = natives[i % 2]
+        s_ = np.array([i % 8], dtype=np.int32)
+        d_ = np.array([i + 3], dtype=np.int32)
+        keep += [s_, d_]
+        m = _native.Move()
+        m.src_pool, m.dst_pool, m.n_blocks, m.done_value = p.pool_id, fa.pool_id, 1, 1
+        m.src_blocks, m.dst_blocks = s_.ctypes.data, d_.ctypes.data
+        moves.append(m)
+    arr = (_native.Move * len(moves))(*moves)
+    _native.check(_native.lib().kvm_migrate(arr, len(moves), _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    got = _snapshot(fa)
+    for i in range(130):
+        assert torch.equal(got[:, :, i + 3], snap[i % 2][:, :, i % 8])
+
+
+def test_strided_pool_rejections():
+    fa, caches = _vllm("flash_attn", 16, 3)
+    desc = SHAPE.desc(16)
+    ptrs = (ctypes.c_void_p * SHAPE.layers)(*[c.data_ptr() for c in caches])
+    piece = SHAPE.piece_bytes
+    lib = _native.lib()
+    with pytest.raises(ValueError):   # block stride smaller than a piece
+        _native.check(lib.kvm_pool_register_strided(0, ctypes.byref(desc), ptrs, 16 * piece, piece // 2))
+    with pytest.raises(ValueError):   # K|V planes overlap
+        _native.check(lib.kvm_pool_register_strided(0, ctypes.byref(desc), ptrs, 8 * piece, piece))
+    with pytest.raises(ValueError):   # misaligned stride
+        _native.check(lib.kvm_pool_register_strided(0, ctypes.byref(desc), ptrs, 16 * piece + 8, piece))
+    # decode / re-prefill need native pools
+    from paper_2501_06709_b200.attention import paged_decode
+    from paper_2501_06709_b200.reprefill import reprefill, synthetic_hidden, synthetic_weights
+
+    q = torch.zeros(SHAPE.layers, 1, SHAPE.q_heads, 64, dtype=torch.float16, device="cuda")
+    with pytest.raises(Exception, match="native pool"):
+        paged_decode(fa, q, torch.zeros(1, 1, dtype=torch.int32, device="cuda"),
+                     torch.ones(1, dtype=torch.int32, device="cuda"))
+    bf, _k = _vllm("flash_attn", 16, 4)
+    bf.dtype = torch.bfloat16
+    with pytest.raises(Exception, match="native pool"):
+        reprefill(bf, synthetic_hidden(SHAPE, 16, 0), synthetic_weights(SHAPE, 0, with_q=False),
+                  torch.zeros(1, dtype=torch.int32, device="cuda"))
