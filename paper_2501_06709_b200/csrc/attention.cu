@@ -50,10 +50,19 @@ struct Params {
   const int32_t* seq_lens;
   float* ws_ml;   // [lb][q_heads][splits][2]  (m in log2 units, l)
   float* ws_acc;  // [lb][q_heads][splits][D]
-  int64_t plane_bytes, piece_bytes, tok_stride;  // tok_stride = kv_heads * D * 2
+  // piece (l, kv, b) at layer_base(l) + kv * kv_stride + b * block_stride; layer_base(l) =
+  // layers[l] for a strided (foreign-layout) pool, else pool + l * layer_stride
+  const uint8_t* const* layers;
+  int64_t layer_stride, kv_stride, block_stride, tok_stride;  // tok_stride = kv_heads * D * 2
   int32_t layer0, n_layers, batch, q_heads, kv_heads, max_blocks, splits, num_blocks, bps;
   float scale_log2;  // scale * log2(e)
 };
+
+__device__ __forceinline__ const uint8_t* layer_base(const Params& p, int layer) {
+  if (p.layers)
+    return reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(p.layers) + layer));
+  return p.pool + (int64_t)layer * p.layer_stride;
+}
 
 template <typename T>
 __device__ __forceinline__ void unpack8(const int4& v, float* f) {
@@ -93,14 +102,14 @@ __global__ void __launch_bounds__(WARPS * 32) decode_split_kernel(const __grid_c
     for (int d = 0; d < 8; ++d) acc[g][d] = 0.f;
   }
   const int32_t* table = p.tables + (int64_t)b * p.max_blocks;
-  const uint8_t* kplane = p.pool + ((int64_t)layer * 2 + 0) * p.plane_bytes + (int64_t)h * D * 2 + c * 16;
-  const uint8_t* vplane = kplane + p.plane_bytes;
+  const uint8_t* kplane = layer_base(p, layer) + (int64_t)h * D * 2 + c * 16;
+  const uint8_t* vplane = kplane + p.kv_stride;
 
   for (int blk = blk_lo + warp; blk < blk_hi; blk += WARPS) {
     const int64_t pb = __ldg(table + blk);
     const int ntok = min(16, seq - blk * 16);
-    const uint8_t* kb = kplane + pb * p.piece_bytes;
-    const uint8_t* vb = vplane + pb * p.piece_bytes;
+    const uint8_t* kb = kplane + pb * p.block_stride;
+    const uint8_t* vb = vplane + pb * p.block_stride;
     int4 kv[8], vv[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -291,16 +300,16 @@ __global__ void __launch_bounds__(WARPS * 32) decode_gqa_kernel(const __grid_con
   for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
 
   const int32_t* table = p.tables + (int64_t)b * p.max_blocks;
-  const uint8_t* kplane = p.pool + ((int64_t)layer * 2 + 0) * p.plane_bytes + (int64_t)h * D * 2;
-  const uint8_t* vplane = kplane + p.plane_bytes;
+  const uint8_t* kplane = layer_base(p, layer) + (int64_t)h * D * 2;
+  const uint8_t* vplane = kplane + p.kv_stride;
 
   // stage block `blk` (K and V rows of kv head h) into buffer `buf`: 16 B per lane per step,
   // consecutive lanes on consecutive chunks of a row (two 256 B rows per warp instruction)
   auto stage = [&](int blk, int buf) {
     const int64_t pb = __ldg(table + blk);
     const int ntok = min(16, seq - blk * 16);
-    const uint8_t* kb = kplane + pb * p.piece_bytes;
-    const uint8_t* vb = vplane + pb * p.piece_bytes;
+    const uint8_t* kb = kplane + pb * p.block_stride;
+    const uint8_t* vb = vplane + pb * p.block_stride;
     const uint32_t ks = wbase + buf * 2 * GQA_TILE, vs = ks + GQA_TILE;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -539,7 +548,6 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
   if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
   const Pool* pool = get_pool(a->pool);
   if (!pool) return KVM_ERR_NOT_FOUND;
-  if (pool->strided) return fail(KVM_ERR_UNSUPPORTED, "paged decode needs a native pool (not a strided one)");
   const kvm_pool_desc& d = pool->desc;
   if (d.head_dim != D) return fail(KVM_ERR_UNSUPPORTED, "kvm_paged_decode supports head_dim 128");
   if (d.elem_bytes != 2 || d.block_tokens != 16) return fail(KVM_ERR_UNSUPPORTED, "needs 16-bit KV, 16-token blocks");
@@ -556,8 +564,10 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
   p.out = a->out;
   p.tables = a->block_tables;
   p.seq_lens = a->seq_lens;
-  p.plane_bytes = pool->plane_bytes;
-  p.piece_bytes = pool->piece_bytes;
+  p.layers = pool->layers;
+  p.layer_stride = pool->layer_stride;
+  p.kv_stride = pool->kv_stride;
+  p.block_stride = pool->block_stride;
   p.tok_stride = (int64_t)d.kv_heads * D * 2;
   p.layer0 = a->layer0;
   p.n_layers = a->n_layers;

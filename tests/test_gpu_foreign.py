@@ -134,16 +134,44 @@ def test_strided_pool_rejections():
         _native.check(lib.kvm_pool_register_strided(0, ctypes.byref(desc), ptrs, 8 * piece, piece))
     with pytest.raises(ValueError):   # misaligned stride
         _native.check(lib.kvm_pool_register_strided(0, ctypes.byref(desc), ptrs, 16 * piece + 8, piece))
-    # decode / re-prefill need native pools
-    from paper_2501_06709_b200.attention import paged_decode
+    # re-prefill and split need native pools
     from paper_2501_06709_b200.reprefill import reprefill, synthetic_hidden, synthetic_weights
 
-    q = torch.zeros(SHAPE.layers, 1, SHAPE.q_heads, 64, dtype=torch.float16, device="cuda")
-    with pytest.raises(Exception, match="native pool"):
-        paged_decode(fa, q, torch.zeros(1, 1, dtype=torch.int32, device="cuda"),
-                     torch.ones(1, dtype=torch.int32, device="cuda"))
     bf, _k = _vllm("flash_attn", 16, 4)
     bf.dtype = torch.bfloat16
     with pytest.raises(Exception, match="native pool"):
         reprefill(bf, synthetic_hidden(SHAPE, 16, 0), synthetic_weights(SHAPE, 0, with_q=False),
                   torch.zeros(1, dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("layout", ["flash_attn", "flashinfer"])
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_decode_over_vllm_cache_equals_native(layout, dtype):
+    """kvm_paged_decode reads a strided pool through its per-layer pointers:
+    a request migrated out of a vLLM cache into a native pool decodes
+    bit-identically from either copy (GQA tensor-core path and CUDA cores)."""
+    from paper_2501_06709_b200.attention import paged_decode
+
+    shape = ModelShape("dv", layers=2, kv_heads=2, head_dim=128, q_heads=8, d_model=1024)
+    nb, n_tok = 96, 1000
+    g = torch.Generator(device="cuda").manual_seed(3)
+    caches = [torch.randn(vllm_cache_shape(layout, nb, 16, 2, 128), generator=g, device="cuda").to(dtype)
+              for _ in range(shape.layers)]
+    src = StridedKVPool.from_vllm(caches, layout, name="dv", q_heads=8)
+    dst = KVPool(shape, nb, dtype=dtype)
+    k = (n_tok + 15) // 16
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(4))[:k].to(torch.int32)
+    db = torch.randperm(nb, generator=torch.Generator().manual_seed(5))[:k].to(torch.int32)
+    m = _native.Move()
+    m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, k, 1
+    sbn, dbn = sb.numpy(), db.numpy()
+    m.src_blocks, m.dst_blocks = sbn.ctypes.data, dbn.ctypes.data
+    _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    q = torch.randn(shape.layers, 1, 8, 128, generator=g, device="cuda").to(dtype)
+    lens = torch.tensor([n_tok], dtype=torch.int32, device="cuda")
+    for cc in (False, True):
+        a = paged_decode(src, q, sb[None].contiguous().cuda(), lens, cuda_cores=cc)
+        b = paged_decode(dst, q, db[None].contiguous().cuda(), lens, cuda_cores=cc)
+        torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
