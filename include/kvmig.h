@@ -269,10 +269,9 @@ int kvm_pool_register(int device, void* base, const kvm_pool_desc* desc);
  * (kv_stride = blocks * piece, block_stride = piece), FlashInfer backend
  * [blocks][2][16][H][D] (kv_stride = piece, block_stride = 2 * piece).
  * kvm_migrate / kvm_compact accept any mix of native and strided pools with
- * the same piece size (pieces are copied as opaque bytes); kvm_paged_decode
- * reads strided pools too (pieces ordered [block_tokens][kv_heads][head_dim],
- * as in both vLLM layouts); re-prefill and split need native pools
- * (KVM_ERR_UNSUPPORTED otherwise). */
+ * the same piece size (pieces are copied as opaque bytes); kvm_paged_decode,
+ * kvm_reprefill and kvm_split_migrate address them the same way (pieces
+ * ordered [block_tokens][kv_heads][head_dim], as in both vLLM layouts). */
 int kvm_pool_register_strided(int device, const kvm_pool_desc* desc, void* const* layer_bases, int64_t kv_stride,
                               int64_t block_stride);
 int kvm_pool_unregister(int pool);

@@ -37,6 +37,23 @@ struct Pool {
   int64_t layer_stride = 0, kv_stride = 0, block_stride = 0;
 };
 
+// Device-side view of a pool's piece addressing (native or strided).
+struct PoolAddr {
+  uint8_t* base;                 // native: pool base
+  const uint8_t* const* layers;  // strided: per-layer bases (device array), else NULL
+  int64_t layer_stride, kv_stride, block_stride;
+};
+inline PoolAddr pool_addr(const Pool& p) {
+  return PoolAddr{p.base, p.layers, p.layer_stride, p.kv_stride, p.block_stride};
+}
+// First byte of piece (layer l, K|V kv, block blk).
+__device__ __forceinline__ uint8_t* piece_ptr(const PoolAddr& a, int l, int kv, int64_t blk) {
+  const uint8_t* lb =
+      a.layers ? reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(a.layers) + l))
+               : a.base + (int64_t)l * a.layer_stride;
+  return const_cast<uint8_t*>(lb) + kv * a.kv_stride + blk * a.block_stride;
+}
+
 // Look up a registered pool; returns nullptr (and sets the error) if unknown.
 const Pool* get_pool(int id);
 void count_launch(int64_t n = 1);

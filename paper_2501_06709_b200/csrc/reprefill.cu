@@ -53,7 +53,7 @@ constexpr uint32_t TMEM_COLS = 512;
 struct Params {
   CUtensorMap tmap_x;  // [rows][d_model] bf16, box {64, 128}
   CUtensorMap tmap_w;  // [layers][n_out][d_model] bf16, box {64, 256, 1} (pair kernel: {64, 128, 1})
-  uint8_t* pool;
+  PoolAddr pool;        // destination pool (native or strided)
   __nv_bfloat16* q_out;
   const int32_t* dst_blocks;
   uint32_t* done_flag;
@@ -61,16 +61,14 @@ struct Params {
   uint32_t* tile_ctr;   // pair kernel: dynamic tile counter (self-resetting)
   const float2* rope;   // KVM_REPREFILL_ROPE: (cos, sin) per [token t][i < 64] of the suffix, else NULL
   int32_t x_per_layer;  // KVM_REPREFILL_X_PER_LAYER: tmap_x is 3D [layers][rows][d_model]
-  int64_t plane_bytes;  // num_blocks * piece_bytes
   int64_t piece_bytes;
   int32_t rows, n_out, d_model, layers, q_cols, kvd, tok0, block_tokens, n_dst_blocks;
   int32_t m_tiles, n_tiles, k_blocks, total_tiles;  // pair kernel: m = 256-feature tiles, n = 256-token tiles
   uint32_t done_value;
   // fused split migration (kvm_split_migrate): the transferred prefix, streamed by
   // warps 2-3 while the tensor cores re-prefill the suffix
-  const uint8_t* csrc;          // source pool base (local or peer-mapped)
+  PoolAddr csrc;                // source pool (local or peer-mapped, native or strided)
   const int32_t* csrc_blocks;   // source blocks of the prefix
-  int64_t c_src_plane;          // source pool bytes per (layer, K|V) plane
   int64_t c_units;              // 8 KiB copy units: planes * prefix_blocks * units_per_piece
   int32_t c_nblocks, c_upp;     // prefix blocks, units per piece
   int32_t* table_row;           // if set: the last CTA writes table_row[i] = dst_blocks[i], i < table_n
@@ -190,10 +188,9 @@ __device__ __forceinline__ bool copy_one_unit(const Params& p, int* next, int la
   const int32_t bi = r / p.c_upp, ui = r - bi * p.c_upp;
   const int64_t off = (int64_t)ui * CUNIT;
   const int nv = (int)(min((int64_t)CUNIT, p.piece_bytes - off) >> 4);
-  const int4* src = reinterpret_cast<const int4*>(p.csrc + plane * p.c_src_plane +
-                                                  (int64_t)__ldg(p.csrc_blocks + bi) * p.piece_bytes + off);
-  int4* dst = reinterpret_cast<int4*>(p.pool + plane * p.plane_bytes +
-                                      (int64_t)__ldg(p.dst_blocks + bi) * p.piece_bytes + off);
+  const int4* src =
+      reinterpret_cast<const int4*>(piece_ptr(p.csrc, plane >> 1, plane & 1, __ldg(p.csrc_blocks + bi)) + off);
+  int4* dst = reinterpret_cast<int4*>(piece_ptr(p.pool, plane >> 1, plane & 1, __ldg(p.dst_blocks + bi)) + off);
   int4 v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -348,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1) reprefill_kernel(const __grid_cons
         const int blk = __ldg(p.dst_blocks + tok / p.block_tokens);
         const int64_t slot_off = (int64_t)(tok % p.block_tokens) * row_bytes;
         for (int kv = 0; kv < 2; ++kv)
-          kv_row[kv] = p.pool + ((int64_t)l * 2 + kv) * p.plane_bytes + (int64_t)blk * p.piece_bytes + slot_off;
+          kv_row[kv] = piece_ptr(p.pool, l, kv, blk) + slot_off;
       }
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
       // bf16 store of 32 consecutive output columns of this thread's token row
@@ -794,8 +791,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
             } else {
               const int tok = p.tok0 + tok_i;
               const int blk = __ldg(p.dst_blocks + tok / p.block_tokens);
-              dst = p.pool + ((int64_t)l * 2 + (kind - 1)) * p.plane_bytes + (int64_t)blk * p.piece_bytes +
-                    (int64_t)(tok % p.block_tokens) * p.kvd * 2 + (int64_t)fcol * 2;
+              dst = piece_ptr(p.pool, l, kind - 1, blk) + (int64_t)(tok % p.block_tokens) * p.kvd * 2 +
+                    (int64_t)fcol * 2;
             }
             *reinterpret_cast<uint4*>(dst + (lane & 3) * 16) = v;
           }
@@ -945,10 +942,9 @@ static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(KVM_ERR_CUDA, "cuTensorMapEncodeTiled(w) failed: " + std::to_string((int)r));
   }
-  p.pool = pool->base;
+  p.pool = pool_addr(*pool);
   p.q_out = static_cast<__nv_bfloat16*>(q_out);
   p.dst_blocks = dst_blocks;
-  p.plane_bytes = pool->plane_bytes;
   p.piece_bytes = pool->piece_bytes;
   p.rows = rows;
   p.n_out = n_out;
@@ -1077,7 +1073,6 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
   const Pool* pool = get_pool(a->dst_pool);
   if (!pool) return KVM_ERR_NOT_FOUND;
-  if (pool->strided) return fail(KVM_ERR_UNSUPPORTED, "re-prefill needs a native pool (not a strided one)");
   const kvm_pool_desc& d = pool->desc;
   if (d.elem_bytes != 2) return fail(KVM_ERR_CONFIG, "re-prefill writes bf16 KV: pool elem_bytes must be 2");
   const int kvd = d.kv_heads * d.head_dim;
@@ -1118,8 +1113,6 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   const Pool* dst = get_pool(a->dst_pool);
   const Pool* src = dst ? get_pool(a->src_pool) : nullptr;
   if (!dst || !src) return KVM_ERR_NOT_FOUND;
-  if (src->strided || dst->strided)
-    return fail(KVM_ERR_UNSUPPORTED, "split migration needs native pools (not strided ones)");
   const kvm_pool_desc &sd = src->desc, &d = dst->desc;
   if (sd.layers != d.layers || sd.kv_heads != d.kv_heads || sd.head_dim != d.head_dim ||
       sd.block_tokens != d.block_tokens || sd.elem_bytes != d.elem_bytes)
@@ -1156,9 +1149,8 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   p.done_value = a->done_value;
   p.table_row = a->dst_table_row;
   p.table_n = a->dst_table_row ? n_blocks : 0;
-  p.csrc = src->base;
+  p.csrc = pool_addr(*src);
   p.csrc_blocks = a->src_blocks;
-  p.c_src_plane = src->plane_bytes;
   p.c_nblocks = a->prefix_blocks;
   p.c_upp = (int32_t)((dst->piece_bytes + CUNIT - 1) / CUNIT);
   p.c_units = (int64_t)2 * d.layers * a->prefix_blocks * p.c_upp;

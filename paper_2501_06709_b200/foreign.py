@@ -7,9 +7,9 @@ block stride), so a request can be migrated straight out of, or into, a vLLM
 instance's cache — or between a vLLM cache and a native `KVPool` — without a
 staging copy.  Pieces (16 tokens x kv_heads x head_dim of one layer, K or V) are
 copied as opaque bytes, so any two layouts whose piece bytes are ordered the
-same way interoperate; `attention.paged_decode` reads a strided pool in place
-(pieces ordered [16][H][D], as in both vLLM layouts); re-prefill and split
-moves need native pools.
+same way interoperate; paged decode, re-prefill and fused split moves
+address a strided pool in place too (pieces ordered [16][H][D], as in both
+vLLM layouts).
 
 Layouts (vLLM 0.22, `get_kv_cache_shape(num_blocks, block_size, kv_heads, head_size)`):
   "flash_attn"  [2][num_blocks][16][H][D] per layer  (FlashAttentionBackend)

@@ -134,14 +134,6 @@ def test_strided_pool_rejections():
         _native.check(lib.kvm_pool_register_strided(0, ctypes.byref(desc), ptrs, 8 * piece, piece))
     with pytest.raises(ValueError):   # misaligned stride
         _native.check(lib.kvm_pool_register_strided(0, ctypes.byref(desc), ptrs, 16 * piece + 8, piece))
-    # re-prefill and split need native pools
-    from paper_2501_06709_b200.reprefill import reprefill, synthetic_hidden, synthetic_weights
-
-    bf, _k = _vllm("flash_attn", 16, 4)
-    bf.dtype = torch.bfloat16
-    with pytest.raises(Exception, match="native pool"):
-        reprefill(bf, synthetic_hidden(SHAPE, 16, 0), synthetic_weights(SHAPE, 0, with_q=False),
-                  torch.zeros(1, dtype=torch.int32, device="cuda"))
 
 
 @pytest.mark.parametrize("layout", ["flash_attn", "flashinfer"])
@@ -175,3 +167,91 @@ def test_decode_over_vllm_cache_equals_native(layout, dtype):
         b = paged_decode(dst, q, db[None].contiguous().cuda(), lens, cuda_cores=cc)
         torch.cuda.synchronize()
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+def _bf16_pair(layout, nb, shape, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    caches = [torch.randint(-2 ** 15, 2 ** 15, vllm_cache_shape(layout, nb, 16, shape.kv_heads, shape.head_dim),
+                            generator=g, device="cuda", dtype=torch.int16).view(torch.bfloat16)
+              for _ in range(shape.layers)]
+    return StridedKVPool.from_vllm(caches, layout, name=shape.name, q_heads=shape.q_heads), caches
+
+
+@pytest.mark.parametrize("single_cta", [False, True])
+@pytest.mark.parametrize("layout", ["flash_attn", "flashinfer"])
+def test_reprefill_into_vllm_cache_equals_native(layout, single_cta):
+    """Re-prefill writes a strided pool's pieces in place: every recomputed
+    token slot equals the same re-prefill into a native pool, bit for bit
+    (RoPE on), and nothing else in the vLLM cache changes."""
+    from paper_2501_06709_b200.reprefill import reprefill, synthetic_hidden, synthetic_weights
+
+    shape = ModelShape("rv", layers=2, kv_heads=2, head_dim=128, q_heads=4, d_model=256)
+    nb, rows, tok0 = 40, 300, 21
+    fx, _caches = _bf16_pair(layout, nb, shape, 8)
+    nat = KVPool(shape, nb, dtype=torch.bfloat16)
+    blocks = torch.randperm(nb, generator=torch.Generator().manual_seed(9))[:(tok0 + rows + 15) // 16]
+    blocks = blocks.to(torch.int32).cuda()
+    x = synthetic_hidden(shape, rows, 0, seed=10)
+    w = synthetic_weights(shape, 0, with_q=True, seed=11)
+    before = [[[fx.piece(l, kv, b).clone() for b in range(nb)] for kv in range(2)] for l in range(2)]
+    reprefill(fx, x, w, blocks, tok0=tok0, single_cta=single_cta, rope_theta=10000.0)
+    reprefill(nat, x, w, blocks, tok0=tok0, single_cta=single_cta, rope_theta=10000.0)
+    torch.cuda.synchronize()
+    written = set()
+    for t in range(tok0, tok0 + rows):
+        written.add((int(blocks[t // 16]), t % 16))
+    for l in range(2):
+        for kv in range(2):
+            for b in range(nb):
+                got = fx.piece(l, kv, b).view(torch.int16)
+                for slot in range(16):
+                    if (b, slot) in written:
+                        assert torch.equal(got[slot], nat.tensor[l, kv, b, slot].view(torch.int16))
+                    else:
+                        assert torch.equal(got[slot], before[l][kv][b][slot].view(torch.int16))
+
+
+@pytest.mark.parametrize("src_kind,dst_kind", [("flash_attn", "native"), ("native", "flashinfer"),
+                                               ("flashinfer", "flash_attn")])
+def test_fused_split_between_layouts(src_kind, dst_kind):
+    """kvm_split_migrate with strided pools on either side: the prefix arrives
+    bit-exact, the recomputed suffix equals the same split into native pools."""
+    from paper_2501_06709_b200.reprefill import synthetic_hidden, synthetic_weights
+    from paper_2501_06709_b200.split import make_split, split_migrate_fused
+
+    shape = ModelShape("sv", layers=2, kv_heads=2, head_dim=128, q_heads=4, d_model=256)
+    tokens, suffix = 700, 188
+    plan = make_split(tokens, suffix)
+    nb = plan.total_blocks + 6
+
+    def mk(kind, seed):
+        if kind == "native":
+            p = KVPool(shape, nb, dtype=torch.bfloat16)
+            p.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1,
+                                              generator=torch.Generator(device="cuda").manual_seed(seed))
+            return p
+        return _bf16_pair(kind, nb, shape, seed)[0]
+
+    def piece(pool, l, kv, b):
+        return pool.piece(l, kv, b) if isinstance(pool, StridedKVPool) else pool.tensor[l, kv, b]
+
+    src, dst = mk(src_kind, 1), mk(dst_kind, 2)
+    nsrc, ndst = KVPool(shape, nb, dtype=torch.bfloat16), KVPool(shape, nb, dtype=torch.bfloat16)
+    for l in range(2):
+        for kv in range(2):
+            for b in range(nb):
+                nsrc.tensor[l, kv, b] = piece(src, l, kv, b)
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(3))[:plan.total_blocks].to(torch.int32).cuda()
+    db = torch.randperm(nb, generator=torch.Generator().manual_seed(4))[:plan.total_blocks].to(torch.int32).cuda()
+    x = synthetic_hidden(shape, suffix, 0, seed=5)
+    w = synthetic_weights(shape, 0, with_q=True, seed=6)
+    split_migrate_fused(src, dst, sb, db, plan, x, w, rope_theta=10000.0)
+    split_migrate_fused(nsrc, ndst, sb, db, plan, x, w, rope_theta=10000.0)
+    torch.cuda.synchronize()
+    for l in range(2):
+        for kv in range(2):
+            for i in range(plan.total_blocks):
+                b = int(db[i])
+                got, exp = piece(dst, l, kv, b).view(torch.int16), ndst.tensor[l, kv, b].view(torch.int16)
+                n_valid = min(16, tokens - 16 * i)
+                assert torch.equal(got[:n_valid], exp[:n_valid])
