@@ -255,3 +255,43 @@ def test_fused_split_between_layouts(src_kind, dst_kind):
                 got, exp = piece(dst, l, kv, b).view(torch.int16), ndst.tensor[l, kv, b].view(torch.int16)
                 n_valid = min(16, tokens - 16 * i)
                 assert torch.equal(got[:n_valid], exp[:n_valid])
+
+
+def test_executor_and_live_migration_on_vllm_caches():
+    """The executor and live migration take strided pools like native ones:
+    a plan moves requests from a FlashAttention-layout cache (logical GPU 0)
+    to a FlashInfer-layout cache (logical GPU 1), then live migration brings
+    one back, with the block tables rewritten by the kernels."""
+    from paper_2501_06709_b200.executor import MigrationExecutor
+    from paper_2501_06709_b200.live import LiveMigration
+    from paper_2501_06709_b200.planner import KV_TRANSFER, PendingMove, PlannedMove
+
+    p0, _c0 = _vllm("flash_attn", 64, 1)
+    p1, _c1 = _vllm("flashinfer", 64, 2)
+    tables = {0: BlockTable(4, 16), 1: BlockTable(4, 16)}
+    ex = MigrationExecutor({0: p0, 1: p1}, tables)
+    ex.admit(1, 0, 70)
+    ex.admit(2, 0, 40)
+    src = {r: [[[p0.piece(l, kv, int(b)).clone() for b in ex.where(r).blocks] for kv in range(2)]
+               for l in range(SHAPE.layers)] for r in (1, 2)}
+    bpt = SHAPE.kv_bytes_per_token
+    ex.execute([PlannedMove(PendingMove(1, 0, 1, 70 * bpt, 70), KV_TRANSFER),
+                PlannedMove(PendingMove(2, 0, 1, 40 * bpt, 40), KV_TRANSFER)])
+    for r in (1, 2):
+        res = ex.where(r)
+        assert res.gpu == 1
+        assert np.array_equal(tables[1].rows[tables[1].slot(r), :len(res.blocks)].cpu().numpy(), res.blocks)
+        for l in range(SHAPE.layers):
+            for kv in range(2):
+                for i, b in enumerate(res.blocks):
+                    assert torch.equal(p1.piece(l, kv, int(b)).view(torch.int16), src[r][l][kv][i].view(torch.int16))
+    lm = LiveMigration(ex, 1, 0)
+    lm.precopy()
+    lm.drain()
+    lm.finish()
+    res = ex.where(1)
+    assert res.gpu == 0
+    for l in range(SHAPE.layers):
+        for kv in range(2):
+            for i, b in enumerate(res.blocks):
+                assert torch.equal(p0.piece(l, kv, int(b)).view(torch.int16), src[1][l][kv][i].view(torch.int16))
