@@ -73,3 +73,26 @@ def allreduce_max(value: float, device=None) -> float:
                      device=device if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def collective_ring_exchange(pool, send_blocks, recv_blocks, ri: RankInfo, group=None):
+    """COMPARISON BASELINE ONLY, not the product path: the same
+    ring exchange as bench.py's kvm_migrate push, done the library way —
+    gather this rank's request into a contiguous buffer (`index_select` over the
+    block axis of a native pool tensor [L][2][blocks][16][H][D]), one
+    `batch_isend_irecv` (ncclSend / ncclRecv inside a group with the nccl
+    backend) to ri.send_to / from ri.recv_from, then scatter the received
+    request into `recv_blocks`.  send_blocks / recv_blocks: int64 tensors on
+    the pool's device.  Returns the received buffer."""
+    import torch
+    import torch.distributed as dist
+
+    out = pool.index_select(2, send_blocks)
+    inc = torch.empty((pool.shape[0], pool.shape[1], recv_blocks.numel()) + tuple(pool.shape[3:]),
+                      dtype=pool.dtype, device=pool.device)
+    ops = [dist.P2POp(dist.isend, out, ri.send_to, group=group),
+           dist.P2POp(dist.irecv, inc, ri.recv_from, group=group)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    pool.index_copy_(2, recv_blocks, inc)
+    return inc

@@ -72,3 +72,52 @@ def test_two_rank_control_plane_gloo():
         assert handles_ok is True, blocks_ok
         assert blocks_ok is True
         assert mx == 2.5  # max over ranks
+
+
+def _ring_worker(rank, world, port, q):
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2501_06709_b200.dist import RankInfo, collective_ring_exchange
+
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        ri = RankInfo(rank, world, rank)
+        g = torch.Generator().manual_seed(rank)
+        pool = torch.randint(-2 ** 15, 2 ** 15, (2, 2, 12, 16, 2, 8), generator=g, dtype=torch.int16)
+        before = pool.clone()
+        send = torch.tensor([1, 7, 3], dtype=torch.int64)
+        recv = torch.tensor([10, 0, 5], dtype=torch.int64)
+        collective_ring_exchange(pool, send, recv, ri)
+        peer = torch.randint(-2 ** 15, 2 ** 15, (2, 2, 12, 16, 2, 8), generator=torch.Generator().manual_seed(
+            ri.recv_from), dtype=torch.int16)
+        ok = torch.equal(pool[:, :, recv], peer[:, :, send])
+        untouched = [b for b in range(12) if b not in (10, 0, 5)]
+        ok = ok and torch.equal(pool[:, :, untouched], before[:, :, untouched])
+        q.put((rank, bool(ok), ""))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+
+
+def test_collective_ring_baseline_gloo():
+    """The NCCL-style comparison baseline (gather -> batch_isend_irecv ->
+    scatter) moves each rank's request to its ring successor exactly."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    world = 3
+    procs = [ctx.Process(target=_ring_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=30)
+    for rank, ok, err in res:
+        assert ok, err
