@@ -45,24 +45,31 @@ class StridedKVPool:
     while the pool is registered.
     """
 
-    def __init__(self, shape: ModelShape, num_blocks: int, layer_tensors: Sequence, kv_stride: int,
-                 block_stride: int, *, allocator: bool = True, layout: str = "strided"):
-        if len(layer_tensors) != shape.layers:
-            raise ConfigError(f"need {shape.layers} layer tensors, got {len(layer_tensors)}")
-        t0 = layer_tensors[0]
-        if any(t.device != t0.device or t.dtype != t0.dtype for t in layer_tensors):
-            raise ConfigError("layer tensors must share device and dtype")
-        if t0.element_size() != shape.elem_bytes:
-            raise ConfigError("layer tensor dtype size does not match shape.elem_bytes")
+    def __init__(self, shape: ModelShape, num_blocks: int, layer_tensors: Optional[Sequence], kv_stride: int,
+                 block_stride: int, *, allocator: bool = True, layout: str = "strided",
+                 _layer_ptrs: Optional[Sequence[int]] = None, _device: int = 0, _dtype=None):
+        self._mapped = []
+        if layer_tensors is not None:
+            if len(layer_tensors) != shape.layers:
+                raise ConfigError(f"need {shape.layers} layer tensors, got {len(layer_tensors)}")
+            t0 = layer_tensors[0]
+            if any(t.device != t0.device or t.dtype != t0.dtype for t in layer_tensors):
+                raise ConfigError("layer tensors must share device and dtype")
+            if t0.element_size() != shape.elem_bytes:
+                raise ConfigError("layer tensor dtype size does not match shape.elem_bytes")
+            self.device, self.dtype = t0.device.index, t0.dtype
+            self.layers = list(layer_tensors)
+            self.layer_ptrs = [t.data_ptr() for t in layer_tensors]
+        else:   # peer-mapped (from_ipc): raw pointers, no tensors
+            self.device, self.dtype = _device, _dtype
+            self.layers = None
+            self.layer_ptrs = list(_layer_ptrs)
         self.shape = shape
         self.num_blocks = num_blocks
-        self.device = t0.device.index
-        self.dtype = t0.dtype
         self.layout = layout
-        self.layers = list(layer_tensors)
         self.kv_stride, self.block_stride = kv_stride, block_stride
         self._desc = shape.desc(num_blocks)
-        ptrs = (ctypes.c_void_p * shape.layers)(*[t.data_ptr() for t in layer_tensors])
+        ptrs = (ctypes.c_void_p * shape.layers)(*self.layer_ptrs)
         self.pool_id = _native.check(
             _native.lib().kvm_pool_register_strided(self.device, ctypes.byref(self._desc), ptrs,
                                                     ctypes.c_int64(kv_stride), ctypes.c_int64(block_stride)),
@@ -92,8 +99,42 @@ class StridedKVPool:
         kv_stride, block_stride = (nb * piece, piece) if layout == "flash_attn" else (piece, 2 * piece)
         return cls(shape, nb, kv_caches, kv_stride, block_stride, allocator=allocator, layout=layout)
 
+    # -- cross-process (one process per GPU, e.g. one vLLM instance per GPU) ----
+    def ipc_handles(self) -> list:
+        """(64-byte handle, offset) per layer, for from_ipc() in a peer process."""
+        out = []
+        for ptr in self.layer_ptrs:
+            h = (ctypes.c_ubyte * 64)()
+            off = ctypes.c_int64()
+            _native.check(_native.lib().kvm_ipc_export(ctypes.c_void_p(ptr), h, ctypes.byref(off)),
+                          "kvm_ipc_export")
+            out.append((bytes(h), off.value))
+        return out
+
+    @classmethod
+    def from_ipc(cls, shape: ModelShape, num_blocks: int, local_device: int, handles: Sequence, kv_stride: int,
+                 block_stride: int, dtype=None, layout: str = "strided") -> "StridedKVPool":
+        """Map a peer process's strided cache (handles from ipc_handles()); each
+        distinct allocation is mapped once (vLLM carves every layer out of one)."""
+        import torch
+
+        bases = {}
+        for h, _ in handles:
+            if h not in bases:
+                ptr = ctypes.c_void_p()
+                _native.check(_native.lib().kvm_ipc_import(local_device, (ctypes.c_ubyte * 64).from_buffer_copy(h),
+                                                           0, ctypes.byref(ptr)), "kvm_ipc_import")
+                bases[h] = ptr.value
+        pool = cls(shape, num_blocks, None, kv_stride, block_stride, allocator=False, layout=layout,
+                   _layer_ptrs=[bases[h] + off for h, off in handles], _device=local_device,
+                   _dtype=dtype or torch.float16)
+        pool._mapped = list(bases.values())
+        return pool
+
     def piece(self, layer: int, kv: int, block: int):
         """View of one piece, [block_tokens][kv_heads][head_dim] (for tests and tools)."""
+        if self.layers is None:
+            raise ValueError("a peer-mapped pool has no local tensors")
         t = self.layers[layer]
         off = (kv * self.kv_stride + block * self.block_stride) // t.element_size()
         s = self.shape
@@ -104,6 +145,9 @@ class StridedKVPool:
         if getattr(self, "pool_id", None) is not None and self.pool_id >= 0:
             _native.lib().kvm_pool_unregister(self.pool_id)
             self.pool_id = -1
+        for ptr in getattr(self, "_mapped", []):
+            _native.lib().kvm_ipc_close(ctypes.c_void_p(ptr), 0)
+        self._mapped = []
 
     def __del__(self):
         try:

@@ -187,3 +187,85 @@ def test_two_process_split_pull():
         p.join(timeout=60)
     for rank, ok, err in res:
         assert ok, f"rank {rank} failed:\n{err}"
+
+
+def _vllm_worker(rank, world, port, result_q):
+    """Rank 1 plays a vLLM instance: its FlashAttention-layout per-layer caches
+    are views into ONE allocation (as vLLM carves them).  Rank 0 maps them with
+    StridedKVPool.from_ipc (one mapping for all layers) and pushes a request
+    from its native pool straight into the peer's vLLM cache."""
+    import ctypes
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2501_06709_b200 import _native
+    from paper_2501_06709_b200.dist import exchange_objects
+    from paper_2501_06709_b200.foreign import StridedKVPool, vllm_cache_shape
+    from paper_2501_06709_b200.kvcache import KVPool, ModelShape
+
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        shape = ModelShape("vipc", layers=3, kv_heads=4, head_dim=64, q_heads=4, d_model=256)
+        nb, n = 30, 7
+        g = torch.Generator(device="cuda:0").manual_seed(7)
+        if rank == 0:
+            pool = KVPool(shape, nb)
+            pool.tensor.view(torch.int16).copy_(torch.randint(-2 ** 15, 2 ** 15, pool.view_shape, generator=g,
+                                                              device="cuda:0", dtype=torch.int16))
+            torch.cuda.synchronize()
+            info = exchange_objects(None)
+            handles, kv_stride, block_stride, dst_blocks = info[1]
+            peer = StridedKVPool.from_ipc(shape, nb, 0, handles, kv_stride, block_stride, dtype=torch.float16,
+                                          layout="flash_attn")
+            assert len(peer._mapped) == 1
+            sb = np.arange(3, 3 + n, dtype=np.int32)
+            db = np.asarray(dst_blocks, dtype=np.int32)
+            m = _native.Move()
+            m.src_pool, m.dst_pool, m.n_blocks, m.done_value = pool.pool_id, peer.pool_id, n, 1
+            m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
+            _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1,
+                                                    _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK,
+                                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            torch.cuda.synchronize()
+            exchange_objects(pool.tensor[:, :, torch.from_numpy(sb).long()].view(torch.int16).cpu().numpy())
+            peer.close()
+            ok = True
+        else:
+            per = vllm_cache_shape("flash_attn", nb, 16, shape.kv_heads, shape.head_dim)
+            numel = int(np.prod(per))
+            raw = torch.zeros(shape.layers * numel, dtype=torch.float16, device="cuda:0")
+            caches = [raw[l * numel:(l + 1) * numel].view(per) for l in range(shape.layers)]
+            mine = StridedKVPool.from_vllm(caches, "flash_attn", name="vipc")
+            dst_blocks = [29, 0, 11, 5, 17, 2, 23]
+            torch.cuda.synchronize()
+            exchange_objects((mine.ipc_handles(), mine.kv_stride, mine.block_stride, dst_blocks))
+            sent = exchange_objects(None)[0]
+            got = np.stack([np.stack([np.stack([mine.piece(l, kv, b).view(torch.int16).cpu().numpy()
+                                                for b in dst_blocks]) for kv in range(2)])
+                            for l in range(shape.layers)])
+            ok = bool(np.array_equal(got, sent))
+        result_q.put((rank, ok, ""))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        result_q.put((rank, False, traceback.format_exc()))
+
+
+def test_two_process_push_into_peer_vllm_cache():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_vllm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, err in res:
+        assert ok, f"rank {rank} failed:\n{err}"
