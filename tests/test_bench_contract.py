@@ -51,6 +51,7 @@ def test_gpu_arm_contract():
     k = d["kernels"]   # fresh re-prefill / decode measurements beside the headline
     assert k["reprefill_13b_s1360"]["unit"] == "TFLOP/s" and 0.3 < k["reprefill_13b_s1360"]["frac"] < 1.5
     assert k["decode_7b_4k_32l"]["unit"] == "GB/s" and 0.3 < k["decode_7b_4k_32l"]["frac"] < 1.5
+    assert 0 < k["small_move_7b_1block"]["issue_to_landed_us_p50"] < 1000
 
 
 @pytest.mark.gpu

@@ -84,6 +84,41 @@ def main():
                "MiB": n * LLAMA2_7B.kv_bytes_per_token * 16 / 2 ** 20}
         rows.append(row)
         print(json.dumps(row), flush=True)
+    # one block, host lists, with completion consumers (table row + done flag):
+    # .gpu scope derived per call (pointer checks) vs forced .sys (no checks)
+    from paper_2501_06709_b200.kvcache import BlockTable
+
+    table = BlockTable(1, 4)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sb, db = np.array([1], dtype=np.int32), np.array([nb - 1], dtype=np.int32)
+    for label, extra in (("tracked_gpu_scope", 0), ("tracked_sys_scope", _native.KVM_F_SYS_SCOPE)):
+        m = _native.Move()
+        m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, 1, 1
+        m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
+        m.dst_table_row, m.done_flag = table.row_ptr(0), flag.data_ptr()
+        mp = ctypes.byref(m)
+        flags = _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK | extra
+        for _ in range(20):
+            lib.kvm_migrate(mp, 1, flags, sp)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(a.calls):
+            lib.kvm_migrate(mp, 1, flags, sp)
+        host_us = (time.perf_counter() - t0) / a.calls * 1e6
+        torch.cuda.synchronize()
+        lats = []
+        for _ in range(50):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            lib.kvm_migrate(mp, 1, flags, sp)
+            e1.record(s)
+            e1.synchronize()
+            lats.append(e0.elapsed_time(e1) * 1e3)
+        row = {"n_blocks": 1, "variant": label, "host_us": round(host_us, 2),
+               "lat_us": round(statistics.median(lats), 2)}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
     out = {"ctypes_us": round(ctypes_us, 3), "rows": rows, "device": torch.cuda.get_device_name(0)}
     print(json.dumps({"ctypes_us": out["ctypes_us"]}))
     if a.json:
