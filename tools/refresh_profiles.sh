@@ -22,6 +22,8 @@ for a in "" "--rows 4096" "--shape llama2-7b --rows 2048" "--kv-only" "--rows 14
   run "reprefill_${a// /_}" 300 python tools/bench_reprefill.py $a
 done
 run split 600 python tools/bench_split.py
+run issue 600 python tools/bench_issue.py
+run foreign 600 python tools/bench_foreign.py
 run live 600 python tools/bench_live.py
 for a in "" "--layers 1" "--shape llama3-70b-gqa --seq 16384" "--shape llama3-70b-gqa --seq 16384 --layers 1" \
          "--shape llama2-13b --seq 8192" "--batch 8 --layers 4"; do
