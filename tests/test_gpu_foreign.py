@@ -295,3 +295,33 @@ def test_executor_and_live_migration_on_vllm_caches():
         for kv in range(2):
             for i, b in enumerate(res.blocks):
                 assert torch.equal(p0.piece(l, kv, int(b)).view(torch.int16), src[1][l][kv][i].view(torch.int16))
+
+
+@pytest.mark.parametrize("layout", ["flash_attn", "flashinfer"])
+def test_fp8_vllm_cache_migrates_bit_exact(layout):
+    """vLLM's fp8 (e4m3) KV caches: one byte per element, pieces of 16 x H x D
+    bytes, moved into a native fp8 pool and back, bit-exact."""
+    shape = ModelShape("f8", layers=2, kv_heads=8, head_dim=128, q_heads=8, d_model=1024, elem_bytes=1)
+    nb = 24
+    g = torch.Generator(device="cuda").manual_seed(12)
+    caches = [torch.randint(0, 256, vllm_cache_shape(layout, nb, 16, 8, 128), generator=g, device="cuda",
+                            dtype=torch.uint8).view(torch.float8_e4m3fn) for _ in range(2)]
+    fx = StridedKVPool.from_vllm(caches, layout, name="f8")
+    nat = KVPool(shape, nb, dtype=torch.float8_e4m3fn)
+    nat.tensor.view(torch.uint8).zero_()
+    sb = np.array([3, 17, 0, 9], dtype=np.int32)
+    db = np.array([1, 2, 20, 23], dtype=np.int32)
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for s_pool, d_pool, s_b, d_b in ((fx, nat, sb, db), (nat, fx, db, np.array([4, 5, 6, 7], dtype=np.int32))):
+        m = _native.Move()
+        m.src_pool, m.dst_pool, m.n_blocks, m.done_value = s_pool.pool_id, d_pool.pool_id, 4, 1
+        m.src_blocks, m.dst_blocks = s_b.ctypes.data, d_b.ctypes.data
+        _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST |
+                                                _native.KVM_F_ENGINE_BULK, stream))
+    torch.cuda.synchronize()
+    for l in range(2):
+        for kv in range(2):
+            for i in range(4):
+                orig = fx.piece(l, kv, int(sb[i])).view(torch.uint8)
+                assert torch.equal(nat.tensor[l, kv, int(db[i])].view(torch.uint8), orig)
+                assert torch.equal(fx.piece(l, kv, 4 + i).view(torch.uint8), orig)
