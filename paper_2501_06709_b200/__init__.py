@@ -29,6 +29,11 @@ _SCHED_NAMES = ("MellScheduler", "PriorityConfig", "DEFAULT_PRIORITY", "Move", "
                 "batch_operations")
 
 
+# the trace side (workload.py): generator and trace-file format
+_WORKLOAD_NAMES = ("ArrivalRecord", "Trace", "LengthDistribution", "gen_poisson", "scale_trace", "load_trace",
+                   "save_trace")
+
+
 def __getattr__(name):  # data-path objects load the native library lazily
     if name in ("KVPool", "BlockTable", "BlockAllocator", "ModelShape", "LLAMA2_7B",
                 "LLAMA2_13B", "LLAMA3_70B", "SHAPES"):
@@ -43,4 +48,13 @@ def __getattr__(name):  # data-path objects load the native library lazily
     if name in ("MigrationExecutor", "ExecReport", "ExecRecord", "Residency"):
         from . import executor
         return getattr(executor, name)
+    if name in _WORKLOAD_NAMES:
+        from . import workload
+        return getattr(workload, name)
+    if name in ("simulate", "run_slots", "resolve_config", "load_config", "LoopResult"):
+        from . import runtime
+        return getattr(runtime, name)
+    if name in ("StridedKVPool", "vllm_cache_shape"):
+        from . import foreign
+        return getattr(foreign, name)
     raise AttributeError(name)

@@ -25,6 +25,8 @@ Reference line map for the loop body:
 """
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass, field
 from typing import Callable, Dict, List, Optional, Sequence, Tuple
@@ -241,13 +243,32 @@ def resolve_config(doc: Optional[dict] = None) -> Dict[str, dict]:
     return out
 
 
-def simulate(doc: Optional[dict] = None, records: Optional[Sequence[Tuple[int, int, int, int]]] = None, *,
+def load_config(path: str) -> Dict[str, dict]:
+    """A run-config JSON file -> resolve_config (config.py:189-197); unreadable
+    files and bad JSON raise ConfigError like the reference's loader."""
+    import json
+
+    from .errors import ConfigError
+
+    try:
+        with open(path, "r", encoding="utf-8") as fh:
+            doc = json.load(fh)
+    except OSError as exc:
+        raise ConfigError(f"cannot read config {path!r}: {exc}") from exc
+    except json.JSONDecodeError as exc:
+        raise ConfigError(f"invalid JSON in {path!r}: {exc}") from exc
+    return resolve_config(doc)
+
+
+def simulate(doc: Optional[dict] = None, records=None, *,
              executor=None, bpt=None, models: Optional[Dict[int, str]] = None,
              on_slot: Optional[Callable[[int, list], None]] = None) -> LoopResult:
     """Drop-in for the Mell path of the reference's `sim.run(config, trace)`
     (sim.py:103-268): build ClusterState + the native MellScheduler, Topology
-    and Boundaries from a reference config document, generate the Poisson trace
-    from its workload section unless `records` are given, and run the live slot
+    and Boundaries from a reference config document, take the trace from
+    `records` (a workload.Trace or (id, slot, prompt, response) rows), else from
+    workload.trace_path (a trace CSV, workload.load_trace), else generate the
+    Poisson trace from the workload section (cli.py:54-66), and run the live slot
     loop (optionally executing every plan on the GPUs through `executor`).
     `bpt` overrides workload.kv_bytes_per_token (an int, or a per-request dict
     for multi-LLM traces).  Returns the reference's metric series (LoopResult)."""
@@ -255,16 +276,20 @@ def simulate(doc: Optional[dict] = None, records: Optional[Sequence[Tuple[int, i
     from .errors import ConfigError
     from .planner import Topology, load_boundaries
     from .scheduler import MellScheduler, PriorityConfig
-    from .workload import LengthDistribution, gen_poisson
+    from .workload import LengthDistribution, Trace, gen_poisson, load_trace
 
-    cfg = resolve_config(doc)
+    cfg = resolve_config(doc)   # idempotent: a load_config() result passes through
     cl, sc, mg, wl, sm = (cfg[k] for k in ("cluster", "scheduler", "migration", "workload", "sim"))
     if sc["kind"] != "mell":
         raise ConfigError(f"scheduler kind {sc['kind']!r}: only Mell's scheduler is provided "
                           "(the reference's bf/wf/lb baselines are out of scope)")
+    if isinstance(records, Trace):
+        records = records.tuples()
+    if records is None and wl["trace_path"]:
+        if not os.path.exists(wl["trace_path"]):
+            raise ConfigError(f"trace file not found: {wl['trace_path']}")
+        records = load_trace(wl["trace_path"]).tuples()
     if records is None:
-        if wl["trace_path"] is not None:
-            raise ConfigError("trace files are not read here: pass `records`")
         dist = LengthDistribution(prompt_mean_log=wl["prompt_mean_log"], prompt_sigma_log=wl["prompt_sigma_log"],
                                   response_mean_log=wl["response_mean_log"],
                                   response_sigma_log=wl["response_sigma_log"], scale=wl["scale"])
