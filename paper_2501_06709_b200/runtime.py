@@ -50,10 +50,50 @@ class LoopResult:
     completed: int = 0
     rejected: int = 0
     aborted: int = 0
+    requests: int = 0
+    config: Optional[Dict[str, dict]] = None   # the resolved run config (simulate)
 
     @property
     def peak_gpus(self) -> int:
         return max(self.active_gpus, default=0)
+
+    # -- the reference's output files (sim.py:240-333) ------------------------------
+    def metrics_csv(self) -> str:
+        """metrics_to_csv: header + one row per slot (sim.py:312-321)."""
+        import csv
+        import io
+
+        buf = io.StringIO()
+        w = csv.writer(buf, lineterminator="\n")
+        w.writerow(["slot", "active_gpus", "migrations", "deferred", "forced", "used_bytes", "capacity_bytes"])
+        w.writerows(zip(range(len(self.active_gpus)), self.active_gpus, self.logical_moves, self.deferred,
+                        self.forced, self.used_bytes, self.capacity_bytes))
+        return buf.getvalue()
+
+    @property
+    def summary(self) -> Dict[str, object]:
+        """RunResult.summary (sim.py:240-257) for a Mell run."""
+        cfg = self.config or resolve_config({})
+        n = len(self.active_gpus)
+        return {"schema_version": 1, "scheduler": cfg["scheduler"]["kind"],
+                "batching": cfg["scheduler"]["batching"], "slots": n, "peak_gpus": self.peak_gpus,
+                "total_migrations": sum(self.logical_moves), "total_deferred": sum(self.deferred),
+                "total_forced": sum(self.forced), "mean_active_gpus": sum(self.active_gpus) / n if n else 0.0,
+                "mean_utilization": self.mean_utilization, "requests": self.requests, "completed": self.completed,
+                "rejected": self.rejected, "aborted": self.aborted,
+                "config": {**{k: dict(v) for k, v in cfg.items()}, "schema_version": 1}}
+
+    def write_metrics_csv(self, path: str) -> None:
+        with open(path, "w", encoding="utf-8", newline="") as fh:
+            fh.write(self.metrics_csv())
+
+    def write_summary_json(self, path: str) -> None:
+        """write_summary_json (sim.py:329-333): indent 2, sorted keys, newline."""
+        import json
+
+        with open(path, "w", encoding="utf-8") as fh:
+            json.dump(self.summary, fh, indent=2, sort_keys=True)
+            fh.write("\n")
 
     @property
     def mean_utilization(self) -> float:
@@ -217,20 +257,93 @@ _CONFIG_DEFAULTS = {
 }
 
 
+# value checks of each section, in the reference's order (config.py:29-120)
+_SCHEDULER_KINDS = ("mell", "bf", "wf", "lb")
+
+
+def _check_section(name: str, c: dict) -> Optional[str]:
+    if name == "cluster":
+        if c["capacity_bytes"] <= 0:
+            return "cluster.capacity_bytes must be > 0"
+        if c["gpus_per_machine"] < 1:
+            return "cluster.gpus_per_machine must be >= 1"
+        if c["max_gpus"] < 1:
+            return "cluster.max_gpus must be >= 1"
+        for k in ("intra_bandwidth_bytes_per_s", "inter_bandwidth_bytes_per_s", "prefill_tokens_per_s"):
+            if c[k] <= 0:
+                return f"cluster.{k} must be > 0"
+    elif name == "scheduler":
+        if c["kind"] not in _SCHEDULER_KINDS:
+            return f"scheduler.kind must be one of {_SCHEDULER_KINDS}"
+        for k in ("weight_free_mem", "weight_request_count", "weight_same_machine"):
+            if c[k] < 0:
+                return f"scheduler.{k} must be >= 0"
+        if c["rebalance_period"] < 1:
+            return "scheduler.rebalance_period must be >= 1"
+        if not 0.0 < c["imbalance_threshold"] < 1.0:
+            return "scheduler.imbalance_threshold must be in (0, 1)"
+    elif name == "migration":
+        if c["epoch_seconds"] <= 0:
+            return "migration.epoch_seconds must be > 0"
+        if not 0.0 < c["budget_fraction"] <= 1.0:
+            return "migration.budget_fraction must be in (0, 1]"
+        if c["max_defer"] < 0:
+            return "migration.max_defer must be >= 0"
+    elif name == "workload":
+        if c["mean_interarrival_slots"] <= 0:
+            return "workload.mean_interarrival_slots must be > 0"
+        if c["duration_slots"] < 0:
+            return "workload.duration_slots must be >= 0"
+        for k in ("prompt_sigma_log", "response_sigma_log"):
+            if c[k] < 0:
+                return f"workload.{k} must be >= 0"
+        if c["scale"] < 1:
+            return "workload.scale must be >= 1"
+        if c["kv_bytes_per_token"] <= 0:
+            return "workload.kv_bytes_per_token must be > 0"
+    elif name == "sim":
+        if c["tokens_per_slot"] < 1:
+            return "sim.tokens_per_slot must be >= 1"
+        if c["epoch_slots"] < 1:
+            return "sim.epoch_slots must be >= 1"
+    return None
+
+
+def _type_error(name: str, key: str, default, value) -> Optional[str]:
+    """The reference's per-key type rule (config.py:150-170), keyed on the
+    declared type, which the defaults carry (trace_path: Optional, unchecked)."""
+    if default is None:
+        return None
+    if isinstance(default, bool):
+        return None if isinstance(value, bool) else f"{name}.{key} must be a boolean"
+    if isinstance(default, int):
+        return None if isinstance(value, int) and not isinstance(value, bool) else f"{name}.{key} must be an integer"
+    if isinstance(default, float):
+        ok = isinstance(value, (int, float)) and not isinstance(value, bool)
+        return None if ok else f"{name}.{key} must be a number"
+    if isinstance(default, str):
+        return None if isinstance(value, str) else f"{name}.{key} must be a string"
+    return None
+
+
 def resolve_config(doc: Optional[dict] = None) -> Dict[str, dict]:
     """A reference run-config document (config.py's JSON schema, sections
     cluster / scheduler / migration / workload / sim) with the reference's
-    defaults filled in; unknown sections or keys raise ConfigError, like the
-    reference's strict loader (config.py:150-186)."""
+    defaults filled in and validated like config_from_dict (config.py:150-186,
+    dataclass __post_init__ checks): unknown sections or keys, wrong types and
+    out-of-range values raise ConfigError with the reference's messages.
+    Idempotent (a resolved config resolves to itself)."""
     from .errors import ConfigError
 
+    if doc is not None and not isinstance(doc, dict):
+        raise ConfigError("config root must be a JSON object")
     doc = dict(doc or {})
-    version = doc.pop("schema_version", 1)
-    if version != 1:
-        raise ConfigError(f"unsupported schema_version {version}, expected 1")
-    unknown = set(doc) - set(_CONFIG_DEFAULTS)
+    unknown = set(doc) - set(_CONFIG_DEFAULTS) - {"schema_version"}
     if unknown:
         raise ConfigError(f"unknown top-level keys: {sorted(unknown)}")
+    version = doc.pop("schema_version", 1)
+    if not isinstance(version, int) or isinstance(version, bool):
+        raise ConfigError("schema_version must be an integer")
     out = {}
     for name, defaults in _CONFIG_DEFAULTS.items():
         sec = doc.get(name, {})
@@ -239,7 +352,16 @@ def resolve_config(doc: Optional[dict] = None) -> Dict[str, dict]:
         bad = set(sec) - set(defaults)
         if bad:
             raise ConfigError(f"unknown keys in section {name!r}: {sorted(bad)}")
+        for key, value in sec.items():
+            err = _type_error(name, key, defaults[key], value)
+            if err:
+                raise ConfigError(err)
         out[name] = {**defaults, **sec}
+        err = _check_section(name, out[name])
+        if err:
+            raise ConfigError(err)
+    if version != 1:
+        raise ConfigError(f"unsupported schema_version {version}, expected 1")
     return out
 
 
@@ -302,7 +424,10 @@ def simulate(doc: Optional[dict] = None, records=None, *,
                     inter_bandwidth_bytes_per_s=cl["inter_bandwidth_bytes_per_s"],
                     prefill_tokens_per_s=cl["prefill_tokens_per_s"])
     bounds = load_boundaries(topo, mg["epoch_seconds"], mg["budget_fraction"])
-    return run_slots(records, sched, cluster, topo, bounds, bpt=wl["kv_bytes_per_token"] if bpt is None else bpt,
-                     tokens_per_slot=sm["tokens_per_slot"], epoch_slots=sm["epoch_slots"],
-                     max_defer=mg["max_defer"], duration_slots=wl["duration_slots"], executor=executor,
-                     models=models, on_slot=on_slot)
+    records = list(records)
+    res = run_slots(records, sched, cluster, topo, bounds, bpt=wl["kv_bytes_per_token"] if bpt is None else bpt,
+                    tokens_per_slot=sm["tokens_per_slot"], epoch_slots=sm["epoch_slots"],
+                    max_defer=mg["max_defer"], duration_slots=wl["duration_slots"], executor=executor,
+                    models=models, on_slot=on_slot)
+    res.requests, res.config = len(records), cfg
+    return res

@@ -13,6 +13,7 @@ paper_2501_06709_b200.scheduler / .cluster) makes the reference's decisions.
 * Direct public operations (allocate / depart / update / handle_growth) on
   both, with identical results or identical exception classes.
 """
+import json
 import random
 
 import pytest
@@ -247,11 +248,16 @@ def test_simulate_matches_reference_sim_run(doc):
     w = cfg.workload
     trace = ref.gen_poisson(w.mean_interarrival_slots, w.duration_slots, ref.LengthDistribution(scale=w.scale),
                             cfg.sim.seed)
-    m = ref_run(cfg, trace).metrics
+    rr = ref_run(cfg, trace)
+    m = rr.metrics
     out = simulate(doc)
     assert out.active_gpus == m.active_gpus and out.logical_moves == m.migrations
     assert out.deferred == m.deferred and out.forced == m.forced
     assert out.used_bytes == m.used_bytes and out.capacity_bytes == m.capacity_bytes
+    # the reference's output files, byte for byte
+    from kvpack.sim import metrics_to_csv
+    assert out.metrics_csv() == metrics_to_csv(m)
+    assert json.dumps(out.summary, sort_keys=True, indent=2) == json.dumps(rr.summary, sort_keys=True, indent=2)
 
 
 def test_simulate_rejects_unknown_config():
@@ -262,3 +268,53 @@ def test_simulate_rejects_unknown_config():
         simulate({"cluster": {"bogus": 1}})
     with pytest.raises(ConfigError):
         simulate({"scheduler": {"kind": "lb"}})
+
+
+_BAD_CONFIGS = [
+    [], {"bogus": {}}, {"schema_version": 2}, {"schema_version": True}, {"cluster": []},
+    {"cluster": {"capacity_bytes": 0}}, {"cluster": {"capacity_bytes": 1.5}}, {"cluster": {"gpus_per_machine": 0}},
+    {"cluster": {"max_gpus": 0}}, {"cluster": {"intra_bandwidth_bytes_per_s": 0}},
+    {"cluster": {"prefill_tokens_per_s": "fast"}}, {"cluster": {"capacity_bytes": True}},
+    {"scheduler": {"kind": "rr"}}, {"scheduler": {"batching": 1}}, {"scheduler": {"weight_free_mem": -1}},
+    {"scheduler": {"rebalance_period": 0}}, {"scheduler": {"imbalance_threshold": 1.0}}, {"scheduler": {"kind": 3}},
+    {"migration": {"epoch_seconds": 0}}, {"migration": {"budget_fraction": 1.5}}, {"migration": {"max_defer": -1}},
+    {"workload": {"mean_interarrival_slots": 0}}, {"workload": {"duration_slots": -1}},
+    {"workload": {"prompt_sigma_log": -0.1}}, {"workload": {"scale": 0}}, {"workload": {"kv_bytes_per_token": 0}},
+    {"workload": {"trace_path": 5, "scale": 0}}, {"sim": {"tokens_per_slot": 0}}, {"sim": {"epoch_slots": 0}},
+    {"sim": {"seed": 1.0}}, {"cluster": {"capacity_bytes": 0}, "sim": {"epoch_slots": 0}},
+]
+
+
+@pytest.mark.parametrize("doc", _BAD_CONFIGS, ids=[str(i) for i in range(len(_BAD_CONFIGS))])
+def test_config_validation_matches_reference(doc):
+    """resolve_config rejects exactly what config_from_dict rejects, with the
+    same ConfigError message."""
+    from paper_2501_06709_b200.errors import ConfigError
+    from paper_2501_06709_b200.runtime import resolve_config
+
+    with pytest.raises(ConfigError) as ours:
+        resolve_config(doc)
+    ref = sd.kvpack()
+    if ref is None:
+        return
+    from kvpack.config import config_from_dict
+    from kvpack.errors import ConfigError as RefConfigError
+
+    with pytest.raises(RefConfigError) as theirs:
+        config_from_dict(doc)
+    assert str(ours.value) == str(theirs.value)
+
+
+def test_valid_configs_resolve_like_reference():
+    ref = sd.kvpack()
+    if ref is None:
+        pytest.skip("reference tree not mounted")
+    from kvpack.config import config_from_dict
+
+    from paper_2501_06709_b200.runtime import resolve_config
+
+    for doc in ({}, {"cluster": {"intra_bandwidth_bytes_per_s": 900_000_000_000}, "scheduler": {"kind": "bf"}},
+                {"workload": {"trace_path": "x.csv", "scale": 3}, "sim": {"seed": 9}, "schema_version": 1}):
+        r = config_from_dict(doc).to_dict()
+        assert {**resolve_config(doc), "schema_version": 1} == r
+        assert resolve_config(resolve_config(doc)) == resolve_config(doc)
