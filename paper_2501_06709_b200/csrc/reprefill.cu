@@ -75,6 +75,13 @@ struct Params {
   int32_t table_n;
 };
 constexpr int CUNIT = 8192;     // copy unit per warp iteration: 32 lanes x 16 x 16 B
+#ifndef KVM_SPLIT_CS
+#define KVM_SPLIT_CS 4
+#endif
+#ifndef KVM_SPLIT_CLAG
+#define KVM_SPLIT_CLAG 2
+#endif
+constexpr int CS = KVM_SPLIT_CS, CLAG = KVM_SPLIT_CLAG;  // bulk prefix copy (pair kernel): ring slots, loads in flight
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -203,6 +210,58 @@ __device__ __forceinline__ bool copy_one_unit(const Params& p, int* next, int la
     if (i < nv) dst[i] = v[j];
   }
   return true;
+}
+
+// Addresses of copy unit u (u < c_units): 8 KiB (or the piece's tail) of one piece.
+__device__ __forceinline__ void copy_unit_addr(const Params& p, int64_t u, const uint8_t** src, uint8_t** dst,
+                                               uint32_t* bytes) {
+  const int32_t per_plane = p.c_nblocks * p.c_upp;
+  const int32_t plane = (int32_t)(u / per_plane);
+  const int32_t r = (int32_t)(u - (int64_t)plane * per_plane);
+  const int32_t bi = r / p.c_upp, ui = r - bi * p.c_upp;
+  const int64_t off = (int64_t)ui * CUNIT;
+  *bytes = (uint32_t)min((int64_t)CUNIT, p.piece_bytes - off);
+  *src = piece_ptr(p.csrc, plane >> 1, plane & 1, __ldg(p.csrc_blocks + bi)) + off;
+  *dst = piece_ptr(p.pool, plane >> 1, plane & 1, __ldg(p.dst_blocks + bi)) + off;
+}
+
+// One thread: this CTA's units blockIdx.x, blockIdx.x + gridDim.x, ... through a
+// CS-slot smem ring; load i is issued before the store of i - CLAG, so CLAG
+// loads and CS - CLAG stores are in flight.  Returns with every store complete
+// (the CTA's completion accounting follows).
+__device__ __noinline__ void bulk_copy_units(const Params& p, uint8_t* ring, uint64_t* bar) {
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t n = first < p.c_units ? (p.c_units - 1 - first) / stride + 1 : 0;
+  for (int64_t i = 0; i < n + CLAG; ++i) {
+    const int64_t j = i - CLAG;
+    if (j >= 0) {  // store tile j once its load landed
+      const int sj = (int)(j % CS);
+      const uint8_t* src;
+      uint8_t* dst;
+      uint32_t bytes;
+      copy_unit_addr(p, first + j * stride, &src, &dst, &bytes);
+      mbar_wait(bar + sj, (uint32_t)((j / CS) & 1));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"(smem_u32(ring + sj * CUNIT)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (i < n) {  // load tile i into slot i % CS (its previous store has read the slot)
+      const int si = (int)(i % CS);
+      const uint8_t* src;
+      uint8_t* dst;
+      uint32_t bytes;
+      copy_unit_addr(p, first + i * stride, &src, &dst, &bytes);
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(CS - CLAG) : "memory");
+      mbar_expect_tx(bar + si, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(ring + si * CUNIT)),
+          "l"(src), "r"(bytes), "r"(smem_u32(bar + si))
+          : "memory");
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -464,6 +523,20 @@ constexpr int EPI_BF16 = 32 * 32 * 2;                // per warp: [32 tokens][32
 constexpr int EPI_F32 = 32 * 32 * 4;                 // per warp: fp32 exchange tile (RoPE partner)
 constexpr int EPI_BYTES = 4 * (EPI_BF16 + EPI_F32);
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 1024;
+// Fused split migration (kCopy): the prefix is streamed by ONE thread driving the
+// TMA bulk-copy unit (global -> smem -> global, CS x 8 KiB ring, CLAG loads in
+// flight) instead of LDG/STG from idle and epilogue warps.  The ring takes one
+// GEMM stage's shared memory (4, 5 and 6 stages measure within 1 %).
+#ifndef KVM_SPLIT_COPY_BULK
+#define KVM_SPLIT_COPY_BULK 1
+#endif
+constexpr bool COPY_BULK = KVM_SPLIT_COPY_BULK != 0;
+constexpr int COPY_STAGES = COPY_BULK ? STAGES - 1 : STAGES;   // GEMM stages of the kCopy kernel
+constexpr int COPY_RING = COPY_BULK ? CS * CUNIT : 0;
+constexpr int SMEM_BYTES_COPY = COPY_STAGES * STAGE_BYTES + COPY_RING + EPI_BYTES + 1024 + 1024;
+static_assert(SMEM_BYTES_COPY <= 227 * 1024, "pair kernel (copy) shared memory");
+template <bool kCopy>
+__host__ __device__ constexpr int stages_of() { return kCopy ? COPY_STAGES : STAGES; }
 constexpr uint32_t TMEM_COLS = 512;                   // two 128 x 256 fp32 accumulators per CTA
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -582,12 +655,15 @@ __device__ __forceinline__ TokenTile token_tile(const Params& p, int nt) {
 template <bool kCopy>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefill_pair_kernel(
     const __grid_constant__ Params p) {
+  constexpr int kSt = stages_of<kCopy>();
+  constexpr bool kBulkCopy = kCopy && COPY_BULK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* epi = smem + STAGES * STAGE_BYTES;
+  uint8_t* cring = smem + kSt * STAGE_BYTES;                    // kBulkCopy: CS x 8 KiB copy ring
+  uint8_t* epi = cring + (kBulkCopy ? COPY_RING : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(epi + EPI_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* empty = full + kSt;
+  uint64_t* tfull = empty + kSt;
   uint64_t* tempty = tfull + 2;
   TileQueue tq;
   tq.full = tempty + 2;
@@ -596,6 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
   tq.i = 0;
   tq.ph = 0;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq.slot + TQ);
+  uint64_t* cbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // kBulkCopy: CS copy-ring barriers
   __shared__ int s_last;
   __shared__ int s_copy_next;  // next copy unit (CTA-local index) of the fused prefix transfer
 
@@ -608,10 +685,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
       asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_x) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&p.tmap_w) : "memory");
     }
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       mbar_init(full + s, 1);   // leader: its own arrive.expect_tx (both CTAs' bytes complete on it)
       mbar_init(empty + s, 1);  // both: the leader's multicast MMA commit
     }
+    if (kBulkCopy)
+      for (int s = 0; s < CS; ++s) mbar_init(cbar + s, 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);      // both: multicast commit
       mbar_init(tempty + a, 8);     // leader: one elected lane per epilogue warp of each CTA
@@ -668,7 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
             tma_3d_pair(&p.tmap_x, bar, sb, kb * BK, tt.start + (int)rank * half, l);
           else
             tma_2d_pair(&p.tmap_x, bar, sb, kb * BK, tt.start + (int)rank * half);
-          if (++stage == STAGES) {
+          if (++stage == kSt) {
             stage = 0;
             phase ^= 1;
           }
@@ -698,7 +777,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
           for (int k = 0; k < BK / 16; ++k)
             mma_pair(d_tmem, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), id, (kb | k) != 0);
           commit_both(empty + stage);  // both CTAs may refill this stage once the MMAs read it
-          if (++stage == STAGES) {
+          if (++stage == kSt) {
             stage = 0;
             phase ^= 1;
           }
@@ -710,14 +789,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) reprefil
         }
       }
     }
-  } else if (kCopy && (warp == 2 || warp == 3)) {
+  } else if (kBulkCopy && warp == 2) {
+    // fused split migration: one thread streams this CTA's prefix units through the bulk-copy unit
+    if (lane == 0) bulk_copy_units(p, cring, cbar);
+  } else if (kCopy && !kBulkCopy && (warp == 2 || warp == 3)) {
     // fused split migration: warps idle in the GEMM stream the transferred prefix
     while (copy_one_unit(p, &s_copy_next, lane)) {
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> bf16 -> smem transpose -> paged pool ----------------
     const int q = warp & 3;
-    bool copying = kCopy;
+    bool copying = kCopy && !kBulkCopy;
     __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(epi + q * EPI_BF16);  // [32 tokens][32 features]
     float* xch = reinterpret_cast<float*>(epi + 4 * EPI_BF16);                    // 4 x [32 tokens][32 features]
     const uint32_t tempty_leader = mapa(smem_u32(tempty), 0);
@@ -1005,7 +1087,7 @@ static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
     KVM_CUDA_TRY(cudaFuncSetAttribute(pair::reprefill_pair_kernel<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES));
     KVM_CUDA_TRY(cudaFuncSetAttribute(pair::reprefill_pair_kernel<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM_BYTES_COPY));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (sm_count(dev) / 2));
     cfg.blockDim = dim3(THREADS);
@@ -1027,7 +1109,7 @@ static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
   if (copy) work = std::max<int64_t>(work, (p.c_units + 3) / 4);  // ~4 copy warps per cluster
   const int grid = 2 * (int)std::max<int64_t>(1, std::min<int64_t>(work, clusters[dev]));
   if (copy)
-    pair::reprefill_pair_kernel<true><<<grid, THREADS, pair::SMEM_BYTES, stream>>>(p);
+    pair::reprefill_pair_kernel<true><<<grid, THREADS, pair::SMEM_BYTES_COPY, stream>>>(p);
   else
     pair::reprefill_pair_kernel<false><<<grid, THREADS, pair::SMEM_BYTES, stream>>>(p);
   KVM_CUDA_TRY(cudaGetLastError());
