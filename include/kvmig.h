@@ -291,7 +291,11 @@ int kvm_ipc_close(void* mapped_ptr, int64_t offset);
 /* --- data path -------------------------------------------------------------- */
 /* Launch one fused gather -> push -> block-table-rewrite kernel for up to
  * KVM_MAX_MOVES moves (larger batches are split internally), on the device
- * that owns the first move's source pool.  Asynchronous on `stream`. */
+ * that owns the first move's source pool.  Asynchronous on `stream`.
+ * Within one launch (KVM_MAX_MOVES moves) no destination block may be written
+ * twice, nor read by another move while written: with KVM_F_BLOCKS_ON_HOST
+ * this is verified (KVM_ERR_INVALID, nothing launched); with device-resident
+ * lists it is the caller's contract. */
 #define KVM_MAX_MOVES 96
 int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream);
 /* src pool == dst pool: move n blocks of one request into fresh blocks.  The

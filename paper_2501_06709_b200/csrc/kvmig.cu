@@ -659,6 +659,48 @@ static bool local_device_ptr(const void* ptr, int device) {
   return a.type == cudaMemoryTypeDevice && a.device == device && !ipc_imported(ptr);
 }
 
+// Host block lists: within one launch no destination block may be written
+// twice, nor written while another move of the launch reads it (same pool) --
+// the tiles run concurrently, so either would race.  O(total blocks) with a
+// reusable per-thread mark array (touched entries are cleared afterwards).
+static int validate_batch_disjoint(const kvm_move* moves, int n) {
+  thread_local std::vector<uint8_t> mark;
+  int rc = KVM_OK;
+  for (int i = 0; i < n && !rc; ++i) {
+    const int pool = moves[i].dst_pool;
+    bool seen_before = false;   // each distinct dst pool once
+    for (int k = 0; k < i; ++k) seen_before |= (moves[k].dst_pool == pool);
+    if (seen_before) continue;
+    const Pool* dp = get_pool(pool);
+    if ((int)mark.size() < dp->desc.num_blocks) mark.resize(dp->desc.num_blocks, 0);
+    for (int m = i; m < n && !rc; ++m) {
+      if (moves[m].dst_pool != pool) continue;
+      for (int j = 0; j < moves[m].n_blocks; ++j) {
+        uint8_t& v = mark[moves[m].dst_blocks[j]];
+        if (v) {
+          rc = fail(KVM_ERR_INVALID, "dst block " + std::to_string(moves[m].dst_blocks[j]) + " of pool " +
+                                         std::to_string(pool) + " is written twice in one launch");
+          break;
+        }
+        v = 1;
+      }
+    }
+    for (int m = 0; m < n && !rc; ++m) {
+      if (moves[m].src_pool != pool) continue;
+      for (int j = 0; j < moves[m].n_blocks; ++j)
+        if (mark[moves[m].src_blocks[j]]) {
+          rc = fail(KVM_ERR_INVALID, "block " + std::to_string(moves[m].src_blocks[j]) + " of pool " +
+                                         std::to_string(pool) + " is both read and written in one launch");
+          break;
+        }
+    }
+    for (int m = i; m < n; ++m)   // clear what this pool marked
+      if (moves[m].dst_pool == pool)
+        for (int j = 0; j < moves[m].n_blocks; ++j) mark[moves[m].dst_blocks[j]] = 0;
+  }
+  return rc;
+}
+
 template <class P>
 static int launch_copy(const P& p, int64_t tiles, bool any_empty, int flags, int device, const DevState& ds,
                        cudaStream_t stream) {
@@ -774,6 +816,7 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
   }
   p.total_tiles = tiles;
   p.per_layer_flush = any_layer_flags ? 1 : 0;
+  if (on_host && (rc = validate_batch_disjoint(moves, n))) return rc;
 
   // A staging slot is needed only for host lists that are not inline and for
   // completion counters; an untracked inline move is parameters only.

@@ -416,3 +416,31 @@ def test_executor_stream_ordered_chain():
     assert np.array_equal(got6.view(torch.int16).cpu().numpy(), src_np[:, :, b6])
     assert np.array_equal(row5.cpu().numpy(), ex.where(5).blocks)
     assert pools[1].allocator.n_free == 64
+
+
+def test_batch_write_write_and_read_write_conflicts_rejected():
+    """Host block lists: a launch may not write one destination block twice, nor
+    read a block another move of the same launch writes; rejected before any
+    byte moves (ValueError), legal batches still run."""
+    nb = 32
+    a, b = KVPool(SMALL, nb), KVPool(SMALL, nb)
+    _fill(a, 1)
+    _fill(b, 2)
+    before = (a.tensor.view(torch.int16).clone(), b.tensor.view(torch.int16).clone())
+    flags = _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK
+    arrs = lambda *xs: [np.array(x, dtype=np.int32) for x in xs]  # noqa: E731
+    s1, d1, s2, d2 = arrs([1, 2], [5, 6], [3, 4], [6, 7])          # dst 6 written twice
+    with pytest.raises(ValueError, match="written twice"):
+        _run([_move(a, b, s1, d1), _move(a, b, s2, d2)], flags)
+    s1, d1, s2, d2 = arrs([1, 2], [5, 6], [6, 9], [10, 11])        # move 2 reads b:6 that move 1 writes
+    with pytest.raises(ValueError, match="read and written"):
+        _run([_move(a, b, s1, d1), _move(b, a, s2, d2)], flags)
+    s1, d1 = arrs([1, 2, 3], [9, 2, 8])                            # compaction-style self overlap
+    with pytest.raises(ValueError, match="read and written"):
+        _run([_move(a, a, s1, d1)], flags)
+    assert torch.equal(a.tensor.view(torch.int16), before[0]) and torch.equal(b.tensor.view(torch.int16), before[1])
+    s1, d1, s2, d2 = arrs([1, 2], [5, 6], [1, 2], [7, 8])          # the same source read twice is fine
+    _run([_move(a, b, s1, d1), _move(a, b, s2, d2)], flags)
+    got = b.tensor.view(torch.int16)
+    assert torch.equal(got[:, :, [5, 6]], before[0][:, :, [1, 2]]) and torch.equal(got[:, :, [7, 8]],
+                                                                                    before[0][:, :, [1, 2]])
