@@ -187,6 +187,14 @@ typedef struct kvm_split_args {
  * (fp16, or bf16 with KVM_DECODE_BF16).  Split-K workspace is library-owned
  * per device: calls on one device must be stream-ordered. */
 #define KVM_DECODE_BF16 0x1
+/* Layer-wise pipelining with an incoming migration: every CTA of layer l
+ * first waits (ld.acquire.sys) until layer_flags[l] >= layer_value -- the
+ * per-layer flags kvm_migrate publishes (kvm_move.layer_flags) -- so decode
+ * of layer l overlaps the copy of later layers.  block_tables must already
+ * hold the destination blocks (they are known before the copy); only KV
+ * contents are awaited.  timeout_ns > 0 bounds the wait: on expiry *err_word
+ * is set to 1 and the kernel proceeds (its output is then meaningless). */
+#define KVM_DECODE_WAIT_LAYERS 0x4
 #define KVM_DECODE_CUDA_CORES 0x2 /* force the CUDA-core path (G in {1,2,4,8});
                                      default: tensor-core mma path for G <= 8 */
 typedef struct kvm_decode_args {
@@ -203,6 +211,12 @@ typedef struct kvm_decode_args {
   const int32_t* block_tables; /* [batch][max_blocks], device */
   const int32_t* seq_lens;     /* [batch], device */
   void* out;            /* [n_layers][batch][q_heads][128] */
+  /* KVM_DECODE_WAIT_LAYERS only (else ignored): */
+  const uint32_t* layer_flags; /* [layers] (absolute layer index), device-visible */
+  uint32_t layer_value;
+  uint32_t _pad;
+  uint64_t timeout_ns;         /* 0: wait forever */
+  uint32_t* err_word;          /* nullable */
 } kvm_decode_args;
 
 /* Native planner (kvm_plan_hybrid): the reference's plan_hybrid

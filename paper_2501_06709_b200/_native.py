@@ -56,6 +56,7 @@ EXPORTS = (
 )
 KVM_DECODE_BF16 = 0x1
 KVM_DECODE_CUDA_CORES = 0x2
+KVM_DECODE_WAIT_LAYERS = 0x4
 
 
 class PoolDesc(ctypes.Structure):
@@ -95,7 +96,8 @@ class DecodeArgs(ctypes.Structure):
                 ("batch", ctypes.c_int32), ("q_heads", ctypes.c_int32), ("max_blocks", ctypes.c_int32),
                 ("max_seq_len", ctypes.c_int32), ("flags", ctypes.c_int32), ("scale", ctypes.c_float),
                 ("q", ctypes.c_void_p), ("block_tables", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p),
-                ("out", ctypes.c_void_p)]
+                ("out", ctypes.c_void_p), ("layer_flags", ctypes.c_void_p), ("layer_value", ctypes.c_uint32),
+                ("_pad", ctypes.c_uint32), ("timeout_ns", ctypes.c_uint64), ("err_word", ctypes.c_void_p)]
 
 
 class Pending(ctypes.Structure):

@@ -54,9 +54,35 @@ struct Params {
   // layers[l] for a strided (foreign-layout) pool, else pool + l * layer_stride
   const uint8_t* const* layers;
   int64_t layer_stride, kv_stride, block_stride, tok_stride;  // tok_stride = kv_heads * D * 2
+  const uint32_t* layer_flags;  // KVM_DECODE_WAIT_LAYERS, else NULL
+  uint32_t layer_value;
+  uint64_t timeout_ns;
+  uint32_t* err_word;
   int32_t layer0, n_layers, batch, q_heads, kv_heads, max_blocks, splits, num_blocks, bps;
   float scale_log2;  // scale * log2(e)
 };
+
+// KVM_DECODE_WAIT_LAYERS: one thread acquires layer `layer`'s flag, the CTA
+// follows it through the barrier.  Bounded by timeout_ns (then *err_word = 1).
+__device__ __forceinline__ void wait_layer(const Params& p, int layer) {
+  if (!p.layer_flags) return;
+  if (threadIdx.x == 0) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned ns = 32;
+    while (ld_acquire_sys_u32(p.layer_flags + layer) < p.layer_value) {
+      __nanosleep(ns);
+      if (ns < 512) ns <<= 1;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (p.timeout_ns && t - t0 > p.timeout_ns) {
+        if (p.err_word) atomicExch(p.err_word, 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
 
 __device__ __forceinline__ const uint8_t* layer_base(const Params& p, int layer) {
   if (p.layers)
@@ -82,6 +108,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_split_kernel(const __grid_c
   const int nblk = (seq + 15) >> 4;
   const int blk_lo = split * p.bps;
   const int blk_hi = min(nblk, blk_lo + p.bps);
+  wait_layer(p, layer);
 
   __shared__ float s_m[WARPS][G], s_l[WARPS][G];
   __shared__ float s_acc[WARPS][G][D];
@@ -282,6 +309,7 @@ __global__ void __launch_bounds__(WARPS * 32) decode_gqa_kernel(const __grid_con
   const int blk_lo = split * p.bps;
   const int blk_hi = min(nblk, blk_lo + p.bps);
   const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(gsm) + warp * GQA_WARP_SMEM;
+  wait_layer(p, layer);
 
   // Q^T fragments (B operand of S = K Q^T): head g, dims 16kk + 2t (+8); heads >= G are zero
   uint32_t qf[8][2];
@@ -558,6 +586,10 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
   if (a->max_blocks <= 0 || a->max_seq_len <= 0 || a->max_seq_len > a->max_blocks * 16)
     return fail(KVM_ERR_INVALID, "max_seq_len must be in (0, 16 * max_blocks]");
   const int G = a->q_heads / d.kv_heads;
+  if (a->flags & ~(KVM_DECODE_BF16 | KVM_DECODE_CUDA_CORES | KVM_DECODE_WAIT_LAYERS))
+    return fail(KVM_ERR_INVALID, "unknown flags");
+  if ((a->flags & KVM_DECODE_WAIT_LAYERS) && !a->layer_flags)
+    return fail(KVM_ERR_INVALID, "KVM_DECODE_WAIT_LAYERS needs layer_flags");
   Params p;
   p.pool = pool->base;
   p.q = a->q;
@@ -565,6 +597,11 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
   p.tables = a->block_tables;
   p.seq_lens = a->seq_lens;
   p.layers = pool->layers;
+  const bool wait = (a->flags & KVM_DECODE_WAIT_LAYERS) != 0;
+  p.layer_flags = wait ? a->layer_flags : nullptr;
+  p.layer_value = a->layer_value;
+  p.timeout_ns = a->timeout_ns;
+  p.err_word = a->err_word;
   p.layer_stride = pool->layer_stride;
   p.kv_stride = pool->kv_stride;
   p.block_stride = pool->block_stride;

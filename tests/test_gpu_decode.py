@@ -100,3 +100,85 @@ def test_decode_concurrent_streams_have_private_workspaces():
         s.synchronize()
     for o, e in zip(outs, expect):
         assert torch.equal(o.view(torch.int16), e.view(torch.int16))
+
+
+def _wait_setup(layers=4, seq=3000, seed=21):
+    shape = ModelShape("dw", layers=layers, kv_heads=2, head_dim=128, q_heads=8, d_model=1024)
+    k = (seq + 15) // 16
+    nb = 2 * k + 8
+    src, dst = KVPool(shape, nb, dtype=torch.bfloat16), KVPool(shape, nb, dtype=torch.bfloat16)
+    _fill_normal(src, seed)
+    dst.tensor.zero_()
+    sb = torch.randperm(nb, generator=torch.Generator().manual_seed(seed))[:k].to(torch.int32)
+    db = torch.randperm(nb, generator=torch.Generator().manual_seed(seed + 1))[:k].to(torch.int32)
+    q = torch.randn(layers, 1, 8, 128, generator=torch.Generator(device="cuda").manual_seed(seed),
+                    device="cuda").to(torch.bfloat16)
+    lens = torch.tensor([seq], dtype=torch.int32, device="cuda")
+    return shape, src, dst, sb, db, q, lens
+
+
+def test_decode_waits_on_layer_flags_written_by_the_host():
+    """KVM_DECODE_WAIT_LAYERS with flags in pinned host memory, released by the
+    host one layer at a time after the kernel is queued: the decode waits, then
+    equals an unconditional decode bit for bit; no timeout fired."""
+    import threading
+    import time
+
+    shape, src, dst, sb, db, q, lens = _wait_setup()
+    ref = paged_decode(src, q, sb[None].contiguous().cuda(), lens)
+    flags = torch.zeros(shape.layers, dtype=torch.int32).pin_memory()
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+
+    def release():
+        for l in range(shape.layers):
+            time.sleep(0.005)
+            flags[l] = 7
+    th = threading.Thread(target=release)
+    t0 = time.perf_counter()
+    out = paged_decode(src, q, sb[None].contiguous().cuda(), lens, stream=s, layer_flags=flags, layer_value=7,
+                       timeout_ns=10_000_000_000, err_word=err)
+    th.start()
+    s.synchronize()
+    waited = time.perf_counter() - t0
+    th.join()
+    assert err.item() == 0
+    assert waited >= 0.015   # the kernel could not finish before the last layer was released
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+
+
+def test_decode_layer_wait_times_out_instead_of_hanging():
+    shape, src, dst, sb, db, q, lens = _wait_setup(layers=2, seq=200)
+    flags = torch.zeros(shape.layers, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    paged_decode(src, q, sb[None].contiguous().cuda(), lens, layer_flags=flags, timeout_ns=2_000_000, err_word=err)
+    torch.cuda.synchronize()
+    assert err.item() == 1
+
+
+def test_decode_pipelined_behind_an_incoming_migration():
+    """Layer-wise pipelining on one GPU: kvm_migrate (per-layer flags) on one
+    stream, the destination decode (waiting on those flags, destination block
+    table known up front) on another; the result equals decoding the source."""
+    import ctypes
+
+    from paper_2501_06709_b200 import _native
+
+    shape, src, dst, sb, db, q, lens = _wait_setup(layers=8, seq=6000, seed=33)
+    ref = paged_decode(src, q, sb[None].contiguous().cuda(), lens)
+    flags = torch.zeros(shape.layers, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    copy_s, dec_s = torch.cuda.Stream(), torch.cuda.Stream()
+    m = _native.Move()
+    m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, len(sb), 1
+    sbn, dbn = sb.numpy(), db.numpy()
+    m.src_blocks, m.dst_blocks, m.layer_flags = sbn.ctypes.data, dbn.ctypes.data, flags.data_ptr()
+    _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK,
+                                            ctypes.c_void_p(copy_s.cuda_stream)))
+    out = paged_decode(dst, q, db[None].contiguous().cuda(), lens, stream=dec_s, layer_flags=flags, layer_value=1,
+                       timeout_ns=5_000_000_000, err_word=err)
+    torch.cuda.synchronize()
+    assert err.item() == 0
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
