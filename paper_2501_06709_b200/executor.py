@@ -58,6 +58,9 @@ class ExecRecord:
     tokens_moved: int = 0  # tokens of the members copied: algorithmic bytes = tokens_moved * bpt
     request_tokens: Dict[int, int] = field(default_factory=dict)  # per moved request: its tokens
     done: Optional[object] = None  # stream-ordered calls: CUDA event recorded after the move (and read-back)
+    # execute(layer_flags=True): per moved request, an int32 device tensor [layers] on the destination
+    # GPU; entry l reaches 1 once layer l landed (paged_decode(..., layer_flags=...) pipelines on it)
+    layer_flags: Dict[int, object] = field(default_factory=dict)
 
 
 @dataclass
@@ -228,11 +231,15 @@ class MigrationExecutor:
 
     # -- execution ---------------------------------------------------------------
     def execute(self, plan, members_of: Optional[Callable[[int], Sequence[int]]] = None,
-                wait: bool = True, stream_ordered: bool = False) -> ExecReport:
+                wait: bool = True, stream_ordered: bool = False, layer_flags: bool = False) -> ExecReport:
         """Carry out `plan.executed` (or a list of PlannedMove) in plan order.
 
         members_of(item) -> request ids of a group item (negative id); the
         default treats every item as a single request.
+
+        layer_flags: kv moves publish per-layer completion into `rec.layer_flags[rid]`
+        (value 1), so a destination decode can start layer by layer
+        (attention.paged_decode(..., layer_flags=...)) while the copy runs.
 
         stream_ordered: return right after issuing, with residencies already
         switched on the host.  Each destination GPU's executor stream waits
@@ -298,6 +305,12 @@ class MigrationExecutor:
                     if table is not None:
                         table.set_host(rid, db)
                         m.dst_table_row = table.row_ptr(rid)
+                    if layer_flags:
+                        import torch
+
+                        fl = torch.zeros(src_pool.shape.layers, dtype=torch.int32, device=f"cuda:{dst_pool.device}")
+                        rec.layer_flags[rid] = fl
+                        m.layer_flags = fl.data_ptr()
                     by_dev.setdefault(src_pool.device, []).append(m)
                     rec.bytes_moved += nb * src_pool.shape.piece_bytes * 2 * src_pool.shape.layers
                     rec.tokens_moved += res.tokens

@@ -444,3 +444,33 @@ def test_batch_write_write_and_read_write_conflicts_rejected():
     got = b.tensor.view(torch.int16)
     assert torch.equal(got[:, :, [5, 6]], before[0][:, :, [1, 2]]) and torch.equal(got[:, :, [7, 8]],
                                                                                     before[0][:, :, [1, 2]])
+
+
+def test_executor_layer_flags_feed_a_pipelined_decode():
+    """execute(stream_ordered=True, layer_flags=True): the destination decode
+    starts right away, layer by layer behind the copy, and equals decoding the
+    request where it was."""
+    from paper_2501_06709_b200.attention import paged_decode
+    from paper_2501_06709_b200.executor import MigrationExecutor
+    from paper_2501_06709_b200.planner import KV_TRANSFER, PendingMove, PlannedMove
+
+    shape = ModelShape("lf", layers=6, kv_heads=2, head_dim=128, q_heads=8, d_model=1024)
+    pools = {0: KVPool(shape, 200, dtype=torch.bfloat16), 1: KVPool(shape, 200, dtype=torch.bfloat16)}
+    g = torch.Generator(device="cuda").manual_seed(4)
+    pools[0].tensor.copy_(torch.randn(pools[0].view_shape, generator=g, device="cuda").to(torch.bfloat16))
+    ex = MigrationExecutor(pools)
+    ex.admit(9, 0, 2500)
+    q = torch.randn(shape.layers, 1, 8, 128, generator=g, device="cuda").to(torch.bfloat16)
+    lens = torch.tensor([2500], dtype=torch.int32, device="cuda")
+    ref = paged_decode(pools[0], q, torch.from_numpy(ex.where(9).blocks)[None].contiguous().cuda(), lens)
+    torch.cuda.synchronize()
+    rep = ex.execute([PlannedMove(PendingMove(9, 0, 1, 2500 * shape.kv_bytes_per_token, 2500), KV_TRANSFER)],
+                     stream_ordered=True, layer_flags=True)
+    rec = rep.records[0]
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dec = torch.cuda.Stream()
+    out = paged_decode(pools[1], q, torch.from_numpy(ex.where(9).blocks)[None].contiguous().cuda(), lens,
+                       stream=dec, layer_flags=rec.layer_flags[9], timeout_ns=5_000_000_000, err_word=err)
+    torch.cuda.synchronize()
+    assert err.item() == 0 and rec.layer_flags[9].cpu().tolist() == [1] * shape.layers
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
