@@ -43,7 +43,9 @@
 extern "C" {
 #endif
 
-#define KVM_ABI_VERSION 1
+/* 2: kvm_decode_args gained the layer-wait fields (KVM_DECODE_WAIT_LAYERS);
+ *    kvm_pool_register_strided; KVM_F_SYS_SCOPE; KVM_REPREFILL_X_PER_LAYER. */
+#define KVM_ABI_VERSION 2
 
 #define KVM_OK 0
 #define KVM_ERR_INVALID (-1)     /* bad argument              -> ValueError   */

@@ -18,6 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KVM_LIB_PATH") or os.path.join(HERE, "_lib", "libkvmig.so")
 
 KVM_OK = 0
+ABI_VERSION = 2   # include/kvmig.h KVM_ABI_VERSION
 KVM_ERR_INVALID = -1
 KVM_ERR_CONFIG = -2
 KVM_ERR_CUDA = -3
@@ -193,6 +194,9 @@ def lib() -> ctypes.CDLL:
                     " (there is no CPU fallback for the KV data path)")
             L = ctypes.CDLL(LIB_PATH)
             _declare(L)
+            if L.kvm_version() != ABI_VERSION:   # struct layouts below must match the build
+                raise NativeLibraryMissing(
+                    f"{LIB_PATH} has ABI {L.kvm_version()}, this package needs {ABI_VERSION}: rebuild it")
             _lib = L
     return _lib
 

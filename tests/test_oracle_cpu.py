@@ -136,7 +136,48 @@ def test_abi_library_exports_every_header_symbol():
     assert set(syms) == set(_native.EXPORTS)
     for s in syms:
         assert hasattr(L, s), s
-    assert L.kvm_version() == 1
+    assert L.kvm_version() == _native.ABI_VERSION
+    with open(os.path.join(ROOT, "include", "kvmig.h")) as fh:
+        assert int(re.search(r"#define KVM_ABI_VERSION (\d+)", fh.read()).group(1)) == _native.ABI_VERSION
+
+
+_STRUCTS = {  # ctypes mirror -> C struct in include/kvmig.h
+    "PoolDesc": "kvm_pool_desc", "Move": "kvm_move", "ReprefillArgs": "kvm_reprefill_args",
+    "SplitArgs": "kvm_split_args", "DecodeArgs": "kvm_decode_args", "Pending": "kvm_pending",
+    "PlanParams": "kvm_plan_params", "Planned": "kvm_planned", "PlanLedgers": "kvm_plan_ledgers",
+    "SchedParams": "kvm_sched_params",
+}
+
+
+def test_abi_struct_layouts_match_the_c_compiler(tmp_path):
+    """Every ctypes mirror has the C compiler's size and field offsets for the
+    header's struct (gcc on include/kvmig.h)."""
+    import shutil
+    import subprocess
+
+    from paper_2501_06709_b200 import _native
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "kvmig.h"', "int main(void) {"]
+    for py, c in _STRUCTS.items():
+        lines.append(f'printf("{py} size %zu\\n", sizeof({c}));')
+        for name, _ in getattr(_native, py)._fields_:
+            lines.append(f'printf("{py} {name} %zu\\n", offsetof({c}, {name}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines():
+        py, field, val = line.split()
+        got[(py, field)] = int(val)
+    for py in _STRUCTS:
+        cls = getattr(_native, py)
+        assert got[(py, "size")] == ctypes.sizeof(cls), py
+        for name, _ in cls._fields_:
+            assert got[(py, name)] == getattr(cls, name).offset, (py, name)
 
 
 def test_abi_error_mapping_without_gpu():
