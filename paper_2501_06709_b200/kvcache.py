@@ -227,13 +227,18 @@ class BlockTable:
                                device=f"cuda:{device}")
         self._slot_of: Dict[int, int] = {}
         self._free_slots = list(range(max_requests - 1, -1, -1))
+        self._dirty: set = set()   # freed slots whose row still holds the old request's blocks
         self.host: Dict[int, np.ndarray] = {}
 
     def slot(self, rid: int) -> int:
         if rid not in self._slot_of:
             if not self._free_slots:
                 raise ConfigError("block table full")
-            self._slot_of[rid] = self._free_slots.pop()
+            s = self._free_slots.pop()
+            if s in self._dirty:   # cleared on reuse, not on release (keeps drop() off the pause path)
+                self._dirty.discard(s)
+                self.rows[s].fill_(-1)
+            self._slot_of[rid] = s
         return self._slot_of[rid]
 
     def row_ptr(self, rid: int) -> int:
@@ -248,8 +253,8 @@ class BlockTable:
     def drop(self, rid: int) -> None:
         self.host.pop(rid, None)
         s = self._slot_of.pop(rid, None)
-        if s is not None:
-            self.rows[s].fill_(-1)
+        if s is not None:   # nobody reads a released row; it is reset to -1 when the slot is reused
+            self._dirty.add(s)
             self._free_slots.append(s)
 
     def blocks(self, rid: int) -> np.ndarray:
