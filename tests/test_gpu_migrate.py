@@ -474,3 +474,16 @@ def test_executor_layer_flags_feed_a_pipelined_decode():
     torch.cuda.synchronize()
     assert err.item() == 0 and rec.layer_flags[9].cpu().tolist() == [1] * shape.layers
     assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+
+
+def test_block_table_released_rows_reset_on_reuse():
+    t = BlockTable(2, 8)
+    t.set_host(1, np.arange(6, dtype=np.int32))
+    t.rows[t.slot(1), :6] = torch.arange(6, dtype=torch.int32, device="cuda")
+    s = t.slot(1)
+    t.drop(1)                                   # no device work in the release
+    assert t.rows[s, :6].tolist() == list(range(6))
+    t.set_host(2, np.array([9, 8], dtype=np.int32))
+    t.set_host(3, np.array([7], dtype=np.int32))
+    assert {t.slot(2), t.slot(3)} == {0, 1}
+    assert t.rows[s].tolist() == [-1] * 8       # the reused slot was reset first
