@@ -6,6 +6,7 @@ full-size configs use size-independent properties (gathered src == gathered
 dst, everything else unchanged, via per-piece checksums on the device).
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -247,7 +248,7 @@ def test_executor_plan_roundtrip():
     assert rec.bytes_moved == 4 * 16 * bpt
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "12"))))
 def test_randomized_batches_vs_oracle(seed):
     """Random shapes (piece sizes from 1 KiB to 160 KiB, odd head counts), random
     pools and block lists, several moves of DIFFERENT shapes in one kvm_migrate
