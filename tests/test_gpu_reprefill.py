@@ -174,7 +174,9 @@ def _rope_ref(y, positions, theta, q_cols, kv_cols):
     ang = positions.to(torch.float64)[:, None] * theta ** (-2.0 * i / 128.0)
     c, s = torch.cos(ang).float(), torch.sin(ang).float()          # [rows, 64]
     for lo, hi in ((0, q_cols), (q_cols, q_cols + kv_cols)):
-        seg = y[:, :, lo:hi].reshape(y.shape[0], y.shape[1], -1, 128)
+        if hi <= lo:   # no Q columns
+            continue
+        seg = y[:, :, lo:hi].reshape(y.shape[0], y.shape[1], -1, 128).clone()   # (reshape may alias y)
         a, b = seg[..., :64].clone(), seg[..., 64:].clone()
         seg[..., :64] = a * c[None, :, None, :] - b * s[None, :, None, :]
         seg[..., 64:] = b * c[None, :, None, :] + a * s[None, :, None, :]
@@ -300,3 +302,41 @@ def test_reprefill_many_launches_on_two_streams():
             t = pools[i].tensor
             k_ = t[l, 0, blocks.long()[toks // 16], toks % 16].reshape(rows, kvd).float()
             torch.testing.assert_close(k_, ref[l, :, :kvd], atol=ATOL, rtol=RTOL)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "8"))))
+def test_reprefill_randomized(seed):
+    """Random geometry (layers, heads, head_dim, d_model, rows, tok0), Q on/off,
+    RoPE on/off, per-layer X on/off, either GEMM engine, scattered blocks:
+    every K/V slot and Q within tolerance of fp32, nothing else written."""
+    rng = np.random.default_rng(5000 + seed)
+    head_dim = int(rng.choice([64, 128]))
+    kv_heads = int(rng.integers(1, 5))
+    q_heads = kv_heads * int(rng.choice([1, 2, 4]))
+    layers = int(rng.integers(1, 4))
+    d_model = 64 * int(rng.integers(1, 9))
+    shape = ModelShape(f"fz{seed}", layers=layers, kv_heads=kv_heads, head_dim=head_dim, q_heads=q_heads,
+                       d_model=d_model)
+    rows, tok0 = int(rng.integers(1, 700)), int(rng.integers(0, 300))
+    with_q = bool(rng.integers(2))
+    rope = head_dim == 128 and bool(rng.integers(2))
+    per_layer = bool(rng.integers(2))
+    single = bool(rng.integers(2))
+    nblk = (tok0 + rows + 15) // 16
+    nb = nblk + int(rng.integers(1, 9))
+    pool = KVPool(shape, nb, dtype=torch.bfloat16)
+    pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    before = pool.tensor.view(torch.int16).clone()
+    blocks = torch.from_numpy(rng.permutation(nb)[:nblk].astype(np.int32)).cuda()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    xs = (layers, rows, d_model) if per_layer else (rows, d_model)
+    x = torch.randn(xs, generator=g, device="cuda").to(torch.bfloat16)
+    w = synthetic_weights(shape, 0, with_q=with_q, seed=seed + 1)
+    q = torch.zeros(layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda") if with_q else None
+    reprefill(pool, x, w, blocks, tok0=tok0, q_out=q, single_cta=single, rope_theta=10000.0 if rope else None)
+    torch.cuda.synchronize()
+    ref = torch.einsum("ltk,lnk->ltn" if per_layer else "tk,lnk->ltn", x.float(), w.float())
+    if rope:
+        ref = _rope_ref(ref, torch.arange(tok0, tok0 + rows, device="cuda"), 10000.0,
+                        shape.q_cols if with_q else 0, shape.kv_cols)
+    _check(shape, pool, blocks, tok0, rows, ref, q, before)
