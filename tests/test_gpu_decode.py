@@ -182,3 +182,49 @@ def test_decode_pipelined_behind_an_incoming_migration():
     torch.cuda.synchronize()
     assert err.item() == 0
     assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "8"))))
+def test_decode_randomized(seed):
+    """Random GQA ratio (1..8 query heads per kv head), batch, ragged lengths
+    (incl. empty requests), layer window, dtype and block scatter: within the
+    stated tolerance of the fp32 reference (tensor-core path; CUDA cores too
+    when the ratio is a power of two)."""
+    import numpy as np
+
+    rng = np.random.default_rng(9000 + seed)
+    kv_heads = int(rng.integers(1, 5))
+    G = int(rng.integers(1, 9))
+    layers = int(rng.integers(1, 4))
+    dtype = torch.float16 if rng.integers(2) else torch.bfloat16
+    batch = int(rng.integers(1, 5))
+    seqs = [int(rng.choice([0, 1, 15, 16, 17])) if rng.random() < 0.3 else int(rng.integers(1, 3000))
+            for _ in range(batch)]
+    if max(seqs) == 0:
+        seqs[0] = 5
+    shape = ModelShape(f"dz{seed}", layers=layers, kv_heads=kv_heads, head_dim=128, q_heads=kv_heads * G,
+                       d_model=128 * kv_heads * G)
+    maxb = max((s + 15) // 16 for s in seqs)
+    nb = sum((s + 15) // 16 for s in seqs) + int(rng.integers(1, 6))
+    pool = KVPool(shape, nb, dtype=dtype)
+    _fill_normal(pool, seed)
+    perm = rng.permutation(nb)
+    tables = torch.full((batch, maxb), -1, dtype=torch.int32)
+    off = 0
+    for b, s in enumerate(seqs):
+        k = (s + 15) // 16
+        tables[b, :k] = torch.from_numpy(perm[off:off + k].astype(np.int32))
+        off += k
+    tables = tables.cuda()
+    lens = torch.tensor(seqs, dtype=torch.int32, device="cuda")
+    l0 = int(rng.integers(0, layers))
+    nl = int(rng.integers(1, layers - l0 + 1))
+    q = torch.randn(nl, batch, kv_heads * G, 128, generator=torch.Generator(device="cuda").manual_seed(seed),
+                    device="cuda").to(dtype)
+    out = paged_decode(pool, q, tables, lens, layer0=l0, n_layers=nl)
+    ref = reference_decode(pool, q, tables, lens, layer0=l0)
+    ref[:, lens.cpu() == 0] = 0.0
+    torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
+    if G in (1, 2, 4, 8):
+        out_cc = paged_decode(pool, q, tables, lens, layer0=l0, n_layers=nl, cuda_cores=True)
+        torch.testing.assert_close(out_cc.float(), ref, atol=2e-2, rtol=2e-2)
