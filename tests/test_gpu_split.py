@@ -200,3 +200,57 @@ def test_split_migrated_cache_decodes_like_the_original(single_cta, per_layer):
     exp = src.tensor[:, :, sb.long()[toks // 16], toks % 16].view(torch.int16)
     assert torch.equal(got, exp)
     assert torch.equal(b.view(torch.int16), a.view(torch.int16))
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "6"))))
+def test_fused_split_randomized(seed):
+    """Random geometry, request length, split point (incl. all-transfer and
+    all-recompute), RoPE, GEMM engine and block scatter for kvm_split_migrate:
+    prefix blocks bit-exact, suffix token slots within tolerance, the table
+    row rewritten, nothing else in the destination pool written."""
+    from paper_2501_06709_b200.split import split_migrate_fused
+    from test_gpu_reprefill import ATOL, RTOL, _rope_ref
+
+    rng = np.random.default_rng(7000 + seed)
+    head_dim = int(rng.choice([64, 128]))
+    kv_heads = int(rng.integers(1, 4))
+    shape = ModelShape(f"sz{seed}", layers=int(rng.integers(1, 4)), kv_heads=kv_heads, head_dim=head_dim,
+                       q_heads=kv_heads * int(rng.choice([1, 2])), d_model=64 * int(rng.integers(1, 7)))
+    tokens = int(rng.integers(1, 1200))
+    prefix_blocks = int(rng.integers(0, tokens // 16 + 1))
+    plan = make_split(tokens, tokens - 16 * prefix_blocks)
+    rope = head_dim == 128 and bool(rng.integers(2))
+    nb = plan.total_blocks + int(rng.integers(1, 12))
+    src, dst = KVPool(shape, nb, dtype=torch.bfloat16), KVPool(shape, nb, dtype=torch.bfloat16)
+    src.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    dst.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
+    before = dst.tensor.view(torch.int16).clone()
+    sb = torch.from_numpy(rng.permutation(nb)[:plan.total_blocks].astype(np.int32)).cuda()
+    db = torch.from_numpy(rng.permutation(nb)[:plan.total_blocks].astype(np.int32)).cuda()
+    x = synthetic_hidden(shape, max(plan.suffix, 1), 0, seed=seed)[:plan.suffix].contiguous()
+    w = synthetic_weights(shape, 0, with_q=True, seed=seed + 1)
+    table = BlockTable(1, plan.total_blocks + 1)
+    split_migrate_fused(src, dst, sb, db, plan, x if plan.suffix else None, w, table_row=table.row_ptr(0),
+                        single_cta=bool(rng.integers(2)), rope_theta=10000.0 if rope else 0.0)
+    torch.cuda.synchronize()
+    got = dst.tensor.view(torch.int16)
+    pre = plan.prefix_blocks
+    if pre:
+        assert torch.equal(got[:, :, db[:pre].long()], src.tensor.view(torch.int16)[:, :, sb[:pre].long()])
+    assert np.array_equal(table.rows[0, :plan.total_blocks].cpu().numpy(), db.cpu().numpy())
+    mask = torch.ones(nb, 16, dtype=torch.bool, device="cuda")
+    mask[db[:pre].long()] = False
+    if plan.suffix:
+        toks = torch.arange(plan.prefix_tokens, tokens, device="cuda")
+        blk, slot = db.long()[toks // 16], toks % 16
+        mask[blk, slot] = False
+        ref = torch.einsum("tk,lnk->ltn", x.float(), w.float())
+        if rope:
+            ref = _rope_ref(ref, toks, 10000.0, shape.q_cols, shape.kv_cols)
+        kvd, qc = shape.kv_cols, shape.q_cols
+        for l in range(shape.layers):
+            torch.testing.assert_close(dst.tensor[l, 0, blk, slot].reshape(plan.suffix, kvd).float(),
+                                       ref[l, :, qc:qc + kvd], atol=ATOL, rtol=RTOL)
+            torch.testing.assert_close(dst.tensor[l, 1, blk, slot].reshape(plan.suffix, kvd).float(),
+                                       ref[l, :, qc + kvd:], atol=ATOL, rtol=RTOL)
+    assert torch.equal(got[:, :, mask], before[:, :, mask])
