@@ -836,6 +836,9 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
       memcpy(p.blocks + P::kInlineBlocks, mv.dst_blocks, sizeof(int32_t) * mv.n_blocks);
       d.src_blocks = nullptr;   // marks the inline lists
       d.dst_blocks = nullptr;
+    } else if (on_host && mv.n_blocks == 0) {   // nothing staged (and maybe no slot at all)
+      d.src_blocks = nullptr;
+      d.dst_blocks = nullptr;
     } else if (on_host) {
       uint8_t* h = static_cast<uint8_t*>(slot->host) + off;
       memcpy(h, mv.src_blocks, sizeof(int32_t) * mv.n_blocks);

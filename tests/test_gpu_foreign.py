@@ -325,3 +325,63 @@ def test_fp8_vllm_cache_migrates_bit_exact(layout):
                 orig = fx.piece(l, kv, int(sb[i])).view(torch.uint8)
                 assert torch.equal(nat.tensor[l, kv, int(db[i])].view(torch.uint8), orig)
                 assert torch.equal(fx.piece(l, kv, 4 + i).view(torch.uint8), orig)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "6"))))
+def test_foreign_layouts_randomized(seed):
+    """Random layouts on both sides (native / FlashAttention / FlashInfer),
+    random geometry, one to three moves per launch, host or device lists,
+    either engine: every destination piece equals its source piece and nothing
+    else changes."""
+    rng = np.random.default_rng(11000 + seed)
+    shape = ModelShape(f"fr{seed}", layers=int(rng.integers(1, 4)), kv_heads=int(rng.integers(1, 6)),
+                       head_dim=int(rng.choice([8, 64, 128])), q_heads=1, d_model=64)
+    kinds = ["native", "flash_attn", "flashinfer"]
+
+    def make(kind, nb, sd):
+        if kind == "native":
+            p = KVPool(shape, nb)
+            p.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1,
+                                              generator=torch.Generator(device="cuda").manual_seed(sd))
+            return p, None
+        g = torch.Generator(device="cuda").manual_seed(sd)
+        caches = [torch.randint(-2 ** 15, 2 ** 15, vllm_cache_shape(kind, nb, 16, shape.kv_heads, shape.head_dim),
+                                generator=g, device="cuda", dtype=torch.int16).view(torch.float16)
+                  for _ in range(shape.layers)]
+        return StridedKVPool.from_vllm(caches, kind, name=shape.name), caches
+
+    def snap(pool):
+        return torch.stack([torch.stack([torch.stack([_piece(pool, l, kv, b).reshape(-1).view(torch.int16)
+                                                      for b in range(pool.num_blocks)]) for kv in range(2)])
+                            for l in range(shape.layers)]).cpu()
+
+    nb = int(rng.integers(8, 40))
+    src, _k1 = make(kinds[int(rng.integers(3))], nb, seed)
+    dst, _k2 = make(kinds[int(rng.integers(3))], nb, seed + 1)
+    bs, bd = snap(src), snap(dst)
+    exp = bd.clone()
+    free = list(rng.permutation(nb))
+    moves, keep = [], []
+    host = bool(rng.integers(2))
+    for _ in range(int(rng.integers(1, 4))):
+        n = int(rng.integers(0, min(6, len(free)) + 1))
+        sbn = rng.permutation(nb)[:n].astype(np.int32)
+        dbn = np.array([free.pop() for _ in range(n)], dtype=np.int32)
+        exp[:, :, torch.from_numpy(dbn).long()] = bs[:, :, torch.from_numpy(sbn).long()]
+        m = _native.Move()
+        m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, n, 1
+        if host:
+            keep += [sbn, dbn]
+            m.src_blocks, m.dst_blocks = sbn.ctypes.data, dbn.ctypes.data
+        else:
+            ts, td = torch.from_numpy(sbn).cuda(), torch.from_numpy(dbn).cuda()
+            keep += [ts, td]
+            m.src_blocks, m.dst_blocks = ts.data_ptr(), td.data_ptr()
+        moves.append(m)
+    arr = (_native.Move * len(moves))(*moves)
+    flags = (_native.KVM_F_BLOCKS_ON_HOST if host else 0) | (_native.KVM_F_ENGINE_BULK if rng.integers(2) else 0)
+    _native.check(_native.lib().kvm_migrate(arr, len(moves), flags,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(snap(dst), exp)
+    assert torch.equal(snap(src), bs)

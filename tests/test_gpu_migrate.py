@@ -488,3 +488,18 @@ def test_block_table_released_rows_reset_on_reuse():
     t.set_host(3, np.array([7], dtype=np.int32))
     assert {t.slot(2), t.slot(3)} == {0, 1}
     assert t.rows[s].tolist() == [-1] * 8       # the reused slot was reset first
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+def test_batches_of_empty_moves_without_consumers(engine):
+    """Found by the foreign-layout fuzz: a launch whose moves are all empty and
+    have no table row / flags needs no staging slot at all (it used to
+    dereference the missing slot)."""
+    a, b = KVPool(SMALL, 8), KVPool(SMALL, 8)
+    e = np.zeros(0, dtype=np.int32)
+    for n in (1, 2, 5):
+        _run([_move(a, b, e, e) for _ in range(n)], _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine])
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _run([_move(a, b, e, e), _move(a, b, e, e, flag=flag.data_ptr(), value=3)],
+         _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine])
+    assert flag.item() == 3
