@@ -503,3 +503,36 @@ def test_batches_of_empty_moves_without_consumers(engine):
     _run([_move(a, b, e, e), _move(a, b, e, e, flag=flag.data_ptr(), value=3)],
          _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine])
     assert flag.item() == 3
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "12"))))
+def test_same_pool_batches_randomized(seed):
+    """Random same-pool batches (compaction-like): a batch with a write-write or
+    read-write block conflict is rejected with nothing moved; a conflict-free
+    batch equals the oracle."""
+    rng = np.random.default_rng(3000 + seed)
+    nb = int(rng.integers(6, 30))
+    pool = KVPool(SMALL, nb)
+    _fill(pool, seed)
+    before = pool.tensor.view(torch.int16).cpu().numpy()
+    moves, keep, writes, reads = [], [], [], []
+    for _ in range(int(rng.integers(1, 5))):
+        n = int(rng.integers(0, 5))
+        sb = rng.integers(0, nb, n).astype(np.int32)
+        db = rng.integers(0, nb, n).astype(np.int32)
+        keep += [sb, db]
+        reads += sb.tolist()
+        writes += db.tolist()
+        moves.append(_move(pool, pool, sb, db))
+    conflict = len(set(writes)) != len(writes) or bool(set(writes) & set(reads))
+    flags = _native.KVM_F_BLOCKS_ON_HOST | (_native.KVM_F_ENGINE_BULK if rng.integers(2) else 0)
+    if conflict:
+        with pytest.raises(ValueError):
+            _run(moves, flags)
+        assert np.array_equal(pool.tensor.view(torch.int16).cpu().numpy(), before)
+    else:
+        exp = before.copy()
+        for k in range(0, len(keep), 2):
+            orc.migrate(before, _desc(pool), exp, _desc(pool), keep[k], keep[k + 1])
+        _run(moves, flags)
+        assert np.array_equal(pool.tensor.view(torch.int16).cpu().numpy(), exp)
