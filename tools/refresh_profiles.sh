@@ -24,6 +24,8 @@ done
 run split 600 python tools/bench_split.py
 run issue 600 python tools/bench_issue.py
 run foreign 600 python tools/bench_foreign.py
+run pipelined_decode 600 python tools/bench_pipelined_decode.py
+run split_power 600 python tools/probe_split_power.py
 run live 600 python tools/bench_live.py
 for a in "" "--layers 1" "--shape llama3-70b-gqa --seq 16384" "--shape llama3-70b-gqa --seq 16384 --layers 1" \
          "--shape llama2-13b --seq 8192" "--batch 8 --layers 4"; do
