@@ -184,7 +184,7 @@ def test_decode_pipelined_behind_an_incoming_migration():
     assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "8"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "100"))))
 def test_decode_randomized(seed):
     """Random GQA ratio (1..8 query heads per kv head), batch, ragged lengths
     (incl. empty requests), layer window, dtype and block scatter: within the

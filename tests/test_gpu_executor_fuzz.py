@@ -34,7 +34,7 @@ def _check(ex, fp, pools, tables):
         assert p.allocator.num_blocks - p.allocator.n_free == used, g
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "4"))))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "30"))))
 def test_executor_random_operations(seed):
     rng = np.random.default_rng(20000 + seed)
     pools = {g: KVPool(SHAPE, 1000) for g in range(3)}   # never full: every refusal would be a bug

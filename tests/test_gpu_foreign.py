@@ -327,7 +327,7 @@ def test_fp8_vllm_cache_migrates_bit_exact(layout):
                 assert torch.equal(fx.piece(l, kv, 4 + i).view(torch.uint8), orig)
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "6"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "100"))))
 def test_foreign_layouts_randomized(seed):
     """Random layouts on both sides (native / FlashAttention / FlashInfer),
     random geometry, one to three moves per launch, host or device lists,

@@ -248,7 +248,7 @@ def test_executor_plan_roundtrip():
     assert rec.bytes_moved == 4 * 16 * bpt
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "12"))))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "100"))))
 def test_randomized_batches_vs_oracle(seed):
     """Random shapes (piece sizes from 1 KiB to 160 KiB, odd head counts), random
     pools and block lists, several moves of DIFFERENT shapes in one kvm_migrate
@@ -505,7 +505,7 @@ def test_batches_of_empty_moves_without_consumers(engine):
     assert flag.item() == 3
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "12"))))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVM_FUZZ_SEEDS", "100"))))
 def test_same_pool_batches_randomized(seed):
     """Random same-pool batches (compaction-like): a batch with a write-write or
     read-write block conflict is rejected with nothing moved; a conflict-free

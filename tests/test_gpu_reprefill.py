@@ -304,7 +304,7 @@ def test_reprefill_many_launches_on_two_streams():
             torch.testing.assert_close(k_, ref[l, :, :kvd], atol=ATOL, rtol=RTOL)
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "8"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "100"))))
 def test_reprefill_randomized(seed):
     """Random geometry (layers, heads, head_dim, d_model, rows, tok0), Q on/off,
     RoPE on/off, per-layer X on/off, either GEMM engine, scattered blocks:

@@ -202,7 +202,7 @@ def test_split_migrated_cache_decodes_like_the_original(single_cta, per_layer):
     assert torch.equal(b.view(torch.int16), a.view(torch.int16))
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "6"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "50"))))
 def test_fused_split_randomized(seed):
     """Random geometry, request length, split point (incl. all-transfer and
     all-recompute), RoPE, GEMM engine and block scatter for kvm_split_migrate:
