@@ -37,4 +37,5 @@ def test_c_host_migration(tmp_path):
     exe = _build(tmp_path)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "bit-exact" in out.stdout
+    assert "migration: 5 blocks" in out.stdout and "foreign layout: 3 blocks" in out.stdout
+    assert "MISMATCH" not in out.stdout and out.stdout.count("bit-exact") == 2

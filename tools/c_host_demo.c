@@ -116,10 +116,58 @@ static int migration_demo(void) {
   return bad;
 }
 
+/* A vLLM-style per-layer cache (FlashAttention layout [2][blocks][16][H][D], one
+ * allocation per layer) registered in place; a request moves into it from a
+ * native pool with kvm_migrate. */
+static int foreign_demo(void) {
+  int ndev = 0;
+  if (kvm_device_count(&ndev) < 0 || ndev == 0) return 0;
+  kvm_pool_desc d = {4, 8, 128, 16, 32, 2};
+  int64_t bytes = 0, piece = (int64_t)16 * 8 * 128 * 2, layer_bytes = 2 * 32 * piece;
+  check(kvm_pool_bytes(&d, &bytes), "kvm_pool_bytes");
+  uint16_t* host = (uint16_t*)malloc((size_t)bytes);
+  for (int64_t i = 0; i < bytes / 2; ++i) host[i] = (uint16_t)(i * 40503u + 17);
+  void* native = NULL;
+  void* layers[4] = {NULL, NULL, NULL, NULL};
+  if (cudaMalloc(&native, (size_t)bytes) != 0) return 1;
+  cudaMemcpy(native, host, (size_t)bytes, H2D);
+  for (int l = 0; l < 4; ++l)
+    if (cudaMalloc(&layers[l], (size_t)layer_bytes) != 0) return 1;
+  int src = check(kvm_pool_register(0, native, &d), "kvm_pool_register");
+  int dst = check(kvm_pool_register_strided(0, &d, layers, 32 * piece, piece), "kvm_pool_register_strided");
+  int32_t sb[] = {9, 2, 31};
+  int32_t db[] = {4, 0, 17};
+  kvm_move m;
+  memset(&m, 0, sizeof(m));
+  m.src_pool = src;
+  m.dst_pool = dst;
+  m.n_blocks = 3;
+  m.src_blocks = sb;
+  m.dst_blocks = db;
+  check(kvm_migrate(&m, 1, KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK, NULL), "kvm_migrate");
+  cudaDeviceSynchronize();
+  uint8_t* got = (uint8_t*)malloc((size_t)piece);
+  int bad = 0;
+  for (int l = 0; l < 4; ++l)
+    for (int kv = 0; kv < 2; ++kv)
+      for (int b = 0; b < 3; ++b) {
+        cudaMemcpy(got, (char*)layers[l] + kv * 32 * piece + db[b] * piece, (size_t)piece, D2H);
+        bad |= memcmp(got, (char*)host + (2 * l + kv) * 32 * piece + sb[b] * piece, (size_t)piece) != 0;
+      }
+  kvm_pool_unregister(dst);
+  kvm_pool_unregister(src);
+  for (int l = 0; l < 4; ++l) cudaFree(layers[l]);
+  cudaFree(native);
+  free(host);
+  free(got);
+  printf("foreign layout: 3 blocks into a per-layer [2][blocks][16][H][D] cache, %s\n", bad ? "MISMATCH" : "bit-exact");
+  return bad;
+}
+
 int main(int argc, char** argv) {
   int cpu_only = argc > 1 && strcmp(argv[1], "--cpu-only") == 0;
   printf("libkvmig ABI %d\n", kvm_version());
   int rc = scheduler_demo();
-  if (!cpu_only) rc |= migration_demo();
+  if (!cpu_only) rc |= migration_demo() | foreign_demo();
   return rc;
 }
