@@ -9,15 +9,24 @@ A step = one migration of one request's full paged KV cache (every layer, K
 and V) on every rank.
   N = 1 : intra-GPU migration (compaction) of the request into fresh blocks of
           the same pool: HBM -> HBM, bound = HBM copy bandwidth.
-  N > 1 : one process per GPU (torchrun), ring i -> (i+1) mod N; each rank
-          pushes its request into the next rank's pool over NVLink (CUDA-IPC
-          mapped peer memory, stores issued by the kernel), weak scaling.
+  N > 1 : one process per GPU, ring i -> (i+1) mod N; each rank pushes its
+          request into the next rank's pool over NVLink (CUDA-IPC mapped peer
+          memory, stores issued by the kernel; dist.PeerLink), weak scaling.
+          Launched by torchrun, or — when WORLD_SIZE is unset — bench.py
+          re-launches itself under torch.distributed.run with N ranks, so a
+          plain `python bench.py --gpus N` measures N GPUs.  N larger than
+          the visible GPU count is an error unless --shared-gpu (test mode:
+          ranks share one GPU, no NVLink hop, labelled as such).
 `value` is payload GB/s (kv_bytes, sim.py:214 definition) over all ranks,
 device-timed with CUDA events, max over ranks; the roofline object counts the
-kernel's algorithmic traffic (read + write for HBM; bytes crossing the link
-for NVLink).  `e2e` is the same metric through the public API with host block
-lists (pinned staging + H2D inside the call) and a D2H read of the rewritten
-destination block-table row every step.
+kernel's algorithmic traffic (read + write for HBM; bytes leaving the GPU for
+NVLink) and, at N > 1, the NVLink bytes NVML saw cross the ports.  `e2e` is
+the same metric through the public API with host block lists (pinned staging
++ H2D inside the call) and a D2H read of the rewritten destination block-table
+row every step.  At N > 1 the same ring done the library way (NCCL
+batch_isend_irecv of the gathered request) is timed in the same run
+(`library`), and the 70B-GQA 16k-token ring (configs[3]) is measured beside
+the headline (`extra_workloads`).
 
 --impl reference: the reference has no data path (it deletes executed moves,
 sim.py:221-223), so its CPU implementation of the path is the oracle port
@@ -29,9 +38,12 @@ import argparse
 import ctypes
 import json
 import os
+import platform
+import random
+import socket
 import statistics
+import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -48,25 +60,31 @@ NVLINK_PEAK_GBS = 900.0        # nominal per direction per GPU
 NVLINK_MEASURED_GBS = 770.0    # B200_PROFILING.md: measured peer copy per direction
 
 
+def _peaks():
+    """(hbm GB/s, bf16 burst TF/s, bf16 sustained TF/s, source)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return (float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d["bf16_tflops_sustained"]),
+                "measured (MEASURED_PEAKS.json)")
+    except Exception:
+        return 6650.0, 2250.0, 2250.0, "fallback (B200_PROFILING.md / nominal dense bf16)"
+
+
 def _kernel_extras(device: int) -> dict:
     """Fresh measurements of the path's other kernels on the same box, reported
     beside the headline (not part of the timed region): K3 re-prefill on the
     CTA-pair tcgen05 kernel (configs[2]'s 13B suffix of 1 360 tokens, QKV, 40
-    layers) and K5 paged decode over a 7B 4k-token cache (32 layers), each with
-    its roofline fraction against MEASURED_PEAKS.json."""
+    layers) against the burst bf16 peak (a ~6 ms launch timed alone) with
+    cuBLAS on the same shape in the same session; K5 paged decode over a 7B
+    4k-token cache (32 layers); and the one-block move latency."""
     import torch
 
     from paper_2501_06709_b200.attention import paged_decode
     from paper_2501_06709_b200.kvcache import SHAPES, KVPool
     from paper_2501_06709_b200.reprefill import reprefill, reprefill_flops, synthetic_hidden, synthetic_weights
 
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            pk = json.load(fh)
-        tflops_peak, tsrc = float(pk["bf16_tflops_sustained"]), "measured (MEASURED_PEAKS.json bf16 sustained)"
-        hbm_peak = float(pk["hbm_gbs"])
-    except Exception:
-        tflops_peak, tsrc, hbm_peak = 2250.0, "fallback (nominal dense bf16)", 6650.0
+    hbm_peak, burst, sustained, psrc = _peaks()
     st = torch.cuda.Stream(device=device)
 
     def timed(fn, reps=5, iters=3):
@@ -92,12 +110,29 @@ def _kernel_extras(device: int) -> dict:
         pool = KVPool(sh, nblk + 4, device=device, dtype=torch.bfloat16)
         blocks = torch.arange(nblk, dtype=torch.int32, device=f"cuda:{device}")
         x, w = synthetic_hidden(sh, rows, device), synthetic_weights(sh, device, with_q=True)
-        ms = timed(lambda: reprefill(pool, x, w, blocks, stream=st))
-        tf = reprefill_flops(sh, rows, with_q=True) / ms / 1e9
-        out["reprefill_13b_s1360"] = {"kernel": "reprefill_pair_kernel (tcgen05 cta_group::2)", "ms": round(ms, 4),
-                                      "achieved": round(tf, 1), "peak": tflops_peak, "unit": "TFLOP/s",
-                                      "frac": round(tf / tflops_peak, 4), "peak_source": tsrc}
-        del pool, x, w
+        flops = reprefill_flops(sh, rows, with_q=True)
+        outs = torch.empty(rows, w.shape[1], dtype=torch.bfloat16, device=f"cuda:{device}")
+
+        def cublas():
+            for l in range(sh.layers):
+                torch.matmul(x, w[l].t(), out=outs)
+
+        # interleaved rounds: both arms see the same power / thermal state
+        ours_ms, lib_ms = [], []
+        for _ in range(3):
+            ours_ms.append(timed(lambda: reprefill(pool, x, w, blocks, stream=st), reps=3))
+            lib_ms.append(timed(cublas, reps=3))
+        ms, lms = statistics.median(ours_ms), statistics.median(lib_ms)
+        tf, ltf = flops / ms / 1e9, flops / lms / 1e9
+        out["reprefill_13b_s1360"] = {
+            "kernel": "reprefill_pair_kernel (tcgen05 cta_group::2)", "ms": round(ms, 4),
+            "achieved": round(tf, 1), "peak": burst, "unit": "TFLOP/s", "frac": round(tf / burst, 4),
+            "peak_source": psrc + " bf16 burst (kernel timed alone)",
+            "frac_vs_sustained": round(tf / sustained, 4),
+            "cublas_same_shape": {"impl": "torch.matmul per layer (cuBLAS), GEMM only, no K/V scatter",
+                                  "ms": round(lms, 4), "achieved": round(ltf, 1),
+                                  "frac": round(ltf / burst, 4), "ours_over_cublas": round(lms / ms, 4)}}
+        del pool, x, w, outs
     except Exception as e:  # reported, never fatal for the headline
         out["reprefill_13b_s1360"] = {"error": str(e)[:300]}
     try:
@@ -120,8 +155,6 @@ def _kernel_extras(device: int) -> dict:
     except Exception as e:
         out["decode_7b_4k_32l"] = {"error": str(e)[:300]}
     try:   # live-migration tail: one 7B block (8 MiB) with host block lists, table row + done flag
-        import ctypes
-
         import numpy as np
 
         from paper_2501_06709_b200 import _native
@@ -152,9 +185,10 @@ def _kernel_extras(device: int) -> dict:
         out["small_move_7b_1block"] = {"kernel": "migrate_bulk_kernel (one-move, 2-stage)",
                                        "issue_to_landed_us_p50": round(statistics.median(lat), 2),
                                        "bytes": sh.kv_bytes_per_token * 16,
-                                       "definition": "event before the kvm_migrate call -> event after it, stream "
-                                                     "idle: host issue (host block lists, table row, done flag) "
-                                                     "+ kernel"}
+                                       "definition": "the one small-move latency this repo quotes: CUDA event "
+                                                     "recorded on the idle stream right before the kvm_migrate "
+                                                     "call -> event right after it; covers host issue (host "
+                                                     "block lists, table row, done flag) + kernel"}
         del src, dst
     except Exception as e:
         out["small_move_7b_1block"] = {"error": str(e)[:300]}
@@ -162,65 +196,7 @@ def _kernel_extras(device: int) -> dict:
     return out
 
 
-def _peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md)"
-
-
-class ClockSampler:
-    """NVML sampling of SM clock + throttle reasons during the timed region."""
-
-    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
-            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
-
-    def __init__(self, device: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self._nv = None
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
-                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for bit, name in self.BITS.items():
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.005)
-
-    def __enter__(self):
-        if self._nv is not None:
-            self._t.start()
-        return self
-
-    def __exit__(self, *a):
-        self._stop.set()
-        if self._nv is not None:
-            self._t.join()
-
-    def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                    "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
-
-
-def _traffic_for(kernel: str, workload: str, engine: str):
+def _traffic_for(workload: str, engine: str):
     """dram read+write bytes per launch from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -232,8 +208,20 @@ def _traffic_for(kernel: str, workload: str, engine: str):
 
 
 # ----------------------------------------------------------------------------------
-# CPU baseline (oracle port) — only here and in --impl reference
+# CPU baselines — only here and in --impl reference (the checker and the
+# reference itself are never on the measured GPU path)
 # ----------------------------------------------------------------------------------
+def _cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
 def _cpu_setup(shape, tokens, seed=0):
     import numpy as np
 
@@ -274,6 +262,148 @@ def cpu_migrate_rate(shape, tokens, threads, budget_s=6.0, min_reps=2, max_reps=
     return kv_bytes, times
 
 
+def _reference_kvpack():
+    """The reference package for the control-plane baseline: baseline/_ref
+    (pip-installed from /root/reference, travels to the GPU box), else the
+    read-only source tree when mounted; None when neither exists."""
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "kvpack")):
+            if p not in sys.path:
+                sys.path.append(p)
+            try:
+                import kvpack
+
+                return kvpack, p
+            except Exception:
+                return None, None
+    return None, None
+
+
+def control_plane_baseline(budget_s: float = 8.0) -> dict:
+    """BASELINE.md CPU baseline 1: the reference's control plane (kvpack
+    plan_hybrid, migration.py:137-170, and MellScheduler.step_epoch,
+    scheduler.py:979-1007) timed on ONE core beside this repo's native
+    planner / scheduler on the same inputs; decisions checked identical."""
+    kp, where = _reference_kvpack()
+    out = {"cores": 1}
+    if kp is None:
+        out["reference"] = "unavailable (baseline/_ref not installed and /root/reference not mounted)"
+    else:
+        out["reference"] = f"kvpack from {os.path.relpath(where, ROOT) if where.startswith(ROOT) else where}"
+    from paper_2501_06709_b200 import cluster as ocl
+    from paper_2501_06709_b200 import scheduler as osch
+    from paper_2501_06709_b200.planner import PendingMove, Topology, load_boundaries, plan_hybrid_native
+    from paper_2501_06709_b200.runtime import run_slots
+    from paper_2501_06709_b200.workload import LengthDistribution, gen_poisson
+
+    old_aff = None
+    try:
+        old_aff = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {sorted(old_aff)[0]})   # this thread only: one core
+    except Exception:
+        pass
+    t_stop = time.perf_counter() + budget_s
+    try:
+        rng = random.Random(0)
+        topo = Topology(gpus_per_machine=8, intra_bandwidth_bytes_per_s=900e9)
+        bounds = load_boundaries(topo, 0.05, 0.2)
+        plans = {}
+        for n in (8, 64, 1024):
+            moves = [PendingMove(i, rng.randrange(16), rng.randrange(16), rng.randint(1, 4 * 10 ** 9),
+                                 rng.randint(1, 8000)) for i in range(n)]
+            defer = {i: rng.randint(0, 4) for i in range(0, n, 3)}
+            reps = max(3, 2000 // n)
+            row = {}
+            plan_hybrid_native(moves, bounds, topo, defer)   # warm (buffers sized)
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                ours = plan_hybrid_native(moves, bounds, topo, defer)
+            row["ours_native_us"] = round((time.perf_counter() - t0) / reps * 1e6, 2)
+            # the C ABI call alone on the marshalled buffers (what a C/C++ host pays)
+            from paper_2501_06709_b200 import planner as _pl
+
+            sc = _pl._scratch
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                sc.fn(sc.a_arr, n, sc.pp_addr, sc.a_out, sc.led_addr)
+            row["ours_c_abi_call_us"] = round((time.perf_counter() - t0) / reps * 1e6, 2)
+            if kp is not None:
+                rtopo = kp.Topology(gpus_per_machine=8, intra_bandwidth_bytes_per_s=900e9)
+                rb = kp.load_boundaries(rtopo, 0.05, 0.2)
+                rmoves = [kp.PendingMove(m.item, m.src, m.dst, m.kv_bytes, m.tokens) for m in moves]
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    ref = kp.plan_hybrid(rmoves, rb, rtopo, defer)
+                row["reference_us"] = round((time.perf_counter() - t0) / reps * 1e6, 2)
+                row["identical"] = [(a.move.item, a.mode, a.latency_s) for a in ours.assignments] == \
+                    [(a.move.item, a.mode, a.latency_s) for a in ref.assignments]
+            plans[n] = row
+        out["plan_hybrid"] = plans
+
+        class Timed:
+            def __init__(self, inner):
+                self.inner, self.times = inner, []
+
+            def step_epoch(self, *a, **k):
+                t = time.perf_counter()
+                r = self.inner.step_epoch(*a, **k)
+                self.times.append(time.perf_counter() - t)
+                return r
+
+        # SURVEY.md §8c B200-shaped 7B run: C = 48 GiB, 8 GPUs/machine, 900e9 B/s, lambda 0.5, scale 10
+        trace = gen_poisson(0.5, 200, LengthDistribution(scale=10), 0).tuples()
+        stopo = Topology(gpus_per_machine=8, intra_bandwidth_bytes_per_s=900e9,
+                         inter_bandwidth_bytes_per_s=50e9, prefill_tokens_per_s=50_000.0)
+        sb = load_boundaries(stopo, 0.05, 0.2)
+        arms = [("ours_native", ocl, osch)] + ([("reference", kp, kp)] if kp is not None else [])
+        sched = {}
+        rows = {}
+        for name, mc, ms in arms:
+            if time.perf_counter() > t_stop and name == "reference":
+                sched["reference"] = "skipped (budget)"
+                continue
+            cl = mc.ClusterState(48 << 30, gpus_per_machine=8)
+            s = Timed(ms.MellScheduler(cl, priority_cfg=ms.PriorityConfig(), batching=True))
+            res = run_slots(trace, s, cl, stopo, sb, bpt=524_288, tokens_per_slot=10, duration_slots=200)
+            t = sorted(s.times)
+            rows[name] = res.plan_rows
+            sched[name] = {"step_epoch_ms_mean": round(1e3 * statistics.fmean(t), 4),
+                           "step_epoch_ms_p50": round(1e3 * t[len(t) // 2], 4), "epochs": len(t),
+                           "peak_gpus": max(res.active_gpus)}
+        if "reference" in rows:
+            sched["identical_plan_rows"] = rows["reference"] == rows["ours_native"]
+        sched["workload"] = "gen_poisson(0.5, 200 slots, scale 10, seed 0), C 48 GiB, 7B bpt, 8 GPUs/machine"
+        out["step_epoch"] = sched
+    finally:
+        if old_aff is not None:
+            try:
+                os.sched_setaffinity(0, old_aff)
+            except Exception:
+                pass
+    return out
+
+
+def cpu_baseline(args, shape, tokens) -> dict:
+    threads = os.cpu_count() or 1
+    cb, times = cpu_migrate_rate(shape, tokens, threads, budget_s=args.cpu_budget_s)
+    # 1 thread on a bounded 2k-token sample of the same shape (BASELINE.md CPU baseline 2)
+    t1_tokens = min(tokens, 2048)
+    cb1, times1 = cpu_migrate_rate(shape, t1_tokens, 1, budget_s=min(4.0, args.cpu_budget_s / 2), min_reps=2)
+    out = {"value": round(cb * len(times) / sum(times) / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+           "sample": f"{len(times)} x {args.workload} migrations ({cb} B each, same workload) inside one host "
+                     f"pool, oracle C port (oracle/kvmig_oracle.c), {threads} pthreads, "
+                     f"~{args.cpu_budget_s:.0f} s budget",
+           "cpu_model": _cpu_model(), "os_cpu_count": os.cpu_count(),
+           "one_thread": {"value": round(cb1 * len(times1) / sum(times1) / 1e9, 3), "unit": "GB/s", "cores": 1,
+                          "sample": f"{len(times1)} x {t1_tokens}-token migrations of the same shape "
+                                    f"({cb1} B each), oracle C port, 1 thread"}}
+    try:
+        out["control_plane"] = control_plane_baseline()
+    except Exception as e:
+        out["control_plane"] = {"error": repr(e)[:300]}
+    return out
+
+
 def run_reference(args) -> int:
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
@@ -301,7 +431,7 @@ def run_reference(args) -> int:
         "latency_ms": {"p50": round(1e3 * statistics.median(times), 3),
                        "p99": round(1e3 * sorted(times)[max(0, int(0.99 * len(times)) - 1)], 3)},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": _cpu_model()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference kvpack moves no bytes (sim.py:221-223); its CPU path is the oracle port",
     }
@@ -340,311 +470,605 @@ def _layout(shape, tokens, seed):
     return n, nb, sb, used
 
 
-def run_ours(args) -> int:
+def _checksum(pool, blocks_np, n):
+    """Order-sensitive int64 checksum of the request's pieces (every layer, K
+    and V) gathered by `blocks_np`: equal sums <=> equal bytes in practice."""
+    import torch
+
+    shape = pool.shape
+    idx = torch.from_numpy(blocks_np).long().to(pool.tensor.device)
+    w = torch.arange(1, shape.piece_bytes // 2 + 1, device=idx.device, dtype=torch.int64)
+    acc = torch.zeros((), dtype=torch.int64, device=idx.device)
+    for l in range(shape.layers):
+        g = pool.tensor[l][:, idx].reshape(2, n, -1).view(torch.int16).to(torch.int64)
+        acc += (g * w).sum() + (g.sum(-1) * torch.arange(1, n + 1, device=idx.device)).sum()
+    return int(acc.item())
+
+
+def _pcts(xs):
+    s = sorted(xs)
+    return statistics.median(s), s[max(0, int(round(0.99 * len(s))) - 1)]
+
+
+class Ring:
+    """One workload on the ring i -> (i+1) mod N (N > 1): this rank's pool,
+    its request, the PeerLink to its neighbours, and the measurements."""
+
+    def __init__(self, ctx, workload: str):
+        import numpy as np
+        import torch
+
+        from paper_2501_06709_b200.dist import PeerLink
+        from paper_2501_06709_b200.kvcache import SHAPES, KVPool
+
+        self.ctx, self.workload = ctx, workload
+        ri, dev = ctx["ri"], ctx["device"]
+        shape_name, self.tokens, self.cfg_desc = WORKLOADS[workload]
+        self.shape = shape = SHAPES[shape_name]
+        self.kv_bytes = self.tokens * shape.kv_bytes_per_token
+        self.n, self.nb, self.sb_np, used = _layout(shape, self.tokens, seed=1 + ri.rank)
+        self.pool = KVPool(shape, self.nb, device=dev)
+        _fill_random(self.pool.tensor, 1234 + ri.rank)
+        self.pool.allocator.take(np.flatnonzero(used))
+        self.db_np = self.pool.allocator.alloc(self.n)          # blocks this rank RECEIVES into
+        self.link = PeerLink(self.pool, self.db_np, ri)
+        self.sb_dev = torch.from_numpy(self.sb_np).to(f"cuda:{dev}")
+        self.stream = torch.cuda.Stream(device=dev)
+        self.seq = 0
+        self.link.peer(ri.send_to)      # map the neighbour's pool now, not inside a timed region
+
+    def reset(self):
+        import torch
+
+        torch.cuda.synchronize()
+        self.ctx["barrier"]()
+        self.seq = 0
+        self.link.reset()
+        torch.cuda.synchronize()
+        self.ctx["barrier"]()
+
+    def step(self, engine: str, host: bool, ev=None):
+        """Push this rank's request to send_to, then make the incoming one (from
+        recv_from) a dependency of this rank's stream."""
+        ri, shared = self.ctx["ri"], self.ctx["shared"]
+        self.seq += 1
+        if ev is not None:
+            ev[0].record(self.stream)
+        self.link.push(ri.send_to, self.sb_np if host else self.sb_dev, self.seq, engine=engine,
+                       stream=self.stream)
+        if ev is not None:
+            ev[1].record(self.stream)
+        if shared:
+            # test mode, several ranks on ONE GPU: a device-side spin on the incoming flag can starve
+            # the peer process's context, so the receive completes on the host: own push done, then
+            # every rank has pushed
+            self.stream.synchronize()
+            self.ctx["barrier"]()
+        else:
+            self.link.wait(self.seq, self.stream)
+        if ev is not None:
+            ev[2].record(self.stream)
+
+    def gate(self, engine: str) -> bool:
+        """One migration, then bit-exact check: what this rank received equals
+        what recv_from sent, and the table row lists the receive blocks."""
+        import numpy as np
+        import torch
+
+        from paper_2501_06709_b200.dist import exchange_objects
+
+        ri = self.ctx["ri"]
+        sent = _checksum(self.pool, self.sb_np, self.n)
+        self.reset()
+        with torch.cuda.stream(self.stream):
+            self.step(engine, host=False)
+        self.stream.synchronize()
+        self.ctx["barrier"]()
+        self.link.check()
+        got = _checksum(self.pool, self.db_np, self.n)
+        sums = exchange_objects(sent)
+        row_ok = bool(np.array_equal(self.link.row[:self.n].cpu().numpy(), self.db_np))
+        ok = got == sums[ri.recv_from] and row_ok
+        if not ok:
+            print(f"rank {ri.rank}: parity gate failed ({engine}): received checksum {got}, sent "
+                  f"{sums[ri.recv_from]}, table row ok {row_ok}", file=sys.stderr)
+        return self.ctx["all_ok"](ok)
+
+    def timed(self, engine: str, K: int, W: int, meter=None, clocks=None) -> dict:
+        import torch
+
+        from paper_2501_06709_b200 import _native
+        from paper_2501_06709_b200.dist import allreduce_max
+
+        dev = self.ctx["device"]
+        self.reset()
+        with torch.cuda.stream(self.stream):
+            for _ in range(W):
+                self.step(engine, host=False)
+        self.stream.synchronize()
+        self.ctx["barrier"]()
+        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = _native.launch_count()
+        torch.cuda.synchronize()
+        self.ctx["barrier"]()
+        if meter is not None:
+            meter.start()
+        if clocks is not None:
+            clocks.__enter__()
+        with torch.cuda.stream(self.stream):
+            t0.record(self.stream)
+            for i in range(K):
+                self.step(engine, host=False, ev=ev[i])
+            t1.record(self.stream)
+        self.stream.synchronize()
+        torch.cuda.synchronize()
+        if clocks is not None:
+            clocks.__exit__()
+        if meter is not None:
+            meter.stop()
+        self.ctx["barrier"]()
+        self.link.check()
+        launches = _native.launch_count() - launches0
+        elapsed = allreduce_max(t0.elapsed_time(t1), dev)
+        push = [a.elapsed_time(b) for a, b, _ in ev]
+        stepms = [a.elapsed_time(c) for a, _, c in ev]
+        p50, p99 = _pcts(push)
+        s50, s99 = _pcts(stepms)
+        return {"elapsed_ms": elapsed, "push_ms_mean": allreduce_max(statistics.fmean(push), dev),
+                "push_p50": allreduce_max(p50, dev), "push_p99": allreduce_max(p99, dev),
+                "step_p50": allreduce_max(s50, dev), "step_p99": allreduce_max(s99, dev),
+                "launches": launches, "K": K,
+                "value": self.ctx["world"] * self.kv_bytes * K / (elapsed / 1e3) / 1e9}
+
+    def e2e(self, engine: str, K: int) -> dict:
+        """The same ring through the public API (dist.PeerLink) with host block
+        lists every step and a D2H of the rewritten block-table row."""
+        import torch
+
+        from paper_2501_06709_b200.dist import allreduce_max
+
+        dev = self.ctx["device"]
+        self.reset()
+        row = torch.empty(self.n, dtype=torch.int32, pin_memory=True)
+        torch.cuda.synchronize()
+        self.ctx["barrier"]()
+        lat = []
+        t0 = time.perf_counter()
+        for i in range(K):
+            ts = time.perf_counter()
+            with torch.cuda.stream(self.stream):
+                self.step(engine, host=True)
+                # D2H of the block-table row the incoming kernel rewrote, ordered after the wait
+                row.copy_(self.link.row[:self.n], non_blocking=True)
+            self.stream.synchronize()
+            lat.append(time.perf_counter() - ts)
+        torch.cuda.synchronize()
+        e2e_s = allreduce_max(time.perf_counter() - t0, dev)
+        self.ctx["barrier"]()
+        self.link.check()
+        ok = bool((row.numpy() == self.db_np).all())
+        return {"value": self.ctx["world"] * self.kv_bytes * K / e2e_s / 1e9, "h2d_bytes_per_step": 2 * self.n * 4,
+                "d2h_bytes_per_step": self.n * 4, "latency_ms_p50": 1e3 * allreduce_max(statistics.median(lat), dev),
+                "row_ok": self.ctx["all_ok"](ok)}
+
+    def library(self, K: int) -> dict:
+        """COMPARISON ONLY: the same ring exchange done the library way —
+        index_select gather, NCCL batch_isend_irecv (ncclSend/ncclRecv in one
+        group), index_copy_ scatter (dist.collective_ring_exchange)."""
+        import torch
+
+        from paper_2501_06709_b200.dist import allreduce_max, collective_ring_exchange, exchange_objects
+
+        ri, dev = self.ctx["ri"], self.ctx["device"]
+        t = self.pool.tensor
+        sbl = self.sb_dev.long()
+        dbl = torch.from_numpy(self.db_np).long().to(f"cuda:{dev}")
+        sent = _checksum(self.pool, self.sb_np, self.n)
+        self.reset()
+        collective_ring_exchange(t, sbl, dbl, ri)
+        torch.cuda.synchronize()
+        self.ctx["barrier"]()
+        got = _checksum(self.pool, self.db_np, self.n)
+        sums = exchange_objects(sent)
+        ok = self.ctx["all_ok"](got == sums[ri.recv_from])
+        collective_ring_exchange(t, sbl, dbl, ri)
+        torch.cuda.synchronize()
+        self.ctx["barrier"]()
+        cs = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        for _ in range(K):
+            collective_ring_exchange(t, sbl, dbl, ri)
+        e1.record(cs)
+        torch.cuda.synchronize()
+        ms = allreduce_max(e0.elapsed_time(e1), dev)
+        self.ctx["barrier"]()
+        return {"impl": "NCCL batch_isend_irecv ring (torch.distributed nccl) with index_select gather + "
+                        "index_copy_ scatter (dist.collective_ring_exchange)",
+                "value": round(self.ctx["world"] * self.kv_bytes * K / (ms / 1e3) / 1e9, 2), "unit": "GB/s",
+                "ms_per_step": round(ms / K, 4), "steps": K, "bit_exact": ok}
+
+    def close(self):
+        import torch
+
+        torch.cuda.synchronize()
+        self.ctx["barrier"]()
+        self.link.close()
+        self.ctx["barrier"]()     # no peer maps this pool any more
+        self.pool.close()
+        del self.pool
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+
+def _roofline_nvlink(kv_bytes: int, push_ms: float, engine: str, traffic) -> dict:
+    ach = kv_bytes / (push_ms / 1e3) / 1e9
+    return {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_GBS, "unit": "GB/s",
+            "frac": round(ach / NVLINK_MEASURED_GBS, 4),
+            "peak_source": "B200_PROFILING.md measured peer copy per direction per GPU",
+            "peak_nominal": NVLINK_PEAK_GBS, "frac_nominal": round(ach / NVLINK_PEAK_GBS, 4),
+            "kernel": "migrate_ldg_kernel" if engine == "ldg" else "migrate_bulk_kernel",
+            "algorithmic_bytes_per_launch": kv_bytes,
+            "definition": "kv_bytes leaving this GPU per launch / mean launch time (launch -> done flag "
+                          "release-stored to the peer after a system-scope fence), max over ranks",
+            "traffic": traffic}
+
+
+def run_ring(args, ctx) -> int:
+    """N > 1: the ring measurement, its evidence and extras."""
+    import torch
+
+    from paper_2501_06709_b200.dist import exchange_objects
+    from paper_2501_06709_b200.telemetry import ClockSampler, NvlinkMeter, merge_clocks
+
+    ri, world, dev, shared = ctx["ri"], ctx["world"], ctx["device"], ctx["shared"]
+    ring = Ring(ctx, args.workload)
+    engines = [args.engine] if args.engine else ["bulk", "ldg"]
+    gates = {e: ring.gate(e) for e in engines}
+    ab = {}
+    if len(engines) > 1:   # start-up A/B to the peer, behind the bit-exact gate: keep the faster engine
+        for e in engines:
+            if gates[e]:
+                r = ring.timed(e, K=5, W=3)
+                ab[e] = {"push_ms_mean": round(r["push_ms_mean"], 4), "bit_exact": True}
+            else:
+                ab[e] = {"bit_exact": False}
+        ok_eng = [e for e in engines if gates[e]]
+        engine = min(ok_eng, key=lambda e: ab[e]["push_ms_mean"]) if ok_eng else engines[0]
+    else:
+        engine = engines[0]
+    bit_exact = gates[engine]
+    meter = NvlinkMeter(dev)
+    clocks = ClockSampler(dev)
+    main = ring.timed(engine, args.steps, args.warmup, meter=meter, clocks=clocks)
+    nv = exchange_objects(meter.result())
+    clk = merge_clocks(exchange_objects(clocks.summary()))
+    e2e = ring.e2e(engine, args.steps)
+    lib = None
+    if not shared and not args.no_library:
+        try:
+            lib = ring.library(min(args.steps, 20))
+            lib["ours_over_library"] = round(main["value"] / lib["value"], 3)
+        except Exception as e:
+            lib = {"error": repr(e)[:300]}
+    elif shared:
+        lib = {"skipped": "ranks share one GPU (gloo control plane; NCCL needs one GPU per rank)"}
+    kv_bytes = ring.kv_bytes
+    n, nb = ring.n, ring.nb
+    cfg_desc = ring.cfg_desc
+    ring.close()
+    extras = {}
+    extra_list = [w for w in (args.extra_workloads or "").split(",") if w and w != args.workload]
+    for w in extra_list:
+        try:
+            r2 = Ring(ctx, w)
+            ok2 = r2.gate(engine)
+            m2 = r2.timed(engine, min(args.steps, 20), args.warmup)
+            extras[w] = {"config": WORKLOADS[w][2], "kv_bytes_per_rank_per_step": r2.kv_bytes,
+                         "value": round(m2["value"], 2), "unit": "GB/s", "ms_per_step": round(m2["elapsed_ms"] / m2["K"], 4),
+                         "steps": m2["K"], "bit_exact": ok2, "engine": engine,
+                         "latency_ms": {"p50": round(m2["push_p50"], 4), "p99": round(m2["push_p99"], 4)},
+                         "roofline": _roofline_nvlink(r2.kv_bytes, m2["push_ms_mean"], engine, None)
+                         if not shared else None}
+            r2.close()
+        except Exception as e:
+            extras[w] = {"error": repr(e)[:300]}
+    # NVLink bytes NVML saw (per rank), as roofline.traffic per launch
+    tx = [r.get("tx_bytes") for r in nv]
+    traffic = None
+    if all(t is not None for t in tx):
+        traffic = round(statistics.fmean(tx) / main["K"])
+    if shared:
+        hbm_peak, _, _, psrc = _peaks()
+        ach = 2 * kv_bytes / (main["push_ms_mean"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "peak_source": psrc + " hbm_gbs",
+                "kernel": "migrate_ldg_kernel" if engine == "ldg" else "migrate_bulk_kernel",
+                "algorithmic_bytes_per_launch": 2 * kv_bytes, "traffic": None,
+                "note": f"{world} ranks share {ctx['ndev']} GPU(s): IPC path exercised without NVLink"}
+    else:
+        roof = _roofline_nvlink(kv_bytes, main["push_ms_mean"], engine, traffic)
+    roof["nvlink_counters"] = {"per_rank": nv,
+                               "definition": "NVML NVLink TX/RX bytes over the timed region per rank; traffic = "
+                                             "mean TX bytes per launch (null when the box does not expose them)"}
+    line = None
+    if ri.rank == 0:
+        cpu = None if args.no_cpu_baseline else cpu_baseline(args, ring.shape, ring.tokens)
+        line = {
+            "metric": "kv_migration_GBps", "value": round(main["value"], 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(main["elapsed_ms"] / main["K"], 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
+            "data": "synthetic (seeded random KV bits, NaN payloads included)",
+            "config": {"workload": (f"{args.workload} ring push i->(i+1) mod {world} over NVLink (CUDA IPC)"
+                                    if not shared else
+                                    f"{args.workload} ring push i->(i+1) mod {world}, ranks sharing "
+                                    f"{ctx['ndev']} GPU (CUDA IPC test mode, no NVLink hop)"),
+                       "baseline_config": cfg_desc, "kv_bytes_per_rank_per_step": kv_bytes, "blocks": n,
+                       "pool_blocks": nb, "engine": engine, "engine_ab": ab or None,
+                       "l2": "inputs larger than L2 (%.1f GiB per step per rank)" % (kv_bytes / 2 ** 30),
+                       "parallelism": f"{world} ranks, one process per GPU" +
+                                      (f" ({ctx['ndev']} physical GPU, shared)" if shared else ""),
+                       "launcher": ctx["launcher"]},
+            "latency_ms": {"p50": round(main["push_p50"], 4), "p99": round(main["push_p99"], 4),
+                           "definition": "per step on each rank: event before the push launch -> event after the "
+                                         "push kernel, whose last CTA release-stores the done flag into the "
+                                         "destination (system scope) after the block-table row; max over ranks",
+                           "step_p50": round(main["step_p50"], 4), "step_p99": round(main["step_p99"], 4),
+                           "step_definition": "push + wait until the incoming move's done flag is visible here "
+                                              "(ld.acquire.sys)"},
+            "bit_exact": bool(bit_exact),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e["value"], 2), "unit": "GB/s", "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                    "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                    "latency_ms_p50": round(e2e["latency_ms_p50"], 4), "row_ok": e2e["row_ok"],
+                    "path": "dist.PeerLink.push(host block lists) -> PeerLink.wait(done flag) -> "
+                            "block-table row D2H -> host waits"},
+            "library": lib,
+            "extra_workloads": extras or None,
+            "gpu_launches": int(main["launches"]),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_compact(args, ctx) -> int:
+    """N = 1: intra-GPU migration (compaction) of the request, HBM -> HBM."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     from paper_2501_06709_b200 import _native
-    from paper_2501_06709_b200.dist import allreduce_max, exchange_objects, rank_info_from_env
     from paper_2501_06709_b200.executor import ENGINES, MigrationExecutor, Residency
     from paper_2501_06709_b200.kvcache import SHAPES, BlockTable, KVPool
+    from paper_2501_06709_b200.telemetry import ClockSampler
 
-    ri = rank_info_from_env()
-    world = ri.world
-    ndev = torch.cuda.device_count()
-    shared_gpu = world > 1 and ndev < world
-    device = ri.local_rank % max(ndev, 1)
-    torch.cuda.set_device(device)
-    if world > 1:
-        backend = "nccl" if ndev >= world else "gloo"   # gloo: N ranks sharing one GPU (test mode)
-        dist.init_process_group(backend=backend, device_id=torch.device(f"cuda:{device}")
-                                if backend == "nccl" else None)
+    device = ctx["device"]
+    engine = args.engine or "bulk"
     shape_name, tokens, cfg_desc = WORKLOADS[args.workload]
     shape = SHAPES[shape_name]
     kv_bytes = tokens * shape.kv_bytes_per_token
-    n, nb, sb_np, used = _layout(shape, tokens, seed=1 + ri.rank)
-    eng = ENGINES[args.engine] | (_native.KVM_F_L2_EVICT_FIRST if args.l2_evict_first else 0)
+    n, nb, sb_np, used = _layout(shape, tokens, seed=1)
+    eng = ENGINES[engine] | (_native.KVM_F_L2_EVICT_FIRST if args.l2_evict_first else 0)
     lib = _native.lib()
-
     pool = KVPool(shape, nb, device=device)
-    _fill_random(pool.tensor, 1234 + ri.rank)
+    _fill_random(pool.tensor, 1234)
     pool.allocator.take(np.flatnonzero(used))
-    db_np = pool.allocator.alloc(n)          # blocks this rank RECEIVES into
+    db_np = pool.allocator.alloc(n)
     table = BlockTable(4, n, device=device)
-    # one control allocation per rank, exported once: [0, 64) done flags, [64, 64 + n) the block-table
-    # row the incoming transfer rewrites (N > 1)
-    ctrl = torch.zeros(64 + n, dtype=torch.int32, device=f"cuda:{device}")
-    mailbox, rowbuf = ctrl[:64], ctrl[64:]
+    mailbox = torch.zeros(64, dtype=torch.int32, device=f"cuda:{device}")
     stream = torch.cuda.Stream(device=device)
     sptr = ctypes.c_void_p(stream.cuda_stream)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    # ---------------- peers ----------------
-    if world > 1:
-        h_pool, o_pool = pool.ipc_handle()
-        from paper_2501_06709_b200 import kvcache as kvc
-        hb = (ctypes.c_ubyte * 64)()
-        ob = ctypes.c_int64()
-        _native.check(lib.kvm_ipc_export(ctypes.c_void_p(ctrl.data_ptr()), hb, ctypes.byref(ob)))
-        info = exchange_objects((h_pool, o_pool, bytes(hb), ob.value, db_np.tolist()))
-        peer = info[ri.send_to]
-        dst_pool = kvc.KVPool.from_ipc(shape, nb, device, peer[0], peer[1])
-        mb = ctypes.c_void_p()
-        _native.check(lib.kvm_ipc_import(device, (ctypes.c_ubyte * 64).from_buffer_copy(peer[2]), peer[3],
-                                         ctypes.byref(mb)))
-        peer_flag, peer_row = mb.value, mb.value + 64 * 4
-        peer_db = np.asarray(peer[4], dtype=np.int32)
-    else:
-        dst_pool, peer_flag, peer_row, peer_db = pool, mailbox.data_ptr(), table.row_ptr(0), db_np
-
     sb_dev = torch.from_numpy(sb_np).to(f"cuda:{device}")
-    db_dev = torch.from_numpy(peer_db).to(f"cuda:{device}")
+    db_dev = torch.from_numpy(db_np).to(f"cuda:{device}")
     seq = [0]
 
-    def make_move(host: bool, fwd: bool):
+    def step(i):
         m = _native.Move()
-        m.src_pool, m.dst_pool, m.n_blocks = pool.pool_id, dst_pool.pool_id, n
-        if world == 1 and not fwd:       # compaction ping-pong: back into the original blocks
-            m.src_blocks = (db_np.ctypes.data if host else db_dev.data_ptr())
-            m.dst_blocks = (sb_np.ctypes.data if host else sb_dev.data_ptr())
-        else:
-            m.src_blocks = (sb_np.ctypes.data if host else sb_dev.data_ptr())
-            m.dst_blocks = (peer_db.ctypes.data if host else db_dev.data_ptr())
-        m.dst_table_row = peer_row
-        m.done_flag = peer_flag
+        m.src_pool, m.dst_pool, m.n_blocks = pool.pool_id, pool.pool_id, n
+        fwd = i % 2 == 0         # compaction ping-pong: forward into db, then back into the original blocks
+        m.src_blocks = sb_dev.data_ptr() if fwd else db_dev.data_ptr()
+        m.dst_blocks = db_dev.data_ptr() if fwd else sb_dev.data_ptr()
+        m.dst_table_row = table.row_ptr(0)
+        m.done_flag = mailbox.data_ptr()
         seq[0] += 1
         m.done_value = seq[0]
-        return m
+        _native.check(lib.kvm_migrate(ctypes.byref(m), 1, eng, sptr))
 
-    def step(i, host: bool):
-        m = make_move(host, fwd=(i % 2 == 0))
-        _native.check(lib.kvm_migrate(ctypes.byref(m), 1, eng | (_native.KVM_F_BLOCKS_ON_HOST if host else 0),
-                                      sptr))
-        if world > 1 and shared_gpu:
-            # test mode, several ranks on ONE GPU: a device-side spin on the incoming flag can starve
-            # the peer process's context (no time-slicing of a running kernel was observed), so the
-            # receive completes on the host: own push done, then every rank has pushed.
-            stream.synchronize()
-            barrier()
-        elif world > 1:   # wait for the incoming transfer from recv_from (dst-visible completion);
-            # bounded (30 s) so a lost peer write fails the run instead of wedging the GPU
-            _native.check(lib.kvm_wait_flag_timeout(ctypes.c_void_p(mailbox.data_ptr()), seq[0],
-                                                    30_000_000_000, ctypes.c_void_p(mailbox.data_ptr() + 4 * 63),
-                                                    sptr))
-
-    # ---------------- correctness gate (bit-exact) before timing ----------------
-    def gathered_checksum(blocks_np):
-        idx = torch.from_numpy(blocks_np).long().to(pool.tensor.device)
-        w = torch.arange(1, shape.piece_bytes // 2 + 1, device=idx.device, dtype=torch.int64)
-        acc = torch.zeros((), dtype=torch.int64, device=idx.device)
-        for l in range(shape.layers):
-            g = pool.tensor[l][:, idx].reshape(2, n, -1).view(torch.int16).to(torch.int64)
-            acc += (g * w).sum() + (g.sum(-1) * torch.arange(1, n + 1, device=idx.device)).sum()
-        return int(acc.item())
-
-    sent = gathered_checksum(sb_np)
-    # every rank's pool (and the blocks it receives into) is initialised before any peer pushes into it
+    sent = _checksum(pool, sb_np, n)
     torch.cuda.synchronize()
-    barrier()
     with torch.cuda.stream(stream):
-        step(0, host=False)
+        step(0)
     stream.synchronize()
-    barrier()
-    got = gathered_checksum(db_np)
-    if world == 1:
-        ok = got == sent
-    else:   # what this rank received must equal what recv_from sent
-        sums = exchange_objects(sent)
-        ok = got == sums[ri.recv_from] and bool(torch.equal(rowbuf.cpu(), torch.from_numpy(db_np)))
-    if world > 1 and int(mailbox[63].item()) != 0:
-        raise RuntimeError(f"rank {ri.rank}: incoming transfer from rank {ri.recv_from} timed out")
-    if not ok:
-        print(f"rank {ri.rank}: parity gate failed: received checksum {got}, sent "
-              f"{sums[ri.recv_from] if world > 1 else sent}, table row ok "
-              f"{bool(torch.equal(rowbuf.cpu(), torch.from_numpy(db_np))) if world > 1 else None}",
-              file=sys.stderr)
-    bit_exact = allreduce_max(0.0 if ok else 1.0, device) == 0.0
+    bit_exact = _checksum(pool, db_np, n) == sent and \
+        bool(np.array_equal(table.rows[0, :n].cpu().numpy(), db_np)) and int(mailbox[0].item()) == 1
     seq[0] = 0
-    mailbox.zero_()
-    torch.cuda.synchronize()
-    barrier()
-
-    # ---------------- warmup ----------------
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):   # sb and db now hold the same bytes: the ping-pong keeps them equal
         for i in range(args.warmup):
-            step(i, host=False)
+            step(i)
     stream.synchronize()
-    barrier()
-
-    # ---------------- timed: device-resident ----------------
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _native.launch_count()
     torch.cuda.synchronize()
-    barrier()
     with ClockSampler(device) as clk:
         with torch.cuda.stream(stream):
             t_start.record(stream)
             for i in range(K):
                 ev[i][0].record(stream)
-                step(args.warmup + i, host=False)
+                step(args.warmup + i)
                 ev[i][1].record(stream)
             t_end.record(stream)
         stream.synchronize()
         torch.cuda.synchronize()
-    barrier()
     launches = _native.launch_count() - launches0
-    elapsed_ms = allreduce_max(t_start.elapsed_time(t_end), device)
-    per = sorted(a.elapsed_time(b) for a, b in ev)
-    avg_launch_ms = sum(per) / len(per)
-    p50 = statistics.median(per)
-    p99 = per[max(0, int(round(0.99 * len(per))) - 1)]
-    p50 = allreduce_max(p50, device)
-    p99 = allreduce_max(p99, device)
-    avg_launch_ms = allreduce_max(avg_launch_ms, device)
-    value = world * kv_bytes * K / (elapsed_ms / 1e3) / 1e9
+    elapsed_ms = t_start.elapsed_time(t_end)
+    per = [a.elapsed_time(b) for a, b in ev]
+    avg_launch_ms = statistics.fmean(per)
+    p50, p99 = _pcts(per)
+    value = kv_bytes * K / (elapsed_ms / 1e3) / 1e9
 
-    # ---------------- timed: e2e through the public API ----------------
-    h2d = d2h = 0
-    if world == 1:
-        ex = MigrationExecutor({0: pool}, {0: table}, engine=args.engine)
-        pool.allocator.free(db_np)   # the request is resident in sb; db is free again
-        ex.loc[0] = Residency(0, sb_np.copy(), tokens, pool.shape.name)
-        table.set_host(0, sb_np)
-        # make device bytes consistent with the residency (content is irrelevant to timing)
-        rows = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        for i in range(args.warmup):
-            ex.compact(0, row_out=rows[0])
-        torch.cuda.synchronize()
-        e2e_lat = []
-        # every step: host block lists -> H2D -> kernel -> D2H of the rewritten block-table row,
-        # and the host waits for that row; the call is stream-ordered, so the host prepares step
-        # i+1 while the GPU still copies step i (double-buffered pinned rows)
-        t0 = time.perf_counter()
-        prev = None
-        e2e_ok = True
-        for i in range(K):
-            ts = time.perf_counter()
-            rec = ex.compact(0, row_out=rows[i & 1], stream_ordered=True)
-            if prev is not None:
-                prev[0].done.synchronize()
-                e2e_lat.append(time.perf_counter() - prev[1])
-                e2e_ok &= bool(np.array_equal(rows[(i - 1) & 1].numpy(), prev[2]))
-            prev = (rec, ts, ex.where(0).blocks.copy())
-        prev[0].done.synchronize()
-        e2e_lat.append(time.perf_counter() - prev[1])
-        e2e_s = time.perf_counter() - t0
-        torch.cuda.synchronize()
-        h2d, d2h = 2 * n * 4, n * 4
-        assert e2e_ok and np.array_equal(rows[(K - 1) & 1].numpy(), ex.where(0).blocks)
-        # per-call latency of one synchronous call (issue -> row on the host), not pipelined
-        e2e_lat = []
-        for i in range(min(K, 30)):
-            ts = time.perf_counter()
-            ex.compact(0, row_out=rows[0])
-            e2e_lat.append(time.perf_counter() - ts)
-    else:
-        row = torch.empty(n, dtype=torch.int32, pin_memory=True)
-        torch.cuda.synchronize()
-        barrier()
-        e2e_lat = []
-        t0 = time.perf_counter()
-        for i in range(K):
-            ts = time.perf_counter()
-            with torch.cuda.stream(stream):
-                step(i, host=True)
-                # D2H of the block-table row the incoming kernel rewrote, ordered after the wait
-                row.copy_(rowbuf[:n], non_blocking=True)
-            stream.synchronize()
-            e2e_lat.append(time.perf_counter() - ts)
-        torch.cuda.synchronize()
-        e2e_s = allreduce_max(time.perf_counter() - t0, device)
-        barrier()
-        h2d, d2h = 2 * n * 4, n * 4
-    e2e = world * kv_bytes * K / e2e_s / 1e9
+    # ---------------- e2e through the public API ----------------
+    ex = MigrationExecutor({0: pool}, {0: table}, engine=engine)
+    pool.allocator.free(db_np)   # the request is resident in sb; db is free again
+    ex.loc[0] = Residency(0, sb_np.copy(), tokens, pool.shape.name)
+    table.set_host(0, sb_np)
+    rows = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    for i in range(args.warmup):
+        ex.compact(0, row_out=rows[0])
+    torch.cuda.synchronize()
+    # every step: host block lists -> H2D -> kernel -> D2H of the rewritten block-table row, and the
+    # host waits for that row; the call is stream-ordered, so the host prepares step i+1 while the
+    # GPU still copies step i (double-buffered pinned rows)
+    t0 = time.perf_counter()
+    prev = None
+    e2e_ok = True
+    for i in range(K):
+        ts = time.perf_counter()
+        rec = ex.compact(0, row_out=rows[i & 1], stream_ordered=True)
+        if prev is not None:
+            prev[0].done.synchronize()
+            e2e_ok &= bool(np.array_equal(rows[(i - 1) & 1].numpy(), prev[2]))
+        prev = (rec, ts, ex.where(0).blocks.copy())
+    prev[0].done.synchronize()
+    e2e_s = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    e2e_ok &= bool(np.array_equal(rows[(K - 1) & 1].numpy(), ex.where(0).blocks))
+    # content check after the e2e loop: the request's bytes are still the ones it started with
+    e2e_ok &= _checksum(pool, ex.where(0).blocks, n) == sent
+    e2e_lat = []
+    for i in range(min(K, 30)):   # per-call latency of one synchronous call (issue -> row on the host)
+        ts = time.perf_counter()
+        ex.compact(0, row_out=rows[0])
+        e2e_lat.append(time.perf_counter() - ts)
+    e2e = kv_bytes * K / e2e_s / 1e9
 
-    # ---------------- roofline ----------------
-    hbm_peak, hbm_src = _peaks()
-    if world == 1:
-        alg_bytes = 2 * kv_bytes  # read + write, same HBM
-        roof = {"bound": "hbm", "achieved": round(alg_bytes / (avg_launch_ms / 1e3) / 1e9, 1),
-                "peak": hbm_peak, "unit": "GB/s", "peak_source": hbm_src,
-                "kernel": "migrate_ldg_kernel" if args.engine == "ldg" else "migrate_bulk_kernel",
-                "algorithmic_bytes_per_launch": alg_bytes,
-                "traffic": _traffic_for("migrate", args.workload, args.engine)}
-    elif ndev < world:
-        # test mode: ranks share one GPU, so the "peer" stores stay in local HBM
-        alg_bytes = 2 * kv_bytes
-        roof = {"bound": "hbm", "achieved": round(alg_bytes / (avg_launch_ms / 1e3) / 1e9, 1),
-                "peak": hbm_peak, "unit": "GB/s", "peak_source": hbm_src,
-                "kernel": "migrate_ldg_kernel" if args.engine == "ldg" else "migrate_bulk_kernel",
-                "algorithmic_bytes_per_launch": alg_bytes, "traffic": None,
-                "note": f"{world} ranks share {ndev} GPU(s): IPC path exercised without NVLink"}
-    else:
-        alg_bytes = kv_bytes  # bytes crossing this GPU's NVLink egress per launch
-        roof = {"bound": "nvlink", "achieved": round(alg_bytes / (avg_launch_ms / 1e3) / 1e9, 1),
-                "peak": NVLINK_MEASURED_GBS, "unit": "GB/s",
-                "peak_source": "B200_PROFILING.md measured peer copy per direction (nominal 900)",
-                "kernel": "migrate_ldg_kernel" if args.engine == "ldg" else "migrate_bulk_kernel",
-                "algorithmic_bytes_per_launch": alg_bytes, "traffic": None}
-    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    hbm_peak, _, _, psrc = _peaks()
+    alg_bytes = 2 * kv_bytes  # read + write, same HBM
+    ach = alg_bytes / (avg_launch_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(ach / hbm_peak, 4), "peak_source": psrc + " hbm_gbs",
+            "kernel": "migrate_ldg_kernel" if engine == "ldg" else "migrate_bulk_kernel",
+            "algorithmic_bytes_per_launch": alg_bytes, "traffic": _traffic_for(args.workload, engine)}
+    cpu = None if args.no_cpu_baseline else cpu_baseline(args, shape, tokens)
+    line = {
+        "metric": "kv_migration_GBps", "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(elapsed_ms / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
+        "data": "synthetic (seeded random KV bits, NaN payloads included)",
+        "config": {"workload": f"{args.workload} intra-GPU migration (compaction into fresh blocks of the same pool)",
+                   "baseline_config": cfg_desc, "kv_bytes_per_rank_per_step": kv_bytes, "blocks": n,
+                   "pool_blocks": nb, "engine": engine, "l2_evict_first": bool(args.l2_evict_first),
+                   "l2": "inputs larger than L2 (%.1f GiB per step)" % (kv_bytes / 2 ** 30),
+                   "parallelism": "1 GPU", "launcher": ctx["launcher"]},
+        "latency_ms": {"p50": round(p50, 4), "p99": round(p99, 4),
+                       "definition": "kernel launch -> done flag on dst stream (CUDA events)"},
+        "bit_exact": bool(bit_exact and e2e_ok),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": 2 * n * 4, "d2h_bytes_per_step": n * 4,
+                "latency_ms_p50": round(1e3 * statistics.median(e2e_lat), 4),
+                "latency_definition": "one synchronous call through the API: issue -> result row on the host",
+                "path": "MigrationExecutor.compact(stream_ordered) -> kvm_compact(host block lists) -> "
+                        "table row D2H -> host waits for the row (next step issued meanwhile)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_extras:
+        line["kernels"] = _kernel_extras(device)
+    print(json.dumps(line), flush=True)
+    return 0
 
-    line = None
-    if ri.rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            threads = os.cpu_count() or 1
-            cb, times = cpu_migrate_rate(shape, tokens, threads, budget_s=args.cpu_budget_s)
-            cpu = {"value": round(cb * len(times) / sum(times) / 1e9, 3), "unit": "GB/s", "cores": threads,
-                   "kind": "port",
-                   "sample": f"{len(times)} x {args.workload} migrations ({cb} B each, same workload) inside "
-                             f"one host pool, oracle C port (oracle/kvmig_oracle.c), {threads} pthreads, "
-                             f"~{args.cpu_budget_s:.0f} s budget"}
-        line = {
-            "metric": "kv_migration_GBps", "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
-            "steps": K, "warmup": args.warmup, "ms_per_step": round(elapsed_ms / K, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
-            "data": "synthetic (seeded random KV bits, NaN payloads included)",
-            "config": {"workload": (f"{args.workload} intra-GPU migration (compaction into fresh blocks of the "
-                                    f"same pool)" if world == 1 else
-                                    (f"{args.workload} ring push i->(i+1) mod {world} over NVLink (CUDA IPC)"
-                                     if ndev >= world else
-                                     f"{args.workload} ring push i->(i+1) mod {world}, ranks sharing "
-                                     f"{ndev} GPU (CUDA IPC test mode, no NVLink hop)")),
-                       "baseline_config": cfg_desc, "kv_bytes_per_rank_per_step": kv_bytes, "blocks": n,
-                       "pool_blocks": nb, "engine": args.engine, "l2_evict_first": bool(args.l2_evict_first),
-                       "l2": "inputs larger than L2 (%.1f GiB per step per rank)" % (kv_bytes / 2 ** 30),
-                       "parallelism": f"{world} ranks, one process per GPU" if world > 1 else "1 GPU"},
-            "latency_ms": {"p50": round(p50, 4), "p99": round(p99, 4),
-                           "definition": "kernel launch -> done flag on dst stream (CUDA events)"},
-            "bit_exact": bool(bit_exact),
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "latency_ms_p50": round(1e3 * statistics.median(e2e_lat), 4),
-                    "latency_definition": "one synchronous call through the API: issue -> result row on the host",
-                    "path": "MigrationExecutor.compact(stream_ordered) -> kvm_compact(host block lists) -> "
-                            "table row D2H -> host waits for the row (next step issued meanwhile)"
-                    if world == 1 else "kvm_migrate(host block lists) -> kvm_wait_flag -> table row D2H"},
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-        }
-        if world == 1 and not args.no_extras:
-            line["kernels"] = _kernel_extras(device)
-        print(json.dumps(line), flush=True)
+
+def run_ours(args) -> int:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_06709_b200.dist import allreduce_max, rank_info_from_env
+
+    ri = rank_info_from_env()
+    world = ri.world
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        print("bench.py: no CUDA device visible (the GPU arm has no CPU fallback)", file=sys.stderr)
+        return 3
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    shared = world > 1 and ndev < world
+    if shared and not args.shared_gpu:
+        print(f"bench.py: --gpus {world} needs {world} visible GPUs, found {ndev} (pass --shared-gpu to run the "
+              f"ranks on shared GPUs as a functional test; no NVLink is measured then)", file=sys.stderr)
+        return 2
+    device = ri.local_rank % ndev
+    torch.cuda.set_device(device)
+    ctx = {"ri": ri, "world": world, "device": device, "ndev": ndev, "shared": shared,
+           "launcher": os.environ.get("KVM_BENCH_LAUNCHER", "torchrun" if world > 1 else "python")}
     if world > 1:
+        backend = "gloo" if shared else "nccl"   # gloo: N ranks sharing one GPU (test mode)
+        dist.init_process_group(backend=backend, device_id=torch.device(f"cuda:{device}")
+                                if backend == "nccl" else None)
+        ctx["barrier"] = dist.barrier
+        ctx["all_ok"] = lambda ok: allreduce_max(0.0 if ok else 1.0, device) == 0.0
+        try:
+            rc = run_ring(args, ctx)
+        finally:
+            dist.barrier()
+            dist.destroy_process_group()
+        return rc
+    ctx["barrier"] = lambda: None
+    ctx["all_ok"] = bool
+    return run_compact(args, ctx)
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args, argv) -> int:
+    """`python bench.py --gpus N` without torchrun: re-launch this script under
+    torch.distributed.run with N ranks (one process per GPU) on 127.0.0.1;
+    rank 0's JSON line is the output."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *argv]
+    env = dict(os.environ, KVM_BENCH_LAUNCHER="self-launched torch.distributed.run")
+    return subprocess.call(cmd, env=env)
+
+
+def launch_check(args) -> int:
+    """--launch-check: the launcher path without a GPU (CPU tests): every rank
+    joins a gloo group, checks WORLD_SIZE == --gpus, reduces a max over ranks
+    and rank 0 prints one line."""
+    import torch.distributed as dist
+
+    from paper_2501_06709_b200.dist import allreduce_max, exchange_objects, rank_info_from_env
+
+    ri = rank_info_from_env()
+    if ri.world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ri.world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if ri.world > 1:
+        dist.init_process_group("gloo")
+    ranks = exchange_objects(ri.rank) if ri.world > 1 else [0]
+    mx = allreduce_max(float(ri.rank))
+    if ri.rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": ri.world, "ranks": ranks, "max_rank": mx,
+                          "launcher": os.environ.get("KVM_BENCH_LAUNCHER", "torchrun" if ri.world > 1 else "python")}),
+              flush=True)
+    if ri.world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
 def main(argv=None) -> int:
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -652,21 +1076,33 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="7b-4k")
     ap.add_argument("--engine", choices=["ldg", "bulk"], default=None,
-                    help="copy engine; default bulk (TMA) for local HBM at N=1, ldg (128-bit peer "
-                         "stores, the proven NVLink pattern) for N>1")
+                    help="copy engine; default bulk (TMA) at N=1; at N>1 a start-up A/B of both engines to the "
+                         "peer, behind the bit-exact gate, keeps the faster")
     ap.add_argument("--l2-evict-first", type=int, choices=[0, 1], default=0,
-                    help="stream KV through L2 with an evict-first policy (KVM_F_L2_EVICT_FIRST)")
+                    help="stream KV through L2 with an evict-first policy (KVM_F_L2_EVICT_FIRST), N=1")
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
-                    help="skip the re-prefill / decode measurements reported beside the headline")
+                    help="skip the re-prefill / decode measurements reported beside the headline (N=1)")
+    ap.add_argument("--no-library", action="store_true", help="skip the NCCL ring comparison (N>1)")
+    ap.add_argument("--extra-workloads", default=None,
+                    help="comma list of workloads measured beside the headline at N>1 (default 70b-16k)")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="allow N ranks on fewer GPUs (functional test of the IPC path; no NVLink)")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.extra_workloads is None:
+        args.extra_workloads = "70b-16k" if args.workload != "7b-512" else ""
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return self_launch(args, argv)
+    if args.launch_check:
+        return launch_check(args)
     if args.impl == "reference":
         return run_reference(args)
-    if args.engine is None:
-        args.engine = "bulk" if int(os.environ.get("WORLD_SIZE", args.gpus)) == 1 else "ldg"
     return run_ours(args)
 
 

@@ -30,6 +30,22 @@ def test_reference_arm_contract():
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
 
 
+def test_self_launch_runs_n_ranks_cpu():
+    """`python bench.py --gpus 2` without torchrun re-launches itself under
+    torch.distributed.run with 2 ranks (gloo here, no GPU): rank 0 prints the
+    one line and it reports n_gpus == 2."""
+    d = _run(["--launch-check", "--gpus", "2", "--steps", "3", "--warmup", "3"], timeout=300)
+    assert d["launch_check"] is True and d["n_gpus"] == 2 and d["ranks"] == [0, 1] and d["max_rank"] == 1.0
+    assert d["launcher"] == "self-launched torch.distributed.run"
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--launch-check", "--gpus", "1"],
+                         capture_output=True, text=True, cwd=ROOT, env=env, timeout=120)
+    assert out.returncode != 0 and "WORLD_SIZE=2" in out.stderr
+
+
 def test_warmup_floor():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--warmup", "2"], capture_output=True,
                          text=True, cwd=ROOT)
@@ -50,8 +66,30 @@ def test_gpu_arm_contract():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     k = d["kernels"]   # fresh re-prefill / decode measurements beside the headline
     assert k["reprefill_13b_s1360"]["unit"] == "TFLOP/s" and 0.3 < k["reprefill_13b_s1360"]["frac"] < 1.5
+    assert k["reprefill_13b_s1360"]["cublas_same_shape"]["ms"] > 0
     assert k["decode_7b_4k_32l"]["unit"] == "GB/s" and 0.3 < k["decode_7b_4k_32l"]["frac"] < 1.5
     assert 0 < k["small_move_7b_1block"]["issue_to_landed_us_p50"] < 1000
+
+
+@pytest.mark.gpu
+def test_gpu_arm_plain_python_two_ranks():
+    """Plain `python bench.py --gpus 2` (no torchrun) measures two ranks: on a
+    1-GPU box only with --shared-gpu (both ranks on the one GPU, IPC path, no
+    NVLink), and it refuses without it."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "7b-512",
+                              "--steps", "3", "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True,
+                             timeout=600, cwd=ROOT)
+        assert out.returncode != 0 and "--shared-gpu" in out.stderr
+    d = _run(["--gpus", "2", "--workload", "7b-512", "--steps", "5", "--warmup", "3", "--no-cpu-baseline",
+              "--shared-gpu"])
+    assert BASE_KEYS <= set(d) and d["n_gpus"] == 2 and d["bit_exact"] is True and d["value"] > 0
+    assert d["config"]["launcher"] == "self-launched torch.distributed.run"
+    assert d["e2e"]["value"] > 0 and d["e2e"]["row_ok"] is True
+    assert d["config"]["engine"] in ("bulk", "ldg") and set(d["config"]["engine_ab"]) == {"bulk", "ldg"}
+    assert "nvlink_counters" in d["roofline"] and d["gpu_launches"] > 0
 
 
 @pytest.mark.gpu
@@ -67,7 +105,7 @@ def test_gpu_arm_two_ranks_contract():
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                           "--gpus", "2", "--workload", "7b-512", "--steps", "5", "--warmup", "3",
-                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+                          "--no-cpu-baseline", "--shared-gpu"], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout
