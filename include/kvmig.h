@@ -195,7 +195,8 @@ typedef struct kvm_split_args {
  * of layer l overlaps the copy of later layers.  block_tables must already
  * hold the destination blocks (they are known before the copy); only KV
  * contents are awaited.  timeout_ns > 0 bounds the wait: on expiry *err_word
- * is set to 1 and the kernel proceeds (its output is then meaningless). */
+ * is set to 1 and the kernel proceeds (its output is then meaningless), so a
+ * nonzero timeout_ns without err_word is rejected (KVM_ERR_INVALID). */
 #define KVM_DECODE_WAIT_LAYERS 0x4
 #define KVM_DECODE_CUDA_CORES 0x2 /* force the CUDA-core path (G in {1,2,4,8});
                                      default: tensor-core mma path for G <= 8 */

@@ -11,4 +11,5 @@ leg.  The product package (paper_2501_06709_b200) never imports this package.
                       by this repo and pinned by identity / known-answer
                       properties (see the C header).
   kvmig_oracle.py     ctypes wrapper over liboracle_kvmig.so (built by Makefile).
+  attention_ref.py    fp32 torch paged-decode reference (checker of kvm_paged_decode).
 """

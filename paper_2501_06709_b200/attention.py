@@ -60,27 +60,3 @@ def paged_decode(pool: KVPool, q, block_tables, seq_lens, out=None, *, layer0: i
     _native.check(_native.lib().kvm_paged_decode(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),
                   "kvm_paged_decode")
     return out
-
-
-def reference_decode(pool: KVPool, q, block_tables, seq_lens, layer0: int = 0, scale: float = None):
-    """fp32 torch reference (tests only): gather K/V through the tables."""
-    import torch
-
-    sh = pool.shape
-    scale = scale if scale is not None else 1.0 / math.sqrt(sh.head_dim)
-    L, B, Hq, D = q.shape
-    G = Hq // sh.kv_heads
-    out = torch.empty(L, B, Hq, D, dtype=torch.float32, device=q.device)
-    for l in range(L):
-        for b in range(B):
-            n = int(seq_lens[b])
-            t = torch.arange(n, device=q.device)
-            blk = block_tables[b].long()[t // sh.block_tokens]
-            K = pool.tensor[layer0 + l, 0, blk, t % sh.block_tokens].float()  # [n, Hkv, D]
-            V = pool.tensor[layer0 + l, 1, blk, t % sh.block_tokens].float()
-            Kq = K.repeat_interleave(G, dim=1)  # [n, Hq, D]
-            Vq = V.repeat_interleave(G, dim=1)
-            s = torch.einsum("hd,nhd->hn", q[l, b].float(), Kq) * scale
-            p = torch.softmax(s, dim=-1)
-            out[l, b] = torch.einsum("hn,nhd->hd", p, Vq)
-    return out

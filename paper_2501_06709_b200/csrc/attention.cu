@@ -590,6 +590,9 @@ extern "C" int kvm_paged_decode(const kvm_decode_args* a, void* stream) {
     return fail(KVM_ERR_INVALID, "unknown flags");
   if ((a->flags & KVM_DECODE_WAIT_LAYERS) && !a->layer_flags)
     return fail(KVM_ERR_INVALID, "KVM_DECODE_WAIT_LAYERS needs layer_flags");
+  // a timed-out layer wait decodes partly migrated KV: the caller must be able to see that
+  if ((a->flags & KVM_DECODE_WAIT_LAYERS) && a->timeout_ns && !a->err_word)
+    return fail(KVM_ERR_INVALID, "timeout_ns needs err_word (a timed-out wait must be observable)");
   Params p;
   p.pool = pool->base;
   p.q = a->q;

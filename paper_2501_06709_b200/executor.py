@@ -28,9 +28,9 @@ from typing import Callable, Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _native
-from .errors import ConfigError, NotPlaced
+from .errors import ConfigError, NotPlaced, RequestTooLarge
 from .kvcache import BlockTable, KVPool
-from .planner import FORCED_KV_TRANSFER, KV_TRANSFER, TOKEN_TRANSFER, MigrationPlan, PlannedMove
+from .planner import FORCED_KV_TRANSFER, KV_TRANSFER, TOKEN_TRANSFER, MigrationPlan, PendingMove, PlannedMove
 
 ENGINES = {"ldg": 0, "bulk": _native.KVM_F_ENGINE_BULK}
 
@@ -131,6 +131,7 @@ class MigrationExecutor:
         self.reprefill = reprefill
         self.loc: Dict[int, Residency] = {}
         self._streams: Dict[int, "torch.cuda.Stream"] = {}
+        self._fences: Dict[int, Dict[int, object]] = {}   # pool id -> {device: event of a pending read}
         _native.lib()  # fail loudly now if the native library is missing
         devices = {p.device for per in self.pools.values() for p in per.values()}
         if len(devices) > 1:
@@ -235,7 +236,17 @@ class MigrationExecutor:
         """Carry out `plan.executed` (or a list of PlannedMove) in plan order.
 
         members_of(item) -> request ids of a group item (negative id); the
-        default treats every item as a single request.
+        default treats every item as a single request.  Every member that is
+        not physically on the move's dst moves there, from whichever GPU holds
+        it now: a group's members drift while its move is pending (a member
+        that joined at an intermediate GPU, sim.py:207-217), and the item's
+        logical GPU is where its bytes must end up.
+
+        All-or-nothing: every move is validated and every destination block
+        reserved before anything launches (unknown mode, missing or mismatched
+        pools, a re-prefill engine that cannot write the pool, a full pool or
+        block table all raise with nothing changed); a failure while issuing
+        rolls the reservations and new table rows back before re-raising.
 
         layer_flags: kv moves publish per-layer completion into `rec.layer_flags[rid]`
         (value 1), so a destination decode can start layer by layer
@@ -247,22 +258,20 @@ class MigrationExecutor:
         source GPU that feeds it, and `report.done[dst_device]` / `rec.done`
         is an event after which the destination's blocks and table row are
         final: a decode stream `wait_event`s on it.  Freed source blocks may
-        be reallocated by the host at once; launches that reuse them must be
-        queued behind the move (the executor's own streams are; a caller's
-        stream waits on `report.src_done[src_device]`).
+        be reallocated by the host at once: every later executor launch that
+        writes into that pool, from any device, first waits on the source's
+        copy (per-pool fences); a caller's own stream that writes into the
+        pool waits on `report.src_done[src_device]`.
         """
         executed: List[PlannedMove] = plan.executed if isinstance(plan, MigrationPlan) else [
             p for p in plan if p.mode != "deferred"]
         report = ExecReport()
         self._events = {}
-        by_dev: Dict[int, List[Tuple[_native.Move, int, int, np.ndarray, np.ndarray]]] = {}
-        keep = []  # host arrays must outlive the kvm_migrate call
-        post: List[Tuple[int, int, int, np.ndarray]] = []  # (rid, dst, tokens, dst_blocks)
         # phase 1: validate every move and reserve all destination blocks; nothing is
-        # launched yet, so a failure (unknown mode, missing engine, a full pool) leaves
-        # the pools and tables exactly as they were
+        # launched yet, so a failure leaves the pools and tables exactly as they were
         work = []  # (pm, rec, [(rid, res, src_pool, dst_pool, dst_blocks)])
         taken = []  # (pool, blocks) reserved in this call, for rollback
+        new_rows: Dict[int, int] = {}   # id(table) -> slots this call will newly take
         try:
             for pm in executed:
                 mv = pm.move
@@ -271,24 +280,79 @@ class MigrationExecutor:
                 rids = list(members_of(mv.item)) if (members_of and mv.item < 0) else [mv.item]
                 if self._pending:
                     self._check_not_pending(rids)
-                here = [r for r in rids if r in self.loc and self.loc[r].gpu == mv.src]
-                if pm.mode == TOKEN_TRANSFER and self.reprefill is None and here and mv.src != mv.dst:
+                movers = [r for r in rids if r in self.loc and self.loc[r].gpu != mv.dst]
+                if pm.mode == TOKEN_TRANSFER and self.reprefill is None and movers:
                     raise ConfigError("token_transfer planned but executor has no re-prefill engine")
-                rec = ExecRecord(mv.item, mv.src, mv.dst, pm.mode, here, 0, 0, 0)
+                rec = ExecRecord(mv.item, mv.src, mv.dst, pm.mode, movers, 0, 0, 0)
                 items = []
-                if mv.src != mv.dst:
-                    for rid in here:
-                        res = self.loc[rid]
-                        src_pool, dst_pool = self.pool(mv.src, res.model), self.pool(mv.dst, res.model)
-                        dst_blocks = dst_pool.allocator.alloc(len(res.blocks))
-                        taken.append((dst_pool, dst_blocks))
-                        items.append((rid, res, src_pool, dst_pool, dst_blocks))
+                for rid in movers:
+                    res = self.loc[rid]
+                    src_pool, dst_pool = self.pool(res.gpu, res.model), self.pool(mv.dst, res.model)
+                    if _geometry(src_pool) != _geometry(dst_pool):
+                        raise ConfigError(f"request {rid}: pools of GPU {res.gpu} and GPU {mv.dst} have different "
+                                          f"KV geometry {_geometry(src_pool)} vs {_geometry(dst_pool)}")
+                    if pm.mode == TOKEN_TRANSFER:
+                        check = getattr(self.reprefill, "validate", None)
+                        if check is not None:
+                            check(dst_pool)
+                    table = self._table(mv.dst, res.model)
+                    if table is not None:
+                        if len(res.blocks) > table.max_blocks:
+                            raise RequestTooLarge(f"request {rid}: {len(res.blocks)} blocks > block-table width "
+                                                  f"{table.max_blocks} on GPU {mv.dst}")
+                        if not table.has(rid):
+                            new_rows[id(table)] = new_rows.get(id(table), 0) + 1
+                            if new_rows[id(table)] > table.free_slots:
+                                raise ConfigError(f"block table of GPU {mv.dst} is full")
+                    dst_blocks = dst_pool.allocator.alloc(len(res.blocks))
+                    taken.append((dst_pool, dst_blocks))
+                    items.append((rid, res, src_pool, dst_pool, dst_blocks))
                 work.append((pm, rec, items))
         except Exception:
             for pool, blocks in taken:
                 pool.allocator.free(blocks)
             raise
-        # phase 2: launch
+        # phase 2: issue; on failure undo the reservations and the rows this call created
+        created: List[Tuple[BlockTable, int]] = []
+        try:
+            self._issue(work, report, created, layer_flags)
+        except BaseException:
+            try:
+                self.synchronize()      # nothing issued may still be writing the blocks we release
+            finally:
+                for pool, blocks in taken:
+                    pool.allocator.free(blocks)
+                for table, rid in created:
+                    table.drop(rid)
+            raise
+        post = [(rid, pm.move.dst, res.tokens, dst_blocks)
+                for pm, rec, items in work for rid, res, src_pool, dst_pool, dst_blocks in items]
+        if stream_ordered:
+            self._order_across_devices(report, work)
+            self._commit(post)
+        elif wait:
+            if self.timing:
+                self._close_timing(report)
+            self.synchronize()
+            self._commit(post)
+        else:
+            self._pending.append((post, False))
+        return report
+
+    def _issue(self, work, report: "ExecReport", created: list, layer_flags: bool) -> None:
+        """Phase 2 of execute(): re-prefills on their destination streams, then
+        one fused kvm_migrate launch per source device."""
+        by_dev: Dict[int, List[_native.Move]] = {}
+        writes: Dict[int, Dict[int, object]] = {}   # src device -> {dst pool id: dst pool}
+        keep = []  # host arrays must outlive the kvm_migrate call
+
+        def table_for(gpu, model, rid):
+            table = self._table(gpu, model)
+            if table is not None and not table.has(rid):
+                table.slot(rid)
+                created.append((table, rid))
+            return table
+
         for pm, rec, items in work:
             mv = pm.move
             for rid, res, src_pool, dst_pool, dst_blocks in items:
@@ -301,7 +365,7 @@ class MigrationExecutor:
                     db = np.ascontiguousarray(dst_blocks, dtype=np.int32)
                     keep += [sb, db]
                     m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
-                    table = self._table(mv.dst, res.model)
+                    table = table_for(mv.dst, res.model, rid)
                     if table is not None:
                         table.set_host(rid, db)
                         m.dst_table_row = table.row_ptr(rid)
@@ -312,12 +376,14 @@ class MigrationExecutor:
                         rec.layer_flags[rid] = fl
                         m.layer_flags = fl.data_ptr()
                     by_dev.setdefault(src_pool.device, []).append(m)
+                    writes.setdefault(src_pool.device, {})[dst_pool.pool_id] = dst_pool
                     rec.bytes_moved += nb * src_pool.shape.piece_bytes * 2 * src_pool.shape.layers
                     rec.tokens_moved += res.tokens
                 else:  # TOKEN_TRANSFER
-                    self.reprefill(self, rid, mv.dst, dst_blocks, res.tokens,
-                                   self.ordered_stream(dst_pool.device))
-                    table = self._table(mv.dst, res.model)
+                    s = self.ordered_stream(dst_pool.device)
+                    self._wait_fences(s, dst_pool.device, [dst_pool])
+                    self.reprefill(self, rid, mv.dst, dst_blocks, res.tokens, s)
+                    table = table_for(mv.dst, res.model, rid)
                     if table is not None:
                         table.set_host(rid, dst_blocks)
                         table.rows[table.slot(rid), :len(dst_blocks)].copy_(
@@ -326,22 +392,36 @@ class MigrationExecutor:
                     report.launches += 1
                 rec.blocks += nb
                 rec.request_tokens[rid] = res.tokens
-                post.append((rid, mv.dst, res.tokens, dst_blocks))
             report.records.append(rec)
         for dev, moves in by_dev.items():
-            self._launch_migrate(dev, moves)
+            self._launch_migrate(dev, moves, list(writes[dev].values()))
             report.launches += 1
-        if stream_ordered:
-            self._order_across_devices(report, work)
-            self._commit(post)
-        elif wait:
-            if self.timing:
-                self._close_timing(report)
-            self.synchronize()
-            self._commit(post)
-        else:
-            self._pending.append((post, False))
-        return report
+
+    def reconcile(self, target_of: Callable[[int], Optional[int]], skip=(), **kw) -> ExecReport:
+        """Move every resident request whose physical GPU differs from
+        `target_of(rid)` (its item's logical GPU) there, as kv_transfer —
+        except requests in `skip` (members of items still in the backlog,
+        which travel with their item's planned move).
+
+        Why: the reference's planner never sees member-level moves (a member
+        shed from its group and re-placed, scheduler.py:944-975, or a request
+        absorbed into another GPU's group): at the backlog refresh the moved
+        id is no longer an item, so its PendingMove is dropped
+        (sim.py:207-213) and its bytes would stay on the old GPU for good.
+        These moves are outside the plan (no budget, no plan row); the
+        decisions stay the reference's."""
+        moves = []
+        for rid in sorted(self.loc):
+            if rid in skip:
+                continue
+            res = self.loc[rid]
+            g = target_of(rid)
+            if g is None or g == res.gpu:
+                continue
+            moves.append(PlannedMove(PendingMove(rid, res.gpu, g, 0, res.tokens), KV_TRANSFER))
+        if not moves:
+            return ExecReport()
+        return self.execute(moves, **kw)
 
     def _order_across_devices(self, report: "ExecReport", work) -> None:
         """Stream-ordered completion: one event per source device after its
@@ -357,6 +437,9 @@ class MigrationExecutor:
             ev = torch.cuda.Event()
             ev.record(self.stream(dev))
             report.src_done[dev] = ev
+        for pm, rec, items in work:   # the source blocks are freed now; writers elsewhere wait on the read
+            for rid, res, src_pool, dst_pool, dst_blocks in items:
+                self._fence(src_pool, src_pool.device, report.src_done[src_pool.device])
         for dst, srcs in sorted(feeds.items()):
             s = self.stream(dst)
             for src in sorted(srcs):
@@ -397,6 +480,7 @@ class MigrationExecutor:
         if row_out is not None and table is None:
             raise ConfigError("row_out needs a block table on this GPU")
         s = self.ordered_stream(pool.device)
+        self._wait_fences(s, pool.device, [pool])
         lib = _native.lib()
         sp = ctypes.c_void_p(s.cuda_stream)
         _native.check(lib.kvm_compact(pool.pool_id, sb.ctypes.data, dst.ctypes.data, nb, ctypes.c_void_p(row),
@@ -414,6 +498,7 @@ class MigrationExecutor:
 
             rec.done = torch.cuda.Event()
             rec.done.record(s)
+            self._fence(pool, pool.device, rec.done)
             self._commit(post, keep_table=True)
         elif wait:
             s.synchronize()
@@ -451,6 +536,7 @@ class MigrationExecutor:
         s = self.ordered_stream(dev)
         if src_pool.device != dev:
             s.wait_stream(torch.cuda.current_stream(src_pool.device))
+        self._wait_fences(s, dev, [dst_pool])
         with torch.cuda.stream(s):
             sbd = torch.from_numpy(np.ascontiguousarray(res.blocks, dtype=np.int32)).to(f"cuda:{dev}")
             dbd = torch.from_numpy(dst_blocks).to(f"cuda:{dev}")
@@ -485,13 +571,42 @@ class MigrationExecutor:
             raise ValueError(f"requests {sorted(hit)} have an uncommitted move: call commit() first")
 
     # -- internals ---------------------------------------------------------------
-    def _launch_migrate(self, dev: int, moves: List[_native.Move]) -> None:
-        """One fused kvm_migrate launch for every move leaving `dev` this slot."""
+    def _launch_migrate(self, dev: int, moves: List[_native.Move], dst_pools=()) -> None:
+        """One fused kvm_migrate launch for every move leaving `dev` this slot.
+
+        The kernel (on `dev`) also writes the destination devices' memory: the
+        pools, the block-table rows (reset to -1 on slot reuse) and the layer
+        flags (zeroed) — the latter two queued by this call on the destination
+        devices' current streams.  So the launch stream waits on those streams
+        and on the fences of every destination pool first."""
+        import torch
+
         arr = (_native.Move * len(moves))(*moves)
         s = self.ordered_stream(dev)
+        for d in sorted({p.device for p in dst_pools} - {dev}):
+            s.wait_stream(torch.cuda.current_stream(d))
+        self._wait_fences(s, dev, dst_pools)
         _native.check(_native.lib().kvm_migrate(arr, len(moves),
                                                 _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag,
                                                 ctypes.c_void_p(s.cuda_stream)), "kvm_migrate")
+
+    def _wait_fences(self, s, dev: int, pools) -> None:
+        """Make stream `s` (on `dev`) wait for outstanding stream-ordered moves
+        that READ blocks of `pools` and were issued on another device: their
+        source blocks are already free on the host and may be handed out
+        again to the write `s` is about to issue."""
+        for p in pools:
+            fences = self._fences.get(p.pool_id)
+            if not fences:
+                continue
+            for d, ev in list(fences.items()):
+                if ev.query():
+                    del fences[d]
+                elif d != dev:
+                    s.wait_event(ev)
+
+    def _fence(self, pool, dev: int, ev) -> None:
+        self._fences.setdefault(pool.pool_id, {})[dev] = ev
 
     def _commit(self, post, keep_table: bool = False) -> None:
         for rid, dst, tokens, dst_blocks in post:
@@ -517,6 +632,11 @@ class MigrationExecutor:
             return
         t.set_host(rid, blocks)
         t.rows[t.slot(rid), :len(blocks)].copy_(_as_i32_tensor(blocks, t.device))
+
+
+def _geometry(pool) -> tuple:
+    sh = pool.shape
+    return (sh.layers, sh.kv_heads, sh.head_dim, sh.block_tokens, sh.elem_bytes)
 
 
 def _by_model(p) -> Dict[str, KVPool]:

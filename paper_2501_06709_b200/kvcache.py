@@ -241,6 +241,13 @@ class BlockTable:
             self._slot_of[rid] = s
         return self._slot_of[rid]
 
+    def has(self, rid: int) -> bool:
+        return rid in self._slot_of
+
+    @property
+    def free_slots(self) -> int:
+        return len(self._free_slots)
+
     def row_ptr(self, rid: int) -> int:
         return self.rows.data_ptr() + self.slot(rid) * self.max_blocks * 4
 

@@ -177,6 +177,11 @@ class FingerprintedExecutor:
         self.reports.append(report)
         return report
 
+    def reconcile(self, target_of, skip=()):
+        report = self.ex.reconcile(target_of, skip=skip)
+        self.reports.append(report)
+        return report
+
     def verify(self) -> int:
         import torch
 

@@ -108,6 +108,16 @@ class ReprefillEngine:
         self.weights = {(d, s.name): synthetic_weights(s, d, with_q=with_q, seed=seed)
                         for d in set(devices) for s in shapes}
 
+    def validate(self, pool: KVPool) -> None:
+        """Raise before anything is reserved or launched if this engine cannot
+        write into `pool` (the executor calls it in its validation phase)."""
+        import torch
+
+        if pool.dtype != torch.bfloat16:
+            raise ConfigError("re-prefill writes bf16 K/V: pool dtype must be bfloat16")
+        if pool.shape.name not in self.shapes:
+            raise ConfigError(f"re-prefill engine has no weights for model {pool.shape.name!r}")
+
     def hidden(self, shape: ModelShape, rid: int, tokens: int, device: int):
         return synthetic_hidden(shape, tokens, device, seed=10_000 + rid)
 

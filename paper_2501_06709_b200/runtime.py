@@ -47,6 +47,8 @@ class LoopResult:
     used_bytes: List[int] = field(default_factory=list)      # sim.py:231-234 (KV bytes that exist)
     capacity_bytes: List[int] = field(default_factory=list)  # active GPUs x C
     bytes_moved: int = 0
+    reconciled_moves: int = 0      # executor.reconcile moves (outside the plan)
+    reconciled_bytes: int = 0
     completed: int = 0
     rejected: int = 0
     aborted: int = 0
@@ -114,7 +116,7 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
               bpt, tokens_per_slot: int = 10, epoch_slots: int = 1, max_defer: int = 3,
               duration_slots: int = 0, executor=None, reserve_final: bool = False,
               models: Optional[Dict[int, str]] = None,
-              on_slot: Optional[Callable[[int, list], None]] = None) -> LoopResult:
+              on_slot: Optional[Callable[[int, list], None]] = None, reconcile: bool = True) -> LoopResult:
     """Run the slot loop; `records` are (request_id, arrival_slot, prompt, response).
 
     `bpt` is the reference's kv_bytes_per_token (config.py:92), or — multi-LLM
@@ -123,7 +125,11 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
     sim.run just sets them all equal).  `models` names each request's model
     for the executor's per-model pools.  With an executor, placements become
     executor.admit, growth executor.grow, departures executor.release and
-    executed plan rows executor.execute.
+    executed plan rows executor.execute.  reconcile: after the plan, requests
+    whose physical GPU differs from their item's logical GPU and whose item
+    is not in the backlog are moved there (executor.reconcile; member-level
+    moves the reference's refresh drops, sim.py:207-213); counted in
+    `reconciled_moves` / `reconciled_bytes`, not in the plan rows.
     """
     tps = tokens_per_slot
     recs = {r[0]: tuple(r) for r in records}
@@ -223,6 +229,16 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
         for planned in plan.executed:
             del pending[planned.move.item]
             defer_counts.pop(planned.move.item, None)
+        if executor is not None and reconcile:
+            # bytes of requests whose logical move never reached the planner (member-level
+            # moves, dropped at the refresh above) follow their item now; members of items
+            # still pending travel with the item's planned move
+            waiting = set()
+            for item in pending:
+                waiting.update(cluster.groups[item].members if item < 0 and item in cluster.groups else (item,))
+            rep = executor.reconcile(lambda rid: cluster.placement.get(cluster.item_of_request(rid)), skip=waiting)
+            out.reconciled_moves += len(rep.records)
+            out.reconciled_bytes += rep.bytes_moved
         for mv in plan.deferred:
             defer_counts[mv.item] = defer_counts.get(mv.item, 0) + 1
         active = sum(1 for g in cluster.gpus.values() if g.residents)

@@ -8,7 +8,8 @@ import pytest
 import torch
 
 from paper_2501_06709_b200 import _native
-from paper_2501_06709_b200.attention import paged_decode, reference_decode
+from oracle.attention_ref import reference_decode
+from paper_2501_06709_b200.attention import paged_decode
 from paper_2501_06709_b200.kvcache import BlockTable, KVPool, ModelShape
 
 pytestmark = pytest.mark.gpu
@@ -155,6 +156,9 @@ def test_decode_layer_wait_times_out_instead_of_hanging():
     paged_decode(src, q, sb[None].contiguous().cuda(), lens, layer_flags=flags, timeout_ns=2_000_000, err_word=err)
     torch.cuda.synchronize()
     assert err.item() == 1
+    # a bounded wait whose expiry nobody could observe is refused up front
+    with pytest.raises(ValueError):
+        paged_decode(src, q, sb[None].contiguous().cuda(), lens, layer_flags=flags, timeout_ns=2_000_000)
 
 
 def test_decode_pipelined_behind_an_incoming_migration():

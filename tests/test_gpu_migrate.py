@@ -13,7 +13,7 @@ import pytest
 import torch
 
 from oracle import kvmig_oracle as orc
-from paper_2501_06709_b200 import ConfigError, NotPlaced, _native
+from paper_2501_06709_b200 import ConfigError, NotPlaced, RequestTooLarge, _native
 from paper_2501_06709_b200.kvcache import (LLAMA2_7B, LLAMA2_13B, LLAMA3_70B, BlockTable, KVPool,
                                            ModelShape)
 
@@ -536,3 +536,37 @@ def test_same_pool_batches_randomized(seed):
             orc.migrate(before, _desc(pool), exp, _desc(pool), keep[k], keep[k + 1])
         _run(moves, flags)
         assert np.array_equal(pool.tensor.view(torch.int16).cpu().numpy(), exp)
+
+
+def test_executor_validation_leaves_pools_tables_untouched():
+    """a plan whose token_transfer targets an fp16 pool (the re-prefill
+    engine writes bf16) or whose request is wider than the destination block
+    table fails before anything is reserved, launched or given a table row."""
+    from paper_2501_06709_b200 import PendingMove
+    from paper_2501_06709_b200.executor import MigrationExecutor
+    from paper_2501_06709_b200.planner import KV_TRANSFER, TOKEN_TRANSFER, PlannedMove
+    from paper_2501_06709_b200.reprefill import ReprefillEngine
+
+    pools = {0: KVPool(SMALL, 64), 1: KVPool(SMALL, 64)}          # fp16 pools
+    tables = {0: BlockTable(8, 16), 1: BlockTable(8, 4)}          # GPU 1 rows hold 4 blocks
+    ex = MigrationExecutor(pools, tables, reprefill=ReprefillEngine(SMALL, [0]))
+    _fill(pools[0], 3)
+    ex.admit(1, 0, 40)      # 3 blocks
+    ex.admit(2, 0, 40)
+    ex.admit(3, 0, 100)     # 7 blocks > 4
+    before = pools[1].tensor.view(torch.int16).clone()
+    launches = _native.launch_count()
+    free = [p.allocator.n_free for p in pools.values()]
+    for plan in ([PlannedMove(PendingMove(1, 0, 1, 0, 40), KV_TRANSFER),
+                  PlannedMove(PendingMove(2, 0, 1, 0, 40), TOKEN_TRANSFER)],
+                 [PlannedMove(PendingMove(1, 0, 1, 0, 40), KV_TRANSFER),
+                  PlannedMove(PendingMove(3, 0, 1, 0, 100), KV_TRANSFER)]):
+        with pytest.raises((ConfigError, RequestTooLarge)):
+            ex.execute(plan)
+        torch.cuda.synchronize()
+        assert [p.allocator.n_free for p in pools.values()] == free
+        assert _native.launch_count() == launches and torch.equal(pools[1].tensor.view(torch.int16), before)
+        assert not tables[1].has(1) and not tables[1].has(2) and not tables[1].has(3)
+        assert {ex.where(r).gpu for r in (1, 2, 3)} == {0}
+    rep = ex.execute([PlannedMove(PendingMove(1, 0, 1, 0, 40), KV_TRANSFER)])
+    assert rep.records[0].requests == [1] and ex.where(1).gpu == 1 and tables[1].has(1)

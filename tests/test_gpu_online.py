@@ -47,10 +47,21 @@ def test_online_loop_native_scheduler_on_gpu(name, seed):
                     prefill_tokens_per_s=cl["prefill_tokens_per_s"])
     bounds = load_boundaries(topo, cfg["migration"]["epoch_seconds"], cfg["migration"]["budget_fraction"])
     checked = []
+    misplaced = []
 
     def on_slot(slot, rows):
         if slot % 100 == 99:
             checked.append(ex.verify())
+        # the bytes follow the scheduler: every request not waiting in the backlog sits on its
+        # item's logical GPU (planned moves + executor.reconcile of member-level moves)
+        waiting = set()
+        for r in rows:
+            if r[6] == "deferred":
+                waiting.update(cluster.groups[r[1]].members if r[1] < 0 and r[1] in cluster.groups else (r[1],))
+        for rid, res in ex.loc.items():
+            item = cluster.item_of_request(rid)
+            if rid not in waiting and item is not None and cluster.placement.get(item) != res.gpu:
+                misplaced.append((slot, rid))
 
     out = run_slots(trace.tuples(), sched, cluster, topo, bounds, bpt=bpt,
                     tokens_per_slot=cfg["sim"]["tokens_per_slot"], max_defer=cfg["migration"]["max_defer"],
@@ -60,4 +71,5 @@ def test_online_loop_native_scheduler_on_gpu(name, seed):
     assert out.active_gpus == fx["active_gpus"]
     assert out.bytes_moved > 0
     assert sum(checked) > 0
+    assert misplaced == [] and out.reconciled_moves > 0
     assert sum(len(r.records) for r in ex.reports) > 0

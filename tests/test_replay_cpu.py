@@ -50,7 +50,7 @@ class HostExecutor(MigrationExecutor):
     def ordered_stream(self, device):
         return _Stream()
 
-    def _launch_migrate(self, dev, moves):
+    def _launch_migrate(self, dev, moves, dst_pools=()):
         self.launched.append([(m.src_pool, m.dst_pool, m.n_blocks) for m in moves])
 
     def _reprefill(self, ex, rid, dst, blocks, tokens, stream):
