@@ -18,6 +18,11 @@ after the copy has completed.
 Modes (migration.py:19-22):
   kv_transfer, forced_kv_transfer -> kvm_migrate (gather -> push -> table rewrite)
   token_transfer                  -> kvm_reprefill on the destination
+  split_transfer (extension, plan_hybrid(split=True)) -> the prefix's blocks by
+      KV copy and the suffix's tokens by re-prefill: one fused
+      kvm_split_migrate launch on the destination when both pools share a
+      device, else kvm_migrate on the source in parallel with kvm_reprefill
+      on the destination
 """
 from __future__ import annotations
 
@@ -30,7 +35,8 @@ import numpy as np
 from . import _native
 from .errors import ConfigError, NotPlaced, RequestTooLarge
 from .kvcache import BlockTable, KVPool
-from .planner import FORCED_KV_TRANSFER, KV_TRANSFER, TOKEN_TRANSFER, MigrationPlan, PendingMove, PlannedMove
+from .planner import (FORCED_KV_TRANSFER, KV_TRANSFER, SPLIT_TRANSFER, TOKEN_TRANSFER, MigrationPlan, PendingMove,
+                      PlannedMove)
 
 ENGINES = {"ldg": 0, "bulk": _native.KVM_F_ENGINE_BULK}
 
@@ -61,6 +67,8 @@ class ExecRecord:
     # execute(layer_flags=True): per moved request, an int32 device tensor [layers] on the destination
     # GPU; entry l reaches 1 once layer l landed (paged_decode(..., layer_flags=...) pipelines on it)
     layer_flags: Dict[int, object] = field(default_factory=dict)
+    # split_transfer: per moved request, how many of its blocks (from the front) were copied
+    split_prefix_blocks: Dict[int, int] = field(default_factory=dict)
 
 
 @dataclass
@@ -275,14 +283,16 @@ class MigrationExecutor:
         try:
             for pm in executed:
                 mv = pm.move
-                if pm.mode not in (KV_TRANSFER, FORCED_KV_TRANSFER, TOKEN_TRANSFER):
+                if pm.mode not in (KV_TRANSFER, FORCED_KV_TRANSFER, TOKEN_TRANSFER, SPLIT_TRANSFER):
                     raise ValueError(f"cannot execute mode {pm.mode!r}")
+                if pm.mode == SPLIT_TRANSFER and mv.item < 0:
+                    raise ValueError("split_transfer applies to single requests, not groups")
                 rids = list(members_of(mv.item)) if (members_of and mv.item < 0) else [mv.item]
                 if self._pending:
                     self._check_not_pending(rids)
                 movers = [r for r in rids if r in self.loc and self.loc[r].gpu != mv.dst]
-                if pm.mode == TOKEN_TRANSFER and self.reprefill is None and movers:
-                    raise ConfigError("token_transfer planned but executor has no re-prefill engine")
+                if pm.mode in (TOKEN_TRANSFER, SPLIT_TRANSFER) and self.reprefill is None and movers:
+                    raise ConfigError(f"{pm.mode} planned but executor has no re-prefill engine")
                 rec = ExecRecord(mv.item, mv.src, mv.dst, pm.mode, movers, 0, 0, 0)
                 items = []
                 for rid in movers:
@@ -291,7 +301,7 @@ class MigrationExecutor:
                     if _geometry(src_pool) != _geometry(dst_pool):
                         raise ConfigError(f"request {rid}: pools of GPU {res.gpu} and GPU {mv.dst} have different "
                                           f"KV geometry {_geometry(src_pool)} vs {_geometry(dst_pool)}")
-                    if pm.mode == TOKEN_TRANSFER:
+                    if pm.mode in (TOKEN_TRANSFER, SPLIT_TRANSFER):
                         check = getattr(self.reprefill, "validate", None)
                         if check is not None:
                             check(dst_pool)
@@ -379,6 +389,9 @@ class MigrationExecutor:
                     writes.setdefault(src_pool.device, {})[dst_pool.pool_id] = dst_pool
                     rec.bytes_moved += nb * src_pool.shape.piece_bytes * 2 * src_pool.shape.layers
                     rec.tokens_moved += res.tokens
+                elif pm.mode == SPLIT_TRANSFER:
+                    self._issue_split(pm, rec, rid, res, src_pool, dst_pool, dst_blocks, table_for)
+                    report.launches += 1 if src_pool.device == dst_pool.device else 2
                 else:  # TOKEN_TRANSFER
                     s = self.ordered_stream(dst_pool.device)
                     self._wait_fences(s, dst_pool.device, [dst_pool])
@@ -507,54 +520,33 @@ class MigrationExecutor:
             self._pending.append((post, True))
         return rec
 
-    def split_move(self, rid: int, dst_gpu: int, suffix: Optional[int] = None, *, link_bytes_per_s: float = 770e9,
-                   tensor_flops_per_s: float = 1.28e15) -> ExecRecord:
-        """Adaptive split (extension of migration.py:155-169): transfer the first
-        n - s tokens' blocks and re-prefill the last s tokens, in ONE fused
-        kernel on the destination (kvm_split_migrate).  s defaults to the
-        balanced point of the reference's linear cost terms
-        (reprefill.split_point).  Needs a ReprefillEngine; the source pool must
-        be registered on the destination's device."""
-        import torch
+    def split_move(self, rid: int, dst_gpu: int, suffix: Optional[int] = None, *, topology=None,
+                   **execute_kw) -> ExecRecord:
+        """One split_transfer through execute() (the planner's split mode does
+        this for every split it plans): copy the first n - s tokens' blocks,
+        re-prefill the last s tokens on `dst_gpu`.  s is `suffix`, or — with a
+        `topology` — the planner's balanced point from the topology's own link
+        bandwidth and prefill rate (planner.split_suffix, the reference's cost
+        terms migration.py:158-163), without budget limits."""
+        from .planner import split_suffix
 
-        from .reprefill import split_point
-        from .split import flops_per_token, make_split, split_migrate_fused
-
-        if self.reprefill is None:
-            raise ConfigError("split moves need a re-prefill engine")
         res = self._res(rid)
-        src_pool, dst_pool = self.pool(res.gpu, res.model), self.pool(dst_gpu, res.model)
-        sh = dst_pool.shape
+        sh = self.pool(res.gpu, res.model).shape
+        n = res.tokens
+        kv = n * sh.kv_bytes_per_token
         if suffix is None:
-            suffix = split_point(res.tokens, sh.kv_bytes_per_token, link_bytes_per_s,
-                                 flops_per_token(sh, with_q=self.reprefill.with_q), tensor_flops_per_s)
-        # the transferred prefix must be whole blocks
-        suffix = res.tokens - ((res.tokens - suffix) // sh.block_tokens) * sh.block_tokens
-        plan = make_split(res.tokens, suffix, sh.block_tokens)
-        dst_blocks = dst_pool.allocator.alloc(plan.total_blocks)
-        dev = dst_pool.device
-        s = self.ordered_stream(dev)
-        if src_pool.device != dev:
-            s.wait_stream(torch.cuda.current_stream(src_pool.device))
-        self._wait_fences(s, dev, [dst_pool])
-        with torch.cuda.stream(s):
-            sbd = torch.from_numpy(np.ascontiguousarray(res.blocks, dtype=np.int32)).to(f"cuda:{dev}")
-            dbd = torch.from_numpy(dst_blocks).to(f"cuda:{dev}")
-            x = self.reprefill.hidden(sh, rid, max(suffix, 1), dev)[:suffix].contiguous()
-            table = self._table(dst_gpu, res.model)
-            row = 0
-            if table is not None:
-                table.set_host(rid, dst_blocks)
-                row = table.row_ptr(rid)
-            split_migrate_fused(src_pool, dst_pool, sbd, dbd, plan, x, self.reprefill.weights[(dev, sh.name)],
-                                stream=s, table_row=row)
-            for t in (sbd, dbd, x):
-                t.record_stream(s)
-        s.synchronize()
-        self._commit([(rid, dst_gpu, res.tokens, dst_blocks)])
-        return ExecRecord(rid, res.gpu, dst_gpu, "split", [rid], plan.total_blocks,
-                          plan.prefix_blocks * sh.piece_bytes * 2 * sh.layers, suffix,
-                          plan.prefix_tokens, {rid: res.tokens})
+            if topology is None:
+                raise ConfigError("split_move needs suffix= or topology= (the split point comes from its link "
+                                  "bandwidth and prefill rate)")
+            link = topology.link_of(res.gpu, dst_gpu)
+            suffix = split_suffix(n, kv, topology.bandwidth_of(link), topology.prefill_tokens_per_s,
+                                  float("inf"), float("inf"), sh.block_tokens)
+            if suffix is None:
+                suffix = n
+        if not 0 <= suffix <= n:
+            raise ValueError("suffix must be in [0, tokens]")
+        pm = PlannedMove(PendingMove(rid, res.gpu, dst_gpu, kv, n), SPLIT_TRANSFER, 0.0, suffix)
+        return self.execute([pm], **execute_kw).records[0]
 
     def commit(self) -> None:
         """Finish every wait=False execute()/compact(): await streams, then free
@@ -571,6 +563,77 @@ class MigrationExecutor:
             raise ValueError(f"requests {sorted(hit)} have an uncommitted move: call commit() first")
 
     # -- internals ---------------------------------------------------------------
+    def _issue_split(self, pm, rec, rid, res, src_pool, dst_pool, dst_blocks, table_for) -> None:
+        """One split_transfer: the first n - s tokens' blocks are copied, the
+        last s tokens re-prefilled on the destination (s = pm.suffix_tokens,
+        re-based on the request's current length; the prefix stays whole
+        blocks).  Same device: ONE fused kvm_split_migrate launch (idle GEMM
+        warps stream the prefix while the tensor cores recompute the suffix).
+        Across devices: kvm_migrate on the source pushes the prefix over
+        NVLink while kvm_reprefill runs on the destination, whose stream then
+        waits for the prefix's done flag (device side) and gets the full
+        block-table row."""
+        import torch
+
+        from .reprefill import reprefill
+        from .split import make_split, split_migrate_fused
+
+        sh = dst_pool.shape
+        n = res.tokens
+        prefix = max(0, min(n, pm.move.tokens - pm.suffix_tokens))
+        prefix -= prefix % sh.block_tokens
+        plan = make_split(n, n - prefix, sh.block_tokens)
+        eng = self.reprefill
+        dev = dst_pool.device
+        cross = src_pool.device != dev
+        flags = torch.zeros(2, dtype=torch.int32, device=f"cuda:{dev}") if cross else None
+        s = self.ordered_stream(dev)
+        self._wait_fences(s, dev, [dst_pool])
+        w = eng.weights[(dev, sh.name)]
+        table = table_for(pm.move.dst, res.model, rid)
+        row = 0
+        if table is not None:
+            table.set_host(rid, dst_blocks)
+            row = table.row_ptr(rid)
+        rope = float(getattr(eng, "rope_theta", None) or 0.0)
+        db_np = np.ascontiguousarray(dst_blocks, dtype=np.int32)
+        with torch.cuda.stream(s):
+            x = eng.hidden(sh, rid, n, dev)[prefix:].contiguous() if plan.suffix else None
+            dbd = torch.from_numpy(db_np).to(f"cuda:{dev}")
+        keep = [t for t in (x, dbd, flags) if t is not None]
+        if not cross:
+            with torch.cuda.stream(s):
+                sbd = torch.from_numpy(np.ascontiguousarray(res.blocks, dtype=np.int32)).to(f"cuda:{dev}")
+            keep.append(sbd)
+            split_migrate_fused(src_pool, dst_pool, sbd, dbd, plan, x, w, stream=s, table_row=row, rope_theta=rope)
+        else:
+            if plan.prefix_blocks:
+                xs = self.ordered_stream(src_pool.device)
+                xs.wait_stream(torch.cuda.current_stream(dev))   # the flag words / table row reset live there
+                self._wait_fences(xs, src_pool.device, [dst_pool])
+                m = _native.Move()
+                m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src_pool.pool_id, dst_pool.pool_id, \
+                    plan.prefix_blocks, 1
+                sb = np.ascontiguousarray(res.blocks[:plan.prefix_blocks], dtype=np.int32)
+                m.src_blocks, m.dst_blocks, m.done_flag = sb.ctypes.data, db_np.ctypes.data, flags.data_ptr()
+                _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1,
+                                                        _native.KVM_F_BLOCKS_ON_HOST | self.engine_flag,
+                                                        ctypes.c_void_p(xs.cuda_stream)), "kvm_migrate(split prefix)")
+            if plan.suffix:
+                reprefill(dst_pool, x, w, dbd, tok0=prefix, stream=s, rope_theta=rope or None)
+            if plan.prefix_blocks:
+                _native.check(_native.lib().kvm_wait_flag(ctypes.c_void_p(flags.data_ptr()), 1,
+                                                          ctypes.c_void_p(s.cuda_stream)), "kvm_wait_flag")
+            if table is not None:
+                with torch.cuda.stream(s):
+                    table.rows[table.slot(rid), :len(db_np)].copy_(dbd)
+        for t in keep:
+            t.record_stream(s)
+        rec.bytes_moved += plan.prefix_blocks * src_pool.shape.piece_bytes * 2 * src_pool.shape.layers
+        rec.tokens_moved += plan.prefix_tokens
+        rec.tokens_recomputed += plan.suffix
+        rec.split_prefix_blocks[rid] = plan.prefix_blocks
+
     def _launch_migrate(self, dev: int, moves: List[_native.Move], dst_pools=()) -> None:
         """One fused kvm_migrate launch for every move leaving `dev` this slot.
 

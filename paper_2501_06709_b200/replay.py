@@ -90,6 +90,7 @@ class Fingerprints:
     def __init__(self, executor):
         self.ex = executor
         self.recomputed: set = set()
+        self.prefix_only: Dict[int, int] = {}  # split_transfer: rid -> leading blocks still carrying copies
         self._stamped: Dict[int, int] = {}   # rid -> number of blocks stamped
 
     def stamp(self, rid: int) -> None:
@@ -110,6 +111,7 @@ class Fingerprints:
     def forget(self, rid: int) -> None:
         self._stamped.pop(rid, None)
         self.recomputed.discard(rid)
+        self.prefix_only.pop(rid, None)
 
     @staticmethod
     def values(rid, lo, hi, pool):
@@ -133,9 +135,10 @@ class Fingerprints:
             if rid in self.recomputed:
                 continue
             pool = self.ex.pool(r.gpu, r.model)
-            got = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(r.blocks.astype(np.int64)).to(
+            k = min(len(r.blocks), self.prefix_only.get(rid, len(r.blocks)))   # split: the copied prefix only
+            got = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(r.blocks[:k].astype(np.int64)).to(
                 pool.tensor.device)]
-            if not torch.equal(got, self.values(rid, 0, len(r.blocks), pool)):
+            if not torch.equal(got, self.values(rid, 0, k, pool)):
                 raise AssertionError(f"request {rid} on GPU {r.gpu}: KV bytes differ from its fingerprint")
             n += 1
         return n
@@ -174,6 +177,8 @@ class FingerprintedExecutor:
         for rec in report.records:
             if rec.mode == TOKEN_TRANSFER:
                 self.fp.recomputed.update(rec.requests)
+            for rid, k in rec.split_prefix_blocks.items():
+                self.fp.prefix_only[rid] = min(self.fp.prefix_only.get(rid, k), k)
         self.reports.append(report)
         return report
 

@@ -116,7 +116,8 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
               bpt, tokens_per_slot: int = 10, epoch_slots: int = 1, max_defer: int = 3,
               duration_slots: int = 0, executor=None, reserve_final: bool = False,
               models: Optional[Dict[int, str]] = None,
-              on_slot: Optional[Callable[[int, list], None]] = None, reconcile: bool = True) -> LoopResult:
+              on_slot: Optional[Callable[[int, list], None]] = None, reconcile: bool = True,
+              split: bool = False) -> LoopResult:
     """Run the slot loop; `records` are (request_id, arrival_slot, prompt, response).
 
     `bpt` is the reference's kv_bytes_per_token (config.py:92), or — multi-LLM
@@ -129,7 +130,9 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
     whose physical GPU differs from their item's logical GPU and whose item
     is not in the backlog are moved there (executor.reconcile; member-level
     moves the reference's refresh drops, sim.py:207-213); counted in
-    `reconciled_moves` / `reconciled_bytes`, not in the plan rows.
+    `reconciled_moves` / `reconciled_bytes`, not in the plan rows.  split:
+    the planner's split mode (plan_hybrid(split=True), extension, off by
+    default so the plan rows stay the reference's).
     """
     tps = tokens_per_slot
     recs = {r[0]: tuple(r) for r in records}
@@ -218,7 +221,7 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
             size = cluster.item_size(item)
             pending[item] = PendingMove(item, pending[item].src, loc, size, item_tokens(item, size))
         plan = plan_hybrid(list(pending.values()), boundaries, topology, defer_counts=defer_counts,
-                           max_defer=max_defer)
+                           max_defer=max_defer, split=split)
         rows = [[slot, p.move.item, p.move.src, p.move.dst, p.move.kv_bytes, p.move.tokens, p.mode]
                 for p in plan.assignments]
         out.plan_rows.extend(rows)
