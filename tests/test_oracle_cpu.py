@@ -119,6 +119,53 @@ def test_oracle_reprefill_matches_numpy():
             np.testing.assert_allclose(v, ref[l, t, qc + kvd:], rtol=1e-2, atol=1e-2)
 
 
+def test_oracle_reprefill_pinned_to_hf_llama_projections():
+    """Pin the oracle to a third-party implementation: the C
+    restatement's K/V for tokens [tok0, tok0 + rows) == HF transformers'
+    LlamaAttention k_proj / v_proj / q_proj (nn.Linear, fp32 math on the same
+    bf16 operands, rounded to bf16), scattered by the PagedAttention slot
+    rule block_table[p // 16], p % 16.  RoPE is pinned on the GPU kernel
+    (tests/test_gpu_thirdparty.py)."""
+    import torch
+    from transformers import LlamaConfig
+    from transformers.models.llama.modeling_llama import LlamaAttention
+
+    L, H, Hq, D, dm, rows, tok0, nb = 2, 2, 4, 64, 256, 45, 11, 8
+    cfg = LlamaConfig(hidden_size=dm, num_attention_heads=Hq, num_key_value_heads=H, head_dim=D,
+                      num_hidden_layers=L, intermediate_size=512, vocab_size=64)
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(rows, dm, generator=g).to(torch.bfloat16)
+    att = [LlamaAttention(cfg, layer_idx=l) for l in range(L)]
+    ws = []
+    with torch.no_grad():
+        for a in att:
+            for lin in (a.q_proj, a.k_proj, a.v_proj):
+                lin.weight.copy_((torch.randn(lin.weight.shape, generator=g) / 8).to(torch.bfloat16).float())
+            ws.append(torch.cat([a.q_proj.weight, a.k_proj.weight, a.v_proj.weight]).to(torch.bfloat16))
+    w = torch.stack(ws)                                   # [L][q + 2kv][dm], our layout
+    blocks = np.array([6, 1, 3, 0], dtype=np.int32)       # tokens 0..63
+    pool = np.zeros((L, 2, nb, 16, H, D), dtype=np.uint16)
+    q = np.zeros((L, rows, Hq * D), dtype=np.uint16)
+    as_u16 = lambda t: t.contiguous().view(torch.int16).numpy().view(np.uint16)  # noqa: E731
+    orc.reprefill(orc.desc(L, H, D, 16, nb), pool, blocks, as_u16(x), as_u16(w), rows, dm, Hq * D, tok0, q)
+    pool_f = torch.from_numpy(pool.astype(np.int32) << 16).view(torch.float32)
+    q_f = torch.from_numpy(q.astype(np.int32) << 16).view(torch.float32)
+    pos = torch.arange(tok0, tok0 + rows)
+    blk, slot = torch.from_numpy(blocks).long()[pos // 16], pos % 16
+    with torch.no_grad():
+        for l, a in enumerate(att):
+            k = a.k_proj(x.float()).to(torch.bfloat16).float().view(rows, H, D)
+            v = a.v_proj(x.float()).to(torch.bfloat16).float().view(rows, H, D)
+            qq = a.q_proj(x.float()).to(torch.bfloat16).float()
+            torch.testing.assert_close(pool_f[l, 0, blk, slot], k, atol=1e-2, rtol=1.6e-2)
+            torch.testing.assert_close(pool_f[l, 1, blk, slot], v, atol=1e-2, rtol=1.6e-2)
+            torch.testing.assert_close(q_f[l], qq, atol=1e-2, rtol=1.6e-2)
+    # nothing outside the request's token slots was written
+    mask = np.ones((nb, 16), dtype=bool)
+    mask[blk.numpy(), slot.numpy()] = False
+    assert not pool[:, :, mask].any()
+
+
 # --- C ABI surface ----------------------------------------------------------------
 
 def _header_symbols():
