@@ -689,6 +689,47 @@ class Ring:
                 "value": round(self.ctx["world"] * self.kv_bytes * K / (ms / 1e3) / 1e9, 2), "unit": "GB/s",
                 "ms_per_step": round(ms / K, 4), "steps": K, "bit_exact": ok}
 
+    def library_gloo(self, K: int, group) -> dict:
+        """COMPARISON ONLY: the paper prototype's transport (Gloo P2P for KV,
+        PAPER.md:672): gather on the GPU, D2H into pinned memory, Gloo
+        isend/irecv between the processes, H2D, scatter."""
+        import torch
+        import torch.distributed as dist
+
+        from paper_2501_06709_b200.dist import allreduce_max, exchange_objects
+
+        ri, dev = self.ctx["ri"], self.ctx["device"]
+        t = self.pool.tensor
+        sbl = self.sb_dev.long()
+        dbl = torch.from_numpy(self.db_np).long().to(f"cuda:{dev}")
+        out_h = torch.empty((t.shape[0], t.shape[1], self.n) + tuple(t.shape[3:]), dtype=t.dtype, pin_memory=True)
+        in_h = torch.empty_like(out_h, pin_memory=True)
+
+        def step():
+            out_h.copy_(t.index_select(2, sbl))
+            ops = [dist.P2POp(dist.isend, out_h, ri.send_to, group=group),
+                   dist.P2POp(dist.irecv, in_h, ri.recv_from, group=group)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            t.index_copy_(2, dbl, in_h.to(t.device))
+            torch.cuda.synchronize()
+
+        sent = _checksum(self.pool, self.sb_np, self.n)
+        self.reset()
+        step()
+        got = _checksum(self.pool, self.db_np, self.n)
+        ok = self.ctx["all_ok"](got == exchange_objects(sent)[ri.recv_from])
+        self.ctx["barrier"]()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            step()
+        s = allreduce_max(time.perf_counter() - t0, dev)
+        self.ctx["barrier"]()
+        return {"impl": "Gloo P2P with host staging (gather -> D2H pinned -> gloo isend/irecv -> H2D -> scatter), "
+                        "the paper prototype's transport (PAPER.md:672)",
+                "value": round(self.ctx["world"] * self.kv_bytes * K / s / 1e9, 3), "unit": "GB/s",
+                "ms_per_step": round(1e3 * s / K, 2), "steps": K, "bit_exact": ok, "timing": "host wall clock"}
+
     def close(self):
         import torch
 
@@ -752,8 +793,23 @@ def run_ring(args, ctx) -> int:
             lib["ours_over_library"] = round(main["value"] / lib["value"], 3)
         except Exception as e:
             lib = {"error": repr(e)[:300]}
+        try:
+            import torch.distributed as dist
+
+            gl = ring.library_gloo(2 if world <= 2 else 1, dist.new_group(backend="gloo"))
+            gl["ours_over_library"] = round(main["value"] / gl["value"], 1)
+            lib = dict(lib or {}, paper_transport=gl)
+        except Exception as e:
+            lib = dict(lib or {}, paper_transport={"error": repr(e)[:300]})
     elif shared:
         lib = {"skipped": "ranks share one GPU (gloo control plane; NCCL needs one GPU per rank)"}
+        if not args.no_library:
+            try:
+                import torch.distributed as dist
+
+                lib["paper_transport"] = ring.library_gloo(2, dist.new_group(backend="gloo"))
+            except Exception as e:
+                lib["paper_transport"] = {"error": repr(e)[:300]}
     kv_bytes = ring.kv_bytes
     n, nb = ring.n, ring.nb
     cfg_desc = ring.cfg_desc
@@ -945,6 +1001,53 @@ def run_compact(args, ctx) -> int:
         e2e_lat.append(time.perf_counter() - ts)
     e2e = kv_bytes * K / e2e_s / 1e9
 
+    # ---------------- the library path on the same workload ----------------
+    lib_line = None
+    if not args.no_library:
+        try:
+            v = pool.tensor.view(2 * shape.layers, nb, -1)
+            planes = [v[i] for i in range(2 * shape.layers)]
+            tmp = torch.empty(n, v.shape[2], dtype=v.dtype, device=v.device)
+            sl, dl = sb_dev.long(), db_dev.long()
+
+            def view_arm(a, b):      # one gather + one scatter over the [layers*2, blocks, piece] view
+                v.index_copy_(1, b, v.index_select(1, a))
+
+            def plane_arm(a, b):     # per (layer, K|V) plane: dim-0 index ops (torch's contiguous-row path)
+                for pv in planes:
+                    torch.index_select(pv, 0, a, out=tmp)
+                    pv.index_copy_(0, b, tmp)
+
+            arms = {}
+            for name, fn in (("index_select+index_copy_ on the [layers*2, blocks, piece] view", view_arm),
+                             ("index_select+index_copy_ per [blocks, piece] plane", plane_arm)):
+                torch.cuda.synchronize()
+                sent_now = _checksum(pool, sb_np, n)
+                with torch.cuda.stream(stream):
+                    fn(sl, dl)
+                stream.synchronize()
+                ok = _checksum(pool, db_np, n) == sent_now
+                KL = min(K, 20)
+                with torch.cuda.stream(stream):
+                    for _ in range(2):
+                        fn(sl, dl)
+                    l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    l0.record(stream)
+                    for i in range(KL):
+                        fn(*((sl, dl) if i % 2 == 0 else (dl, sl)))
+                    l1.record(stream)
+                stream.synchronize()
+                lms = l0.elapsed_time(l1) / KL
+                arms[name] = {"value": round(kv_bytes / lms / 1e6, 2), "ms_per_step": round(lms, 4), "steps": KL,
+                              "bit_exact": bool(ok)}
+            best = max(arms, key=lambda k: arms[k]["value"])
+            lib_line = {"impl": f"torch {best} (the faster torch arm; both below)", "unit": "GB/s",
+                        **arms[best], "arms": arms,
+                        "ours_over_library": round((kv_bytes / (elapsed_ms / K) / 1e6) / arms[best]["value"], 3)}
+            del tmp
+        except Exception as e:
+            lib_line = {"error": repr(e)[:300]}
+
     hbm_peak, _, _, psrc = _peaks()
     alg_bytes = 2 * kv_bytes  # read + write, same HBM
     ach = alg_bytes / (avg_launch_ms / 1e3) / 1e9
@@ -973,6 +1076,7 @@ def run_compact(args, ctx) -> int:
                 "latency_definition": "one synchronous call through the API: issue -> result row on the host",
                 "path": "MigrationExecutor.compact(stream_ordered) -> kvm_compact(host block lists) -> "
                         "table row D2H -> host waits for the row (next step issued meanwhile)"},
+        "library": lib_line,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -1084,7 +1188,8 @@ def main(argv=None) -> int:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the re-prefill / decode measurements reported beside the headline (N=1)")
-    ap.add_argument("--no-library", action="store_true", help="skip the NCCL ring comparison (N>1)")
+    ap.add_argument("--no-library", action="store_true",
+                    help="skip the library-path comparison (torch index_select/index_copy_ at N=1, NCCL ring at N>1)")
     ap.add_argument("--extra-workloads", default=None,
                     help="comma list of workloads measured beside the headline at N>1 (default 70b-16k)")
     ap.add_argument("--shared-gpu", action="store_true",

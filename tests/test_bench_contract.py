@@ -69,6 +69,8 @@ def test_gpu_arm_contract():
     assert k["reprefill_13b_s1360"]["cublas_same_shape"]["ms"] > 0
     assert k["decode_7b_4k_32l"]["unit"] == "GB/s" and 0.3 < k["decode_7b_4k_32l"]["frac"] < 1.5
     assert 0 < k["small_move_7b_1block"]["issue_to_landed_us_p50"] < 1000
+    lib = d["library"]   # the library path on the same workload, timed in the same run
+    assert lib["bit_exact"] is True and lib["value"] > 0 and lib["ours_over_library"] > 1
 
 
 @pytest.mark.gpu
@@ -90,6 +92,7 @@ def test_gpu_arm_plain_python_two_ranks():
     assert d["e2e"]["value"] > 0 and d["e2e"]["row_ok"] is True
     assert d["config"]["engine"] in ("bulk", "ldg") and set(d["config"]["engine_ab"]) == {"bulk", "ldg"}
     assert "nvlink_counters" in d["roofline"] and d["gpu_launches"] > 0
+    assert d["library"]["paper_transport"]["bit_exact"] is True and d["library"]["paper_transport"]["value"] > 0
 
 
 @pytest.mark.gpu

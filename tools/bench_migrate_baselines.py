@@ -7,7 +7,13 @@ pool; 7B, 4k tokens = 2 GiB by default), inputs > L2, CUDA events, median of
 
   ours-bulk     kvm_compact, TMA bulk engine (one launch)
   ours-ldg      kvm_compact, 128-bit LDG/STG engine (one launch)
-  torch         pool[:, :, dst] = pool[:, :, src]  (index gather + index put)
+  torch-index   v = pool.view(L*2, NB, piece); v.index_copy_(1, dst, v.index_select(1, src))
+                (the library path to beat)
+  torch-index-per-plane  the same per (layer, K|V) plane [NB, piece]: dim-0 index_select
+                + index_copy_ (torch's contiguous-row fast path), 2 * layers * 2 kernels
+  torch         pool[:, :, dst] = pool[:, :, src]  (advanced-index gather + put)
+  vllm-swap_blocks  vLLM 0.22's block copy (_C_cache_ops.swap_blocks) per plane: how
+                vLLM moves KV blocks (one cudaMemcpyAsync per block)
   memcpy-batch  cudaMemcpyBatchAsync: one call, one (src, dst, 128 KiB) entry per
                 (layer, K|V, block) piece -> copy engines
   memcpy-loop   cudaMemcpyAsync per piece (host-issued, 16 384 calls)
@@ -92,6 +98,38 @@ def main():
                                           ctypes.c_void_p(dst.data_ptr()), n, None, engine, sptr))
         return run
 
+    v = pool.tensor.view(2 * shape.layers, nb, -1)
+
+    def torch_index_arm():
+        src, dst = (db_l, sb_l) if flip[0] else (sb_l, db_l)
+        flip[0] = not flip[0]
+        v.index_copy_(1, dst, v.index_select(1, src))
+
+    planes_v = [v[i] for i in range(2 * shape.layers)]   # [NB, piece] each: dim-0 index ops (fast path)
+    tmp = torch.empty(n, v.shape[2], dtype=v.dtype, device=v.device)
+
+    def torch_plane_arm():
+        src, dst = (db_l, sb_l) if flip[0] else (sb_l, db_l)
+        flip[0] = not flip[0]
+        for pv in planes_v:
+            torch.index_select(pv, 0, src, out=tmp)
+            pv.index_copy_(0, dst, tmp)
+
+    try:
+        import vllm._custom_ops as vops
+        vmap = {"f": torch.from_numpy(np.stack([sb, db], 1).astype(np.int64)),
+                "b": torch.from_numpy(np.stack([db, sb], 1).astype(np.int64))}
+        # vLLM's per-layer caches are the pool's (layer, K|V) planes, [NB][16][H][D] contiguous
+        kv_planes = [pool.tensor[l, kv] for l in range(shape.layers) for kv in range(2)]
+    except Exception:
+        vops = None
+
+    def vllm_arm():
+        m = vmap["b" if flip[0] else "f"]
+        flip[0] = not flip[0]
+        for pl in kv_planes:
+            vops.swap_blocks(pl, pl, pb, m)
+
     def torch_arm():
         src, dst = (db_l, sb_l) if flip[0] else (sb_l, db_l)
         flip[0] = not flip[0]
@@ -140,7 +178,10 @@ def main():
         for i in range(cnt):
             cudart.cudaMemcpyAsync(ctypes.c_void_p(d[i]), ctypes.c_void_p(src[i]), ctypes.c_size_t(pb), 3, sptr)
 
-    arms = [("ours-bulk", ours(_native.KVM_F_ENGINE_BULK)), ("ours-ldg", ours(0)), ("torch", torch_arm)]
+    arms = [("ours-bulk", ours(_native.KVM_F_ENGINE_BULK)), ("ours-ldg", ours(0)), ("torch-index", torch_index_arm),
+            ("torch-index-per-plane", torch_plane_arm), ("torch", torch_arm)]
+    if vops is not None:
+        arms.append(("vllm-swap_blocks", vllm_arm))
     if cudart is not None:
         arms += [("memcpy-batch", batch_arm), ("memcpy-loop", loop_arm)]
     for name, fn in arms:
