@@ -850,6 +850,17 @@ def run_ring(args, ctx) -> int:
                                              "mean TX bytes per launch (null when the box does not expose them)"}
     line = None
     if ri.rank == 0:
+        md = None
+        if not shared and ctx["ndev"] >= 2 and not args.no_multidev_checks:
+            # the single-process cross-device path (executor over pools on GPUs 0 and 1, stream-ordered
+            # moves, cross-device split, fused pull over the peer mapping, pipelined decode on the peer)
+            try:
+                sys.path.insert(0, os.path.join(ROOT, "tools"))
+                from multidev_check import run_checks
+
+                md = run_checks(0, 1)
+            except Exception as e:
+                md = {"all_ok": False, "error": repr(e)[:300]}
         cpu = None if args.no_cpu_baseline else cpu_baseline(args, ring.shape, ring.tokens)
         line = {
             "metric": "kv_migration_GBps", "value": round(main["value"], 2), "unit": "GB/s", "n_gpus": world,
@@ -873,7 +884,8 @@ def run_ring(args, ctx) -> int:
                            "step_p50": round(main["step_p50"], 4), "step_p99": round(main["step_p99"], 4),
                            "step_definition": "push + wait until the incoming move's done flag is visible here "
                                               "(ld.acquire.sys)"},
-            "bit_exact": bool(bit_exact),
+            "bit_exact": bool(bit_exact and e2e["row_ok"] and (md is None or md.get("all_ok", False))),
+            "multi_device_checks": md,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e["value"], 2), "unit": "GB/s", "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
@@ -1192,6 +1204,8 @@ def main(argv=None) -> int:
                     help="skip the library-path comparison (torch index_select/index_copy_ at N=1, NCCL ring at N>1)")
     ap.add_argument("--extra-workloads", default=None,
                     help="comma list of workloads measured beside the headline at N>1 (default 70b-16k)")
+    ap.add_argument("--no-multidev-checks", action="store_true",
+                    help="skip rank 0's single-process cross-device checks (tools/multidev_check.py) at N>1")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="allow N ranks on fewer GPUs (functional test of the IPC path; no NVLink)")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)

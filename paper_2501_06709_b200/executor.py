@@ -116,8 +116,15 @@ class MigrationExecutor:
     """
 
     def __init__(self, pools: Dict[int, KVPool], tables: Optional[Dict[int, BlockTable]] = None,
-                 engine: str = "bulk", reprefill: Optional[Callable] = None, timing: bool = False):
+                 engine: str = "bulk", reprefill: Optional[Callable] = None, timing: bool = False,
+                 split_kernels: str = "auto"):
         import torch
+
+        if split_kernels not in ("auto", "fused", "two"):
+            raise ConfigError("split_kernels must be 'auto', 'fused' or 'two'")
+        # split_transfer: "auto" = one fused kvm_split_migrate when source and destination pools share a
+        # device, else kvm_migrate (source) + kvm_reprefill (destination); "two" forces the latter
+        self.split_kernels = split_kernels
 
         self.timing = timing
         self._events: Dict[int, list] = {}
@@ -391,7 +398,7 @@ class MigrationExecutor:
                     rec.tokens_moved += res.tokens
                 elif pm.mode == SPLIT_TRANSFER:
                     self._issue_split(pm, rec, rid, res, src_pool, dst_pool, dst_blocks, table_for)
-                    report.launches += 1 if src_pool.device == dst_pool.device else 2
+                    report.launches += 1 if (src_pool.device == dst_pool.device and self.split_kernels != "two") else 2
                 else:  # TOKEN_TRANSFER
                     s = self.ordered_stream(dst_pool.device)
                     self._wait_fences(s, dst_pool.device, [dst_pool])
@@ -585,7 +592,9 @@ class MigrationExecutor:
         plan = make_split(n, n - prefix, sh.block_tokens)
         eng = self.reprefill
         dev = dst_pool.device
-        cross = src_pool.device != dev
+        cross = src_pool.device != dev or self.split_kernels == "two"
+        if self.split_kernels == "fused" and src_pool.device != dev:
+            raise ConfigError("split_kernels='fused' needs the source pool on the destination's device")
         flags = torch.zeros(2, dtype=torch.int32, device=f"cuda:{dev}") if cross else None
         s = self.ordered_stream(dev)
         self._wait_fences(s, dev, [dst_pool])
