@@ -861,6 +861,19 @@ def run_ring(args, ctx) -> int:
                 md = run_checks(0, 1)
             except Exception as e:
                 md = {"all_ok": False, "error": repr(e)[:300]}
+        if not shared and ctx["ndev"] >= 8 and world >= 8 and args.config5_slots > 0:
+            # configs[4] at real shapes: the live loop (native scheduler -> planner -> executor) with one
+            # logical GPU per B200, full Llama-2-7B KV, slot-limited; bytes fingerprint-checked
+            try:
+                sys.path.insert(0, os.path.join(ROOT, "tools"))
+                from online_loop import run_online
+
+                torch.cuda.empty_cache()
+                extras["config5_online_full_7b"] = run_online(
+                    os.path.join(ROOT, "tests", "golden", "trace_7b_c48g_seed0.json"), shape="full",
+                    verify_every=100, max_slots=args.config5_slots, devices=list(range(8)))
+            except Exception as e:
+                extras["config5_online_full_7b"] = {"error": repr(e)[:300]}
         cpu = None if args.no_cpu_baseline else cpu_baseline(args, ring.shape, ring.tokens)
         line = {
             "metric": "kv_migration_GBps", "value": round(main["value"], 2), "unit": "GB/s", "n_gpus": world,
@@ -1206,6 +1219,8 @@ def main(argv=None) -> int:
                     help="comma list of workloads measured beside the headline at N>1 (default 70b-16k)")
     ap.add_argument("--no-multidev-checks", action="store_true",
                     help="skip rank 0's single-process cross-device checks (tools/multidev_check.py) at N>1")
+    ap.add_argument("--config5-slots", type=int, default=400,
+                    help="at N>=8: slots of the configs[4] live loop at full 7B shapes run by rank 0 (0: skip)")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="allow N ranks on fewer GPUs (functional test of the IPC path; no NVLink)")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)

@@ -229,8 +229,9 @@ class MigrationExecutor:
         pool = self.pool(r.gpu, r.model)
         need = pool.shape.blocks_for(tokens) - len(r.blocks)
         if need > 0:
+            old = len(r.blocks)
             r.blocks = np.concatenate([r.blocks, pool.allocator.alloc(need)])
-            self._table_set(r.gpu, r.model, rid, r.blocks)
+            self._table_set(r.gpu, r.model, rid, r.blocks, start=old)
         r.tokens = tokens
 
     def release(self, rid: int) -> None:
@@ -698,12 +699,14 @@ class MigrationExecutor:
         except KeyError:
             raise NotPlaced(f"request {rid} is not resident") from None
 
-    def _table_set(self, gpu: int, model: str, rid: int, blocks: np.ndarray) -> None:
+    def _table_set(self, gpu: int, model: str, rid: int, blocks: np.ndarray, start: int = 0) -> None:
+        """Host mirror now; the device row entries [start, len) are batched with
+        every other admission / growth and written at the table's next flush
+        (before any kernel or reader uses the rows)."""
         t = self._table(gpu, model)
         if t is None:
             return
-        t.set_host(rid, blocks)
-        t.rows[t.slot(rid), :len(blocks)].copy_(_as_i32_tensor(blocks, t.device))
+        t.stage(rid, blocks, start)
 
 
 def _geometry(pool) -> tuple:

@@ -89,6 +89,7 @@ class BlockAllocator:
             raise ConfigError("num_blocks must be > 0")
         self.num_blocks = num_blocks
         self._free = np.ones(num_blocks, dtype=bool)
+        self._lo = 0    # every id below _lo is in use (lower bound of the lowest free id)
 
     @property
     def n_free(self) -> int:
@@ -97,10 +98,20 @@ class BlockAllocator:
     def alloc(self, n: int) -> np.ndarray:
         if n < 0:
             raise ValueError("n must be >= 0")
-        ids = np.flatnonzero(self._free)[:n]
-        if len(ids) < n:
-            raise RequestTooLarge(f"pool has {len(ids)} free blocks, {n} requested")
+        if n == 0:
+            return np.zeros(0, dtype=np.int32)
+        parts, got, i = [], 0, self._lo
+        while got < n and i < self.num_blocks:   # scan windows upward from the lowest possibly-free id
+            w = self._free[i:i + max(1024, 2 * (n - got))]
+            ids = np.flatnonzero(w)[:n - got] + i
+            parts.append(ids)
+            got += len(ids)
+            i += len(w)
+        if got < n:
+            raise RequestTooLarge(f"pool has {self.n_free} free blocks, {n} requested")
+        ids = np.concatenate(parts) if len(parts) > 1 else parts[0]
         self._free[ids] = False
+        self._lo = int(ids[-1]) + 1
         return ids.astype(np.int32)
 
     def take(self, blocks: Iterable[int]) -> None:
@@ -119,6 +130,8 @@ class BlockAllocator:
         if self._free[b].any():
             raise ValueError("double free")
         self._free[b] = True
+        if b.size:
+            self._lo = min(self._lo, int(b.min()))
 
     def free_mask(self) -> np.ndarray:
         return self._free.copy()
@@ -223,12 +236,26 @@ class BlockTable:
 
         self.device = device
         self.max_blocks = max_blocks
-        self.rows = torch.full((max_requests, max_blocks), -1, dtype=torch.int32,
-                               device=f"cuda:{device}")
+        self._rows = torch.full((max_requests, max_blocks), -1, dtype=torch.int32,
+                                device=f"cuda:{device}")
         self._slot_of: Dict[int, int] = {}
         self._free_slots = list(range(max_requests - 1, -1, -1))
         self._dirty: set = set()   # freed slots whose row still holds the old request's blocks
         self.host: Dict[int, np.ndarray] = {}
+        # host-side row updates (admission, decode growth) awaiting one batched write
+        self._staged: Dict[int, tuple] = {}    # slot -> (first entry to write, blocks)
+        self._bufs: list = [None, None]        # pinned (index, value) staging, double-buffered
+        self._buf_ev: list = [None, None]
+        self._flip = 0
+
+    @property
+    def rows(self):
+        """The device rows [max_requests][max_blocks].  Row updates staged by
+        the host (stage()) are flushed first — one H2D copy + one scatter on
+        the current stream for all of them — so every reader sees them."""
+        if self._staged:
+            self.flush()
+        return self._rows
 
     def slot(self, rid: int) -> int:
         if rid not in self._slot_of:
@@ -237,9 +264,52 @@ class BlockTable:
             s = self._free_slots.pop()
             if s in self._dirty:   # cleared on reuse, not on release (keeps drop() off the pause path)
                 self._dirty.discard(s)
-                self.rows[s].fill_(-1)
+                self._rows[s].fill_(-1)
             self._slot_of[rid] = s
         return self._slot_of[rid]
+
+    def stage(self, rid: int, blocks: np.ndarray, start: int = 0) -> None:
+        """Host mirror := blocks; device entries [start, len(blocks)) are
+        written at the next flush() (any read of `rows` / `row_ptr` flushes)."""
+        if len(blocks) > self.max_blocks:
+            raise RequestTooLarge(f"{len(blocks)} blocks > table width {self.max_blocks}")
+        s = self.slot(rid)
+        b = np.asarray(blocks, dtype=np.int32)
+        self.host[rid] = b
+        prev = self._staged.get(s)
+        self._staged[s] = (min(start, prev[0]) if prev is not None else start, b)
+
+    def flush(self) -> None:
+        """Write every staged row update to the device: one pinned H2D copy of
+        (flat index, block id) pairs and one index_copy_ into the rows, on the
+        current stream."""
+        import torch
+
+        staged, self._staged = self._staged, {}
+        parts = [(s, st, b) for s, (st, b) in staged.items() if st < len(b)]
+        if not parts:
+            return
+        W = self.max_blocks
+        idx = np.concatenate([s * W + np.arange(st, len(b), dtype=np.int64) for s, st, b in parts])
+        val = np.concatenate([b[st:].astype(np.int64) for s, st, b in parts])
+        n = len(idx)
+        k = self._flip
+        self._flip ^= 1
+        buf = self._bufs[k]
+        if buf is None or buf.shape[1] < n:
+            buf = torch.empty((2, max(n, 1024, 0 if buf is None else 2 * buf.shape[1])), dtype=torch.int64,
+                              pin_memory=True)
+            self._bufs[k] = buf
+        elif self._buf_ev[k] is not None:
+            self._buf_ev[k].synchronize()   # the copy that last read this staging buffer is done
+        bn = buf.numpy()
+        bn[0, :n] = idx
+        bn[1, :n] = val
+        dev = buf[:, :n].to(self._rows.device, non_blocking=True)
+        self._rows.view(-1).index_copy_(0, dev[0], dev[1].to(torch.int32))
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self._rows.device))
+        self._buf_ev[k] = ev
 
     def has(self, rid: int) -> bool:
         return rid in self._slot_of
@@ -249,7 +319,7 @@ class BlockTable:
         return len(self._free_slots)
 
     def row_ptr(self, rid: int) -> int:
-        return self.rows.data_ptr() + self.slot(rid) * self.max_blocks * 4
+        return self.rows.data_ptr() + self.slot(rid) * self.max_blocks * 4   # (flushes staged updates)
 
     def set_host(self, rid: int, blocks: np.ndarray) -> None:
         if len(blocks) > self.max_blocks:
@@ -261,6 +331,7 @@ class BlockTable:
         self.host.pop(rid, None)
         s = self._slot_of.pop(rid, None)
         if s is not None:   # nobody reads a released row; it is reset to -1 when the slot is reused
+            self._staged.pop(s, None)
             self._dirty.add(s)
             self._free_slots.append(s)
 

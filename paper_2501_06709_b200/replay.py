@@ -92,44 +92,80 @@ class Fingerprints:
         self.recomputed: set = set()
         self.prefix_only: Dict[int, int] = {}  # split_transfer: rid -> leading blocks still carrying copies
         self._stamped: Dict[int, int] = {}   # rid -> number of blocks stamped
+        self._marked: set = set()            # stamps awaiting flush()
 
     def stamp(self, rid: int) -> None:
-        """Write the fingerprint into blocks the request gained since last time."""
-        if rid in self.recomputed:
-            return
+        """Write the fingerprint into blocks the request gained since last time (now)."""
+        self.mark(rid)
+        self.flush()
+
+    def mark(self, rid: int) -> None:
+        """Like stamp(), but batched: written at the next flush() (one write per
+        pool for every marked request).  Call flush() before anything copies or
+        reads the request's blocks."""
+        if rid not in self.recomputed:
+            self._marked.add(rid)
+
+    def flush(self) -> None:
         import torch
 
-        r = self.ex.where(rid)
-        start = self._stamped.get(rid, 0)
-        if start >= len(r.blocks):
-            return
-        pool = self.ex.pool(r.gpu, r.model)
-        idx = torch.from_numpy(r.blocks[start:].astype(np.int64)).to(pool.tensor.device)
-        pool.tensor.view(torch.int16)[:, :, idx] = self.values(rid, start, len(r.blocks), pool)
-        self._stamped[rid] = len(r.blocks)
+        marked, self._marked = self._marked, set()
+        by_pool: Dict[int, list] = {}
+        for rid in marked:
+            r = self.ex.loc.get(rid)
+            if r is None or rid in self.recomputed:
+                continue
+            start = self._stamped.get(rid, 0)
+            if start >= len(r.blocks):
+                continue
+            pool = self.ex.pool(r.gpu, r.model)
+            by_pool.setdefault(id(pool), [pool, [], [], []])
+            e = by_pool[id(pool)]
+            e[1].append(np.full(len(r.blocks) - start, rid, dtype=np.int64))
+            e[2].append(np.arange(start, len(r.blocks), dtype=np.int64))
+            e[3].append(r.blocks[start:].astype(np.int64))
+            self._stamped[rid] = len(r.blocks)
+        for pool, rids, idx, blocks in by_pool.values():
+            dev = pool.tensor.device
+            rids_t = torch.from_numpy(np.concatenate(rids)).to(dev)
+            idx_t = torch.from_numpy(np.concatenate(idx)).to(dev)
+            blk_t = torch.from_numpy(np.concatenate(blocks)).to(dev)
+            v = self._values(rids_t, idx_t, pool)                  # [L][2][n]
+            pool.tensor.view(torch.int16)[:, :, blk_t] = v[..., None, None, None].expand(
+                *v.shape, *pool.view_shape[3:])
 
     def forget(self, rid: int) -> None:
         self._stamped.pop(rid, None)
         self.recomputed.discard(rid)
         self.prefix_only.pop(rid, None)
+        self._marked.discard(rid)
+
+    @staticmethod
+    def _values(rids, idx, pool):
+        """Fingerprint of (request, logical block, layer, K|V): int16 [L][2][n]."""
+        import torch
+
+        L = pool.shape.layers
+        dev = rids.device
+        base = (rids * 7919 + idx * 104729) % 16381
+        lay = torch.arange(L, device=dev, dtype=torch.int64)[:, None, None] * 2
+        kv = torch.arange(2, device=dev, dtype=torch.int64)[None, :, None]
+        return ((base[None, None, :] * 2 + lay * 3 + kv) % 32749 - 16374).to(torch.int16)
 
     @staticmethod
     def values(rid, lo, hi, pool):
         import torch
 
-        L = pool.shape.layers
         dev = pool.tensor.device
-        i = torch.arange(lo, hi, device=dev, dtype=torch.int32)
-        base = (rid * 7919 + i * 104729) % 16381
-        lay = torch.arange(L, device=dev, dtype=torch.int32)[:, None, None] * 2
-        kv = torch.arange(2, device=dev, dtype=torch.int32)[None, :, None]
-        v = (base[None, None, :] * 2 + lay * 3 + kv) % 32749 - 16374
-        return v.to(torch.int16)[..., None, None, None].expand(L, 2, hi - lo, *pool.view_shape[3:])
+        i = torch.arange(lo, hi, device=dev, dtype=torch.int64)
+        v = Fingerprints._values(torch.full_like(i, rid), i, pool)
+        return v[..., None, None, None].expand(*v.shape, *pool.view_shape[3:])
 
     def verify(self) -> int:
         """Number of resident requests checked; raises on the first mismatch."""
         import torch
 
+        self.flush()
         n = 0
         for rid, r in self.ex.loc.items():
             if rid in self.recomputed:
@@ -160,12 +196,12 @@ class FingerprintedExecutor:
 
     def admit(self, rid, gpu, tokens, model=None):
         r = self.ex.admit(rid, gpu, tokens, model=model)
-        self.fp.stamp(rid)
+        self.fp.mark(rid)
         return r
 
     def grow(self, rid, tokens):
         r = self.ex.grow(rid, tokens)
-        self.fp.stamp(rid)
+        self.fp.mark(rid)
         return r
 
     def release(self, rid):
@@ -173,6 +209,7 @@ class FingerprintedExecutor:
         self.fp.forget(rid)
 
     def execute(self, plan, members_of=None):
+        self.fp.flush()              # the stamps must be in the blocks before they are copied
         report = self.ex.execute(plan, members_of=members_of)
         for rec in report.records:
             if rec.mode == TOKEN_TRANSFER:
@@ -183,6 +220,7 @@ class FingerprintedExecutor:
         return report
 
     def reconcile(self, target_of, skip=()):
+        self.fp.flush()
         report = self.ex.reconcile(target_of, skip=skip)
         self.reports.append(report)
         return report
@@ -225,7 +263,7 @@ class TraceReplay:
     # -- fingerprints ------------------------------------------------------------
     def _stamp(self, rid: int) -> None:
         if self.fingerprint:
-            self.fp.stamp(rid)
+            self.fp.mark(rid)
 
     def verify(self) -> int:
         return self.fp.verify() if self.fingerprint else 0
@@ -272,6 +310,8 @@ class TraceReplay:
                 members[item] = mem
                 if mode != TOKEN_TRANSFER:
                     ref_bytes += kvb
+            if self.fingerprint and planned:
+                self.fp.flush()
             t0 = time.perf_counter()
             report = ex.execute(planned, members_of=lambda it: members.get(it, [it])) if planned else None
             dt = time.perf_counter() - t0

@@ -117,7 +117,7 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
               duration_slots: int = 0, executor=None, reserve_final: bool = False,
               models: Optional[Dict[int, str]] = None,
               on_slot: Optional[Callable[[int, list], None]] = None, reconcile: bool = True,
-              split: bool = False) -> LoopResult:
+              split: bool = False, max_slots: Optional[int] = None) -> LoopResult:
     """Run the slot loop; `records` are (request_id, arrival_slot, prompt, response).
 
     `bpt` is the reference's kv_bytes_per_token (config.py:92), or — multi-LLM
@@ -132,7 +132,9 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
     moves the reference's refresh drops, sim.py:207-213); counted in
     `reconciled_moves` / `reconciled_bytes`, not in the plan rows.  split:
     the planner's split mode (plan_hybrid(split=True), extension, off by
-    default so the plan rows stay the reference's).
+    default so the plan rows stay the reference's).  max_slots: stop after
+    that many slots (a bounded prefix of the run; the rows so far are the
+    reference's).
     """
     tps = tokens_per_slot
     recs = {r[0]: tuple(r) for r in records}
@@ -256,6 +258,8 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
         if on_slot is not None:
             on_slot(slot, rows)
         slot += 1
+        if max_slots is not None and slot >= max_slots:
+            break
         if slot > horizon + 10 ** 6:
             raise RuntimeError("slot loop failed to drain")
     return out

@@ -149,3 +149,17 @@ def test_online_loop_split_mode_executes_splits():
     ref = run_slots(trace, MellScheduler(cl2, priority_cfg=PriorityConfig(), batching=True), cl2, topo, bounds,
                     bpt=524_288, tokens_per_slot=10, duration_slots=200)
     assert not any(r[6] == SPLIT_TRANSFER for r in ref.plan_rows)
+
+
+def test_online_loop_tool_dry_run_sizing():
+    """tools/online_loop.run_online (the configs[4] driver bench.py runs at N=8
+    with full shapes): pools sized from the host-only dry run hold the run
+    (no RequestTooLarge), decisions over the slots run equal the reference's,
+    fingerprints hold.  Mini shapes here (one GPU)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from online_loop import run_online
+
+    res = run_online(os.path.join(ROOT, "tests", "golden", "trace_multillm_7b13b_seed0.json"), shape="mini",
+                     verify_every=50, max_slots=700)
+    assert res["decisions_match_reference"] is True and res["slots"] == 700
+    assert res["fingerprint_checks"] > 0 and res["bytes_moved"] > 0
