@@ -36,6 +36,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import datetime
 import json
 import os
 import platform
@@ -124,6 +125,34 @@ def _kernel_extras(device: int) -> dict:
             lib_ms.append(timed(cublas, reps=3))
         ms, lms = statistics.median(ours_ms), statistics.median(lib_ms)
         tf, ltf = flops / ms / 1e9, flops / lms / 1e9
+        # power roofline: board energy per launch (NVML counter) over ~1 s of back-to-back launches of
+        # each arm; at the board limit, time = energy per launch / limit (tools/power_roofline.py)
+        power = None
+        try:
+            from paper_2501_06709_b200.telemetry import ClockSampler, EnergyMeter
+
+            em = EnergyMeter(device)
+            if em.error is None:
+                power = {"limit_w": em.limit_w}
+                for name, fn, t in (("ours", lambda: reprefill(pool, x, w, blocks, stream=st), ms),
+                                    ("cublas", cublas, lms)):
+                    with torch.cuda.stream(st), ClockSampler(device) as clk:
+                        r = em.measure(fn, max(5, int(1000 / t)), st.synchronize)
+                    if "joules_per_call" in r:
+                        r["tflop_per_joule"] = round(flops / 1e12 / r["joules_per_call"], 3)
+                        r["cap_bound_ms"] = round(r["joules_per_call"] / em.limit_w * 1e3, 4)
+                    r["sm_mhz"] = clk.summary()["sm_mhz"]
+                    power[name] = r
+                if "tflop_per_joule" in power["ours"] and "tflop_per_joule" in power["cublas"]:
+                    power["ours_over_cublas_energy_eff"] = round(power["ours"]["tflop_per_joule"] /
+                                                                 power["cublas"]["tflop_per_joule"], 4)
+                power["definition"] = ("NVML board energy per launch over ~1 s of back-to-back launches; "
+                                       "cap_bound_ms = joules per launch / enforced power limit: the "
+                                       "shortest time at that energy per launch")
+            else:
+                power = {"error": em.error}
+        except Exception as e:
+            power = {"error": repr(e)[:200]}
         out["reprefill_13b_s1360"] = {
             "kernel": "reprefill_pair_kernel (tcgen05 cta_group::2)", "ms": round(ms, 4),
             "achieved": round(tf, 1), "peak": burst, "unit": "TFLOP/s", "frac": round(tf / burst, 4),
@@ -131,7 +160,8 @@ def _kernel_extras(device: int) -> dict:
             "frac_vs_sustained": round(tf / sustained, 4),
             "cublas_same_shape": {"impl": "torch.matmul per layer (cuBLAS), GEMM only, no K/V scatter",
                                   "ms": round(lms, 4), "achieved": round(ltf, 1),
-                                  "frac": round(ltf / burst, 4), "ours_over_cublas": round(lms / ms, 4)}}
+                                  "frac": round(ltf / burst, 4), "ours_over_cublas": round(lms / ms, 4)},
+            "power": power}
         del pool, x, w, outs
     except Exception as e:  # reported, never fatal for the headline
         out["reprefill_13b_s1360"] = {"error": str(e)[:300]}
@@ -756,6 +786,50 @@ def _roofline_nvlink(kv_bytes: int, push_ms: float, engine: str, traffic) -> dic
             "traffic": traffic}
 
 
+def _tool_json(script: str, argv: list, timeout_s: float) -> dict:
+    """Run tools/<script> in a child process (its own CUDA contexts) and return
+    the JSON it writes to --out.  A fault there (illegal address, hang until
+    the timeout) is reported in the line instead of killing this rank."""
+    import tempfile
+
+    fd, out = tempfile.mkstemp(suffix=".json")
+    os.close(fd)
+    t0 = time.perf_counter()
+    try:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", script), *argv, "--out", out],
+                           capture_output=True, text=True, timeout=timeout_s, cwd=ROOT)
+        try:
+            with open(out) as f:
+                res = json.load(f)
+        except (OSError, ValueError):
+            res = {"all_ok": False, "error": f"rc={r.returncode}: " + (r.stderr or r.stdout)[-400:]}
+    except subprocess.TimeoutExpired:
+        res = {"all_ok": False, "error": f"timed out after {timeout_s:.0f} s"}
+    finally:
+        try:
+            os.unlink(out)
+        except OSError:
+            pass
+    res["subprocess_s"] = round(time.perf_counter() - t0, 1)
+    return res
+
+
+def _peer_probe(args, ctx) -> dict:
+    """Rank 0, before any timing, in a child process: the single-process
+    cross-device checks on GPUs 0 and 1 (tools/multidev_check.py), including a
+    push with each copy engine into the peer's pool.  Every rank then waits on
+    a CPU (gloo) barrier and receives the result, so the engine A/B only
+    offers the TMA bulk engine if its peer stores were bit-exact here."""
+    import torch.distributed as dist
+
+    md = None
+    if ctx["ri"].rank == 0 and not ctx["shared"] and ctx["ndev"] >= 2 and not args.no_multidev_checks:
+        md = _tool_json("multidev_check.py", ["--a", "0", "--b", "1"], timeout_s=600)
+    box = [md]
+    dist.broadcast_object_list(box, src=0, group=ctx["cpu_group"])
+    return box[0]
+
+
 def run_ring(args, ctx) -> int:
     """N > 1: the ring measurement, its evidence and extras."""
     import torch
@@ -764,8 +838,10 @@ def run_ring(args, ctx) -> int:
     from paper_2501_06709_b200.telemetry import ClockSampler, NvlinkMeter, merge_clocks
 
     ri, world, dev, shared = ctx["ri"], ctx["world"], ctx["device"], ctx["shared"]
+    md = _peer_probe(args, ctx)
+    bulk_peer_ok = md is None or bool(md.get("engine_push_over_peer", {}).get("bulk", {}).get("ok", False))
     ring = Ring(ctx, args.workload)
-    engines = [args.engine] if args.engine else ["bulk", "ldg"]
+    engines = [args.engine] if args.engine else (["bulk", "ldg"] if bulk_peer_ok else ["ldg"])
     gates = {e: ring.gate(e) for e in engines}
     ab = {}
     if len(engines) > 1:   # start-up A/B to the peer, behind the bit-exact gate: keep the faster engine
@@ -850,30 +926,15 @@ def run_ring(args, ctx) -> int:
                                              "mean TX bytes per launch (null when the box does not expose them)"}
     line = None
     if ri.rank == 0:
-        md = None
-        if not shared and ctx["ndev"] >= 2 and not args.no_multidev_checks:
-            # the single-process cross-device path (executor over pools on GPUs 0 and 1, stream-ordered
-            # moves, cross-device split, fused pull over the peer mapping, pipelined decode on the peer)
-            try:
-                sys.path.insert(0, os.path.join(ROOT, "tools"))
-                from multidev_check import run_checks
-
-                md = run_checks(0, 1)
-            except Exception as e:
-                md = {"all_ok": False, "error": repr(e)[:300]}
         if not shared and ctx["ndev"] >= 8 and world >= 8 and args.config5_slots > 0:
             # configs[4] at real shapes: the live loop (native scheduler -> planner -> executor) with one
-            # logical GPU per B200, full Llama-2-7B KV, slot-limited; bytes fingerprint-checked
-            try:
-                sys.path.insert(0, os.path.join(ROOT, "tools"))
-                from online_loop import run_online
-
-                torch.cuda.empty_cache()
-                extras["config5_online_full_7b"] = run_online(
-                    os.path.join(ROOT, "tests", "golden", "trace_7b_c48g_seed0.json"), shape="full",
-                    verify_every=100, max_slots=args.config5_slots, devices=list(range(8)))
-            except Exception as e:
-                extras["config5_online_full_7b"] = {"error": repr(e)[:300]}
+            # logical GPU per B200, full Llama-2-7B KV, slot-limited; bytes fingerprint-checked.  A child
+            # process (the other ranks wait on a CPU barrier, their GPUs idle)
+            torch.cuda.empty_cache()
+            extras["config5_online_full_7b"] = _tool_json(
+                "online_loop.py", ["--fixture", os.path.join(ROOT, "tests", "golden", "trace_7b_c48g_seed0.json"),
+                                   "--shape", "full", "--engine", engine, "--verify-every", "100",
+                                   "--max-slots", str(args.config5_slots), "--devices", "8"], timeout_s=900)
         cpu = None if args.no_cpu_baseline else cpu_baseline(args, ring.shape, ring.tokens)
         line = {
             "metric": "kv_migration_GBps", "value": round(main["value"], 2), "unit": "GB/s", "n_gpus": world,
@@ -1141,10 +1202,14 @@ def run_ours(args) -> int:
                                 if backend == "nccl" else None)
         ctx["barrier"] = dist.barrier
         ctx["all_ok"] = lambda ok: allreduce_max(0.0 if ok else 1.0, device) == 0.0
+        # control-plane group on the host: ranks that wait while rank 0 runs its child-process checks
+        # and CPU baselines block here on the CPU, not in a spinning NCCL kernel on their GPU, and no
+        # NCCL watchdog fires during rank 0's minutes of extras
+        ctx["cpu_group"] = dist.new_group(backend="gloo", timeout=datetime.timedelta(minutes=60))
         try:
             rc = run_ring(args, ctx)
         finally:
-            dist.barrier()
+            dist.barrier(group=ctx["cpu_group"])
             dist.destroy_process_group()
         return rc
     ctx["barrier"] = lambda: None

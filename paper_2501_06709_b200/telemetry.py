@@ -222,3 +222,59 @@ class NvlinkMeter:
         else:
             out["tx_bytes"], out["rx_bytes"] = self._b[0] - self._a[0], self._b[1] - self._a[1]
         return out
+
+
+class EnergyMeter:
+    """Board energy between start() and stop() from NVML's cumulative energy
+    counter (mJ since driver load), with the enforced power limit.  Used to
+    state a power roofline: a kernel whose mean board power sits at the limit
+    cannot run faster than (joules per launch) / limit at that energy per
+    launch, so its speed is set by energy per FLOP or byte, not by the pipe."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.error: Optional[str] = None
+        self.limit_w: Optional[float] = None
+        self._e0 = self._e1 = None
+        self._t0 = self._t1 = None
+        try:
+            nv = _nvml()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(device)
+            self.limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
+            nv.nvmlDeviceGetTotalEnergyConsumption(self._h)
+        except Exception as e:
+            self._nv, self.error = None, f"NVML energy counter unavailable: {e!r}"[:200]
+
+    def start(self) -> None:
+        self._t0 = time.perf_counter()
+        if self._nv is not None:
+            self._e0 = self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h)
+
+    def stop(self) -> None:
+        if self._nv is not None:
+            self._e1 = self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h)
+        self._t1 = time.perf_counter()
+
+    def joules(self) -> Optional[float]:
+        if self._e0 is None or self._e1 is None:
+            return None
+        return (self._e1 - self._e0) / 1e3
+
+    def measure(self, fn, calls: int, sync) -> dict:
+        """Energy of `calls` back-to-back calls of fn (asynchronous launches;
+        `sync` waits for them).  Returns joules per call, mean board watts over
+        the region, the limit, and whether the region ran at the cap."""
+        sync()
+        self.start()
+        for _ in range(calls):
+            fn()
+        sync()
+        self.stop()
+        j, dt = self.joules(), self._t1 - self._t0
+        if j is None:
+            return {"error": self.error or "no energy reading"}
+        w = j / dt
+        return {"calls": calls, "seconds": round(dt, 3), "joules_per_call": round(j / calls, 4),
+                "board_w": round(w, 1), "limit_w": self.limit_w,
+                "at_cap": bool(self.limit_w and w >= 0.95 * self.limit_w)}

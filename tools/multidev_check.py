@@ -88,6 +88,62 @@ def check_executor_cross_device(a, b):
     return {"moves": 3, "bytes": rep.bytes_moved}
 
 
+def check_engine_push_over_peer(a, b):
+    """kvm_migrate launched on A storing straight into B's pool (UVA peer
+    mapping), once per copy engine: LDG/STG and the TMA bulk engine
+    (cp.async.bulk smem -> peer global).  Bytes + table row bit-exact; each
+    engine's push of 64 blocks of 7B KV (512 MiB) timed with CUDA events on
+    A's stream (the single-process NVLink number beside the ring's IPC one)."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2501_06709_b200 import _native
+    from paper_2501_06709_b200.executor import ENGINES
+    from paper_2501_06709_b200.kvcache import LLAMA2_7B, BlockTable, KVPool
+
+    _native.check(_native.lib().kvm_init(1), "kvm_init")
+    nb, n = 96, 64
+    src, dst = KVPool(LLAMA2_7B, nb, device=a), KVPool(LLAMA2_7B, nb, device=b)
+    _fill(src, 11)
+    table = BlockTable(1, n, device=b)
+    flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{b}")
+    sb = np.random.default_rng(3).permutation(nb)[:n].astype(np.int32)
+    db = np.random.default_rng(4).permutation(nb)[:n].astype(np.int32)
+    want = _gather(src, sb)
+    s = torch.cuda.Stream(device=a)
+    out = {"bytes_per_push": n * LLAMA2_7B.block_tokens * LLAMA2_7B.kv_bytes_per_token}
+    for name, eflag in ENGINES.items():
+        _fill(dst, 12)
+        m = _native.Move()
+        m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, n, 1
+        m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
+        m.dst_table_row, m.done_flag = table.row_ptr(0), flag.data_ptr()
+
+        def push():
+            _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST | eflag,
+                                                    ctypes.c_void_p(s.cuda_stream)), f"kvm_migrate({name})")
+
+        push()
+        s.synchronize()
+        assert torch.equal(_gather(dst, db), want), f"{name}: bytes differ on the peer"
+        assert np.array_equal(table.rows[0].cpu().numpy(), db), f"{name}: table row"
+        assert int(flag.item()) == 1, f"{name}: done flag"
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.device(a):
+            for _ in range(3):
+                push()
+            ev[0].record(s)
+            for _ in range(10):
+                push()
+            ev[1].record(s)
+        s.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / 10
+        out[name] = {"ok": True, "ms": round(ms, 4), "GBps": round(out["bytes_per_push"] / ms / 1e6, 1)}
+    return out
+
+
 def check_stream_ordered_cross_device(a, b):
     import torch
 
@@ -260,6 +316,7 @@ def check_pipelined_decode_on_peer(a, b):
 
 
 CHECKS = {
+    "engine_push_over_peer": check_engine_push_over_peer,
     "executor_cross_device": check_executor_cross_device,
     "stream_ordered_cross_device": check_stream_ordered_cross_device,
     "split_push_and_reprefill": check_split_push_and_reprefill,
@@ -290,11 +347,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--a", type=int, default=0)
     ap.add_argument("--b", type=int, default=1)
+    ap.add_argument("--out", default=None, help="also write the JSON result here (bench.py's subprocess probe)")
     args = ap.parse_args()
     import torch
 
     b = args.b if torch.cuda.device_count() > args.b else args.a
-    print(json.dumps(run_checks(args.a, b)))
+    res = run_checks(args.a, b)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(res, f)
+    print(json.dumps(res))
 
 
 if __name__ == "__main__":

@@ -254,8 +254,14 @@ def main():
     ap.add_argument("--split", action="store_true", help="planner split mode (extension)")
     ap.add_argument("--seed", type=int, default=None,
                     help="another trace seed (same config); decisions are then not checked against the fixture")
+    ap.add_argument("--devices", type=int, default=None, help="spread logical GPUs over the first N devices")
+    ap.add_argument("--out", default=None, help="also write the JSON result here (bench.py's subprocess run)")
     a = ap.parse_args()
-    res = run_online(a.fixture, a.shape, a.engine, a.verify_every, a.seed, a.max_slots, a.split)
+    res = run_online(a.fixture, a.shape, a.engine, a.verify_every, a.seed, a.max_slots, a.split,
+                     devices=None if a.devices is None else list(range(a.devices)))
+    if a.out:
+        with open(a.out, "w") as fh:
+            json.dump(res, fh)
     print(json.dumps(res))
     if res["decisions_match_reference"] is False:
         raise SystemExit("decisions differ from the reference's recorded run")
