@@ -6,6 +6,9 @@ N > 1 run as its multi-device gate (rank 0, devices 0 and 1, reported as
 GPU (the harness itself is exercised on 1-GPU boxes).
 
 Checks (insertion point of every executed move: sim.py:218-227):
+  engine_push_over_peer        kvm_migrate on A storing into B's pool with each
+                               copy engine (LDG/STG, TMA bulk), bytes + row +
+                               flag, and each engine's push GB/s
   executor_cross_device        pools on two devices, one executor (kvm_init(1)
                                peer access), kv moves A -> B, bytes + table rows
   stream_ordered_cross_device  execute(stream_ordered=True) A -> B, then B -> A
@@ -116,6 +119,7 @@ def check_engine_push_over_peer(a, b):
     out = {"bytes_per_push": n * LLAMA2_7B.block_tokens * LLAMA2_7B.kv_bytes_per_token}
     for name, eflag in ENGINES.items():
         _fill(dst, 12)
+        torch.cuda.synchronize(b)    # the fill ran on b's current stream; the push runs on s (device a)
         m = _native.Move()
         m.src_pool, m.dst_pool, m.n_blocks, m.done_value = src.pool_id, dst.pool_id, n, 1
         m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data

@@ -207,11 +207,21 @@ def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_e
     clock = Clock()
     ex.execute = clock.wrap("executor", ex.execute)
     runtime.plan_hybrid = clock.wrap("planner", plan_hybrid)
+    # test harness, not the product: fingerprint stamps written into every block a request gains
+    # (a stand-in for the prefill/decode that fills them in a server) and the periodic read-back checks
+    ex.fp.flush = clock.wrap("fingerprint", ex.fp.flush)
     checked = []
+
+    def timed_verify():
+        f0, t0 = clock.t.get("fingerprint", 0.0), time.perf_counter()
+        n_ok = ex.verify()                      # its own flush() is already counted by the wrapper
+        dt = time.perf_counter() - t0 - (clock.t.get("fingerprint", 0.0) - f0)
+        clock.t["fingerprint"] = clock.t.get("fingerprint", 0.0) + dt
+        return n_ok
 
     def on_slot(slot, rows):
         if verify_every and slot % verify_every == verify_every - 1:
-            checked.append(ex.verify())
+            checked.append(timed_verify())
 
     t0 = time.perf_counter()
     try:
@@ -237,7 +247,8 @@ def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_e
         "bytes_moved": out.bytes_moved, "reconciled_moves": out.reconciled_moves,
         "splits": sum(1 for r in out.plan_rows if r[6] == "split_transfer"),
         "decisions_match_reference": parity, "fingerprint_checks": sum(checked),
-        "ms_per_slot": {k: 1e3 * v / n for k, v in clock.t.items()} | {"loop": 1e3 * wall / n},
+        "ms_per_slot": {k: 1e3 * v / n for k, v in clock.t.items()} | {
+            "loop": 1e3 * wall / n, "loop_minus_fingerprint": 1e3 * (wall - clock.t.get("fingerprint", 0.0)) / n},
         "executor_GBps_while_moving": out.bytes_moved / clock.t.get("executor", 1e-9) / 1e9,
         "device_ms_total": round(dev_ms, 3),
         "device_copy_GBps": round(out.bytes_moved / max(1e-9, dev_ms) / 1e6, 1),
