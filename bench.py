@@ -823,11 +823,25 @@ def _peer_probe(args, ctx) -> dict:
     import torch.distributed as dist
 
     md = None
-    if ctx["ri"].rank == 0 and not ctx["shared"] and ctx["ndev"] >= 2 and not args.no_multidev_checks:
-        md = _tool_json("multidev_check.py", ["--a", "0", "--b", "1"], timeout_s=600)
+    if ctx["ri"].rank == 0 and not args.no_multidev_checks:
+        # ranks sharing one GPU (test mode): the same checks with both 'devices' = cuda:0
+        b = "1" if ctx["ndev"] >= 2 else "0"
+        md = _tool_json("multidev_check.py", ["--a", "0", "--b", b], timeout_s=600)
     box = [md]
     dist.broadcast_object_list(box, src=0, group=ctx["cpu_group"])
     return box[0]
+
+
+def ring_engines(requested, md) -> list:
+    """Copy engines the ring's start-up A/B may try: the one requested, else
+    both, except that the TMA bulk engine is only offered when the cross-device
+    probe pushed into a peer pool with it bit-exact (or no probe ran)."""
+    if requested:
+        return [requested]
+    if md is None:
+        return ["bulk", "ldg"]
+    bulk_ok = bool(((md.get("engine_push_over_peer") or {}).get("bulk") or {}).get("ok", False))
+    return ["bulk", "ldg"] if bulk_ok else ["ldg"]
 
 
 def run_ring(args, ctx) -> int:
@@ -839,9 +853,8 @@ def run_ring(args, ctx) -> int:
 
     ri, world, dev, shared = ctx["ri"], ctx["world"], ctx["device"], ctx["shared"]
     md = _peer_probe(args, ctx)
-    bulk_peer_ok = md is None or bool(md.get("engine_push_over_peer", {}).get("bulk", {}).get("ok", False))
     ring = Ring(ctx, args.workload)
-    engines = [args.engine] if args.engine else (["bulk", "ldg"] if bulk_peer_ok else ["ldg"])
+    engines = ring_engines(args.engine, md)
     gates = {e: ring.gate(e) for e in engines}
     ab = {}
     if len(engines) > 1:   # start-up A/B to the peer, behind the bit-exact gate: keep the faster engine

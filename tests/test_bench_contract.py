@@ -52,6 +52,22 @@ def test_warmup_floor():
     assert out.returncode != 0
 
 
+def test_ring_engine_choice_follows_the_peer_probe():
+    """The N>1 A/B offers the TMA bulk engine only when the child-process probe
+    pushed into a peer pool with it bit-exact; an explicit --engine wins."""
+    sys.path.insert(0, ROOT)
+    from bench import ring_engines
+
+    ok = {"engine_push_over_peer": {"ok": True, "ldg": {"ok": True}, "bulk": {"ok": True}}}
+    bad = {"engine_push_over_peer": {"ok": False, "error": "AssertionError: bulk: bytes differ on the peer"}}
+    crashed = {"all_ok": False, "error": "rc=-6: illegal address"}
+    assert ring_engines(None, None) == ["bulk", "ldg"]
+    assert ring_engines(None, ok) == ["bulk", "ldg"]
+    assert ring_engines(None, bad) == ["ldg"]
+    assert ring_engines(None, crashed) == ["ldg"]
+    assert ring_engines("bulk", bad) == ["bulk"]
+
+
 @pytest.mark.gpu
 def test_gpu_arm_contract():
     d = _run(["--workload", "7b-512", "--steps", "5", "--warmup", "3", "--no-cpu-baseline"])
@@ -93,6 +109,17 @@ def test_gpu_arm_plain_python_two_ranks():
     assert d["config"]["engine"] in ("bulk", "ldg") and set(d["config"]["engine_ab"]) == {"bulk", "ldg"}
     assert "nvlink_counters" in d["roofline"] and d["gpu_launches"] > 0
     assert d["library"]["paper_transport"]["bit_exact"] is True and d["library"]["paper_transport"]["value"] > 0
+    md = d["multi_device_checks"]   # the child-process probe ran (both 'devices' = cuda:0 on a 1-GPU box)
+    assert md["all_ok"] is True and md["engine_push_over_peer"]["bulk"]["ok"] is True, md
+
+
+@pytest.mark.gpu
+def test_gpu_arm_four_ranks_shared():
+    """Four ranks on the ring i -> (i+1) mod 4 (shared GPU on a 1-GPU box):
+    every rank's received request bit-exact, one line with n_gpus == 4."""
+    d = _run(["--gpus", "4", "--workload", "7b-512", "--steps", "5", "--warmup", "3", "--no-cpu-baseline",
+              "--shared-gpu", "--no-multidev-checks"], timeout=900)
+    assert d["n_gpus"] == 4 and d["bit_exact"] is True and d["value"] > 0 and d["e2e"]["row_ok"] is True
 
 
 @pytest.mark.gpu
