@@ -205,7 +205,7 @@ def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_e
     inner = MigrationExecutor(pools, tables, engine=engine, reprefill=rp, timing=True)
     ex = FingerprintedExecutor(inner)
     clock = Clock()
-    ex.execute = clock.wrap("executor", ex.execute)
+    inner.execute = clock.wrap("executor", inner.execute)   # the executor alone (not the stamps)
     runtime.plan_hybrid = clock.wrap("planner", plan_hybrid)
     # test harness, not the product: fingerprint stamps written into every block a request gains
     # (a stand-in for the prefill/decode that fills them in a server) and the periodic read-back checks
