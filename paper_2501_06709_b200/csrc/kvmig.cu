@@ -628,9 +628,9 @@ static int slot_acquire(DevState& ds, size_t bytes, size_t ctrs, Slot** out) {
 
 struct DeviceGuard {
   int prev = -1;
-  explicit DeviceGuard(int d) {
+  explicit DeviceGuard(int d) {   // d < 0: keep the current device
     cudaGetDevice(&prev);
-    if (prev != d) cudaSetDevice(d);
+    if (d >= 0 && prev != d) cudaSetDevice(d);
   }
   ~DeviceGuard() {
     int cur = -1;
@@ -1157,6 +1157,9 @@ int kvm_wait_flag(const uint32_t* flag, uint32_t value, void* stream) {
 int kvm_read_back(void* host, const void* dev, int64_t bytes, void* stream) {
   if (bytes < 0 || (bytes > 0 && (!host || !dev))) return fail(KVM_ERR_INVALID, "bad read-back arguments");
   if (bytes == 0) return KVM_OK;
+  int sdev = -1;
+  if (stream) KVM_CUDA_TRY(cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &sdev));
+  DeviceGuard dg(sdev);   // work goes to the stream's device whatever the caller's current device is
   KVM_CUDA_TRY(cudaMemcpyAsync(host, dev, (size_t)bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
   return KVM_OK;
 }
@@ -1164,6 +1167,9 @@ int kvm_read_back(void* host, const void* dev, int64_t bytes, void* stream) {
 int kvm_wait_flag_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err_word,
                           void* stream) {
   if (!flag) return fail(KVM_ERR_INVALID, "flag is NULL");
+  int sdev = -1;
+  if (stream) KVM_CUDA_TRY(cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &sdev));
+  DeviceGuard dg(sdev);   // a launch into another device's stream fails unless that device is current
   wait_flag_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flag, value, timeout_ns, err_word);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
