@@ -79,6 +79,15 @@ def tokens_at(rec, slot: int, tokens_per_slot: int) -> int:
     return prompt + min(response, tokens_per_slot * max(0, slot - arrival))
 
 
+def _sync_devices(executor) -> None:
+    """Wait for every device the executor's pools live on (torch.cuda.synchronize()
+    alone waits for the current device only)."""
+    import torch
+
+    for dev in sorted({p.device for per in executor.pools.values() for p in per.values()}):
+        torch.cuda.synchronize(dev)
+
+
 class Fingerprints:
     """Per-request KV fingerprints on an executor's pools: every block a
     request owns holds a value that depends on (request, logical block, layer,
@@ -226,9 +235,7 @@ class FingerprintedExecutor:
         return report
 
     def verify(self) -> int:
-        import torch
-
-        torch.cuda.synchronize()
+        _sync_devices(self.ex)
         return self.fp.verify()
 
 
@@ -327,10 +334,10 @@ class TraceReplay:
                 ref_bytes, dt))
             self.reports.append(report)
             if self.fingerprint and verify_every and (s + 1) % verify_every == 0:
-                torch.cuda.synchronize()
+                _sync_devices(self.ex)
                 rep.verified_requests += self.verify()
         if self.fingerprint:
-            torch.cuda.synchronize()
+            _sync_devices(self.ex)
             rep.verified_requests += self.verify()
         rep.recomputed_requests = len(self.recomputed)
         return rep

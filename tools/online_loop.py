@@ -229,7 +229,8 @@ def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_e
                     sched_wrap=lambda f: clock.wrap("scheduler", f))
     finally:
         runtime.plan_hybrid = plan_hybrid
-    torch.cuda.synchronize()
+    for d in sorted({p.device for per in pools.values() for p in per.values()}):
+        torch.cuda.synchronize(d)
     wall = time.perf_counter() - t0
     checked.append(ex.verify())
     n = len(out.active_gpus)
