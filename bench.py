@@ -184,6 +184,15 @@ def _kernel_extras(device: int) -> dict:
         del pool, q, o
     except Exception as e:
         out["decode_7b_4k_32l"] = {"error": str(e)[:300]}
+    try:   # configs[2]: 13B 8k adaptive split on this GPU (fused kernel, two kernels, full transfer)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from bench_split import run_split_bench
+
+        out["split_13b_8k"] = run_split_bench(iters=5, warmup=3, src_dev=device, dst_dev=device)
+        out["split_13b_8k"]["kernel"] = "kvm_split_migrate (reprefill_pair_kernel<kCopy>) / kvm_migrate + kvm_reprefill"
+        torch.cuda.empty_cache()
+    except Exception as e:
+        out["split_13b_8k"] = {"error": repr(e)[:300]}
     try:   # live-migration tail: one 7B block (8 MiB) with host block lists, table row + done flag
         import numpy as np
 
@@ -939,6 +948,11 @@ def run_ring(args, ctx) -> int:
                                              "mean TX bytes per launch (null when the box does not expose them)"}
     line = None
     if ri.rank == 0:
+        if not shared and ctx["ndev"] >= 2 and not args.no_extras:
+            # configs[2] across two GPUs: the prefix pushed 0 -> 1 over NVLink while GPU 1 re-prefills
+            # the suffix (and the fused kernel pulling the prefix), child process, others wait on the CPU
+            extras["split_13b_8k_2gpu"] = _tool_json("bench_split.py", ["--src-dev", "0", "--dst-dev", "1",
+                                                                        "--iters", "5"], timeout_s=600)
         if not shared and ctx["ndev"] >= 8 and world >= 8 and args.config5_slots > 0:
             # configs[4] at real shapes: the live loop (native scheduler -> planner -> executor) with one
             # logical GPU per B200, full Llama-2-7B KV, slot-limited; bytes fingerprint-checked.  A child

@@ -85,6 +85,9 @@ def test_gpu_arm_contract():
     assert k["reprefill_13b_s1360"]["cublas_same_shape"]["ms"] > 0
     assert k["decode_7b_4k_32l"]["unit"] == "GB/s" and 0.3 < k["decode_7b_4k_32l"]["frac"] < 1.5
     assert 0 < k["small_move_7b_1block"]["issue_to_landed_us_p50"] < 1000
+    sp = k["split_13b_8k"]   # configs[2] on this GPU: parity first, then the timed arms
+    assert sp["prefix_bit_exact"] is True and sp["suffix_within_tolerance"] is True, sp
+    assert 0 < sp["ms"]["split_fused_one_kernel"] < sp["ms"]["split_two_kernels_serialized"]
     lib = d["library"]   # the library path on the same workload, timed in the same run
     assert lib["bit_exact"] is True and lib["value"] > 0 and lib["ours_over_library"] > 1
 
