@@ -43,12 +43,20 @@ def raw(rep):
     return res
 
 
+OUR_KERNELS = ("kvm::", "migrate_bulk_kernel", "migrate_ldg_kernel", "reprefill_pair_kernel", "reprefill_kernel",
+               "decode_gqa_kernel", "decode_combine_kernel", "wait_flag_kernel", "rope_table_kernel")
+
+
+def _ours(name):
+    return any(k in name for k in OUR_KERNELS)
+
+
 def launches(path, tag):
     rows = list(csv.reader(open(path)))
     h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[h]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    ours = [r for r in rows[h + 1:] if "kvm::" in r[ki]]
+    ours = [r for r in rows[h + 1:] if _ours(r[ki])]
     agg = defaultdict(list)
     for r in rows[h + 1:]:
         agg[r[ki]].append(float(r[vi].replace(",", "")))
@@ -56,7 +64,7 @@ def launches(path, tag):
         w = csv.writer(fh)
         w.writerow(["kernel", "launches", "mean_ns", "total_ns", "ours"])
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-            w.writerow([k, len(v), round(sum(v) / len(v), 1), round(sum(v)), "kvm::" in k])
+            w.writerow([k, len(v), round(sum(v) / len(v), 1), round(sum(v)), _ours(k)])
         w.writerow([])
         w.writerow(["# per-launch list (ours)"])
         for r in ours:
