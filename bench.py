@@ -58,6 +58,7 @@ WORKLOADS = {
     "7b-512": ("llama2-7b", 512, "test size (contract tests only; not a BASELINE config)"),
 }
 NVLINK_PEAK_GBS = 900.0        # nominal per direction per GPU
+WAIT_NS = 5_000_000_000        # bound on one receive wait in the ring (a 5 GB push takes ~7 ms over NVLink)
 NVLINK_MEASURED_GBS = 770.0    # B200_PROFILING.md: measured peer copy per direction
 
 
@@ -584,9 +585,19 @@ class Ring:
             self.stream.synchronize()
             self.ctx["barrier"]()
         else:
-            self.link.wait(self.seq, self.stream)
+            self.link.wait(self.seq, self.stream, timeout_ns=WAIT_NS)
         if ev is not None:
             ev[2].record(self.stream)
+
+    def landed(self) -> bool:
+        """False if a receive wait timed out (the peer's move never became
+        visible); never raises, so every rank reaches the next collective."""
+        try:
+            self.link.check()
+            return True
+        except TimeoutError as e:
+            print(f"bench.py: {e}", file=sys.stderr)
+            return False
 
     def gate(self, engine: str) -> bool:
         """One migration, then bit-exact check: what this rank received equals
@@ -603,11 +614,11 @@ class Ring:
             self.step(engine, host=False)
         self.stream.synchronize()
         self.ctx["barrier"]()
-        self.link.check()
+        arrived = self.landed()
         got = _checksum(self.pool, self.db_np, self.n)
         sums = exchange_objects(sent)
         row_ok = bool(np.array_equal(self.link.row[:self.n].cpu().numpy(), self.db_np))
-        ok = got == sums[ri.recv_from] and row_ok
+        ok = arrived and got == sums[ri.recv_from] and row_ok
         if not ok:
             print(f"rank {ri.rank}: parity gate failed ({engine}): received checksum {got}, sent "
                   f"{sums[ri.recv_from]}, table row ok {row_ok}", file=sys.stderr)
@@ -647,7 +658,7 @@ class Ring:
         if meter is not None:
             meter.stop()
         self.ctx["barrier"]()
-        self.link.check()
+        arrived = self.ctx["all_ok"](self.landed())
         launches = _native.launch_count() - launches0
         elapsed = allreduce_max(t0.elapsed_time(t1), dev)
         push = [a.elapsed_time(b) for a, b, _ in ev]
@@ -657,7 +668,7 @@ class Ring:
         return {"elapsed_ms": elapsed, "push_ms_mean": allreduce_max(statistics.fmean(push), dev),
                 "push_p50": allreduce_max(p50, dev), "push_p99": allreduce_max(p99, dev),
                 "step_p50": allreduce_max(s50, dev), "step_p99": allreduce_max(s99, dev),
-                "launches": launches, "K": K,
+                "launches": launches, "K": K, "all_landed": arrived,
                 "value": self.ctx["world"] * self.kv_bytes * K / (elapsed / 1e3) / 1e9}
 
     def e2e(self, engine: str, K: int) -> dict:
@@ -685,8 +696,7 @@ class Ring:
         torch.cuda.synchronize()
         e2e_s = allreduce_max(time.perf_counter() - t0, dev)
         self.ctx["barrier"]()
-        self.link.check()
-        ok = bool((row.numpy() == self.db_np).all())
+        ok = self.landed() and bool((row.numpy() == self.db_np).all())
         return {"value": self.ctx["world"] * self.kv_bytes * K / e2e_s / 1e9, "h2d_bytes_per_step": 2 * self.n * 4,
                 "d2h_bytes_per_step": self.n * 4, "latency_ms_p50": 1e3 * allreduce_max(statistics.median(lat), dev),
                 "row_ok": self.ctx["all_ok"](ok)}
@@ -877,6 +887,17 @@ def run_ring(args, ctx) -> int:
         engine = min(ok_eng, key=lambda e: ab[e]["push_ms_mean"]) if ok_eng else engines[0]
     else:
         engine = engines[0]
+    if not any(gates.values()):
+        # nothing landed bit-exact on the peer: no throughput is reported for a path that is wrong
+        if ri.rank == 0:
+            print(json.dumps({"metric": "kv_migration_GBps", "value": 0.0, "unit": "GB/s", "n_gpus": world,
+                              "steps": 0, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                              "scaling": "weak", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
+                              "data": "synthetic", "bit_exact": False, "engines_tried": engines,
+                              "multi_device_checks": md,
+                              "error": "no copy engine passed the bit-exact gate to the peer pool"}), flush=True)
+        ring.close()
+        return 1
     bit_exact = gates[engine]
     meter = NvlinkMeter(dev)
     clocks = ClockSampler(dev)
@@ -985,7 +1006,8 @@ def run_ring(args, ctx) -> int:
                            "step_p50": round(main["step_p50"], 4), "step_p99": round(main["step_p99"], 4),
                            "step_definition": "push + wait until the incoming move's done flag is visible here "
                                               "(ld.acquire.sys)"},
-            "bit_exact": bool(bit_exact and e2e["row_ok"] and (md is None or md.get("all_ok", False))),
+            "bit_exact": bool(bit_exact and main["all_landed"] and e2e["row_ok"]
+                              and (md is None or md.get("all_ok", False))),
             "multi_device_checks": md,
             "roofline": roof,
             "cpu_baseline": cpu,
