@@ -68,6 +68,28 @@ def test_ring_engine_choice_follows_the_peer_probe():
     assert ring_engines("bulk", bad) == ["bulk"]
 
 
+def test_child_process_tools_report_instead_of_failing(tmp_path):
+    """bench.py runs the cross-device probe, the 2-GPU split and config 5 in
+    child processes: a result, a crash and a hang each come back as a dict
+    (the rank that launched it stays alive and prints its line)."""
+    sys.path.insert(0, ROOT)
+    from bench import _tool_json
+
+    ok = tmp_path / "ok.py"
+    ok.write_text("import json, sys\nout = sys.argv[sys.argv.index('--out') + 1]\n"
+                  "json.dump({'all_ok': True, 'x': int(sys.argv[1])}, open(out, 'w'))\n")
+    crash = tmp_path / "crash.py"
+    crash.write_text("raise SystemExit('illegal address')\n")
+    hang = tmp_path / "hang.py"
+    hang.write_text("import time\ntime.sleep(60)\n")
+    r = _tool_json(str(ok), ["7"], timeout_s=60)
+    assert r["all_ok"] is True and r["x"] == 7 and r["subprocess_s"] >= 0
+    r = _tool_json(str(crash), [], timeout_s=60)
+    assert r["all_ok"] is False and "illegal address" in r["error"]
+    r = _tool_json(str(hang), [], timeout_s=2)
+    assert r["all_ok"] is False and "timed out" in r["error"]
+
+
 @pytest.mark.gpu
 def test_gpu_arm_contract():
     d = _run(["--workload", "7b-512", "--steps", "5", "--warmup", "3", "--no-cpu-baseline"])
