@@ -422,6 +422,9 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // the tiles were stored by the async (bulk-copy) proxy: order them before the generic-proxy
+  // fence + release of the layer / done flags and the table row that follow (also across NVLink)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // One warp per CTA; lane 0 drives the bulk unit, the warp cooperates on the

@@ -282,6 +282,9 @@ __device__ __noinline__ void bulk_copy_units(const Params& p, uint8_t* ring, uin
     }
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // the prefix was written by the async (bulk-copy) proxy; order it before the generic-proxy
+  // release of the done flag / table row that follows the kernel's last CTA
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
