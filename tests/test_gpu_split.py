@@ -254,3 +254,21 @@ def test_fused_split_randomized(seed):
             torch.testing.assert_close(dst.tensor[l, 1, blk, slot].reshape(plan.suffix, kvd).float(),
                                        ref[l, :, qc + kvd:], atol=ATOL, rtol=RTOL)
     assert torch.equal(got[:, :, mask], before[:, :, mask])
+
+
+@pytest.mark.parametrize("force_two", [False, True])
+def test_bench_split_tool_paths(force_two):
+    """tools/bench_split.run_split_bench (the bench line's configs[2] extra):
+    the same-device path and the two-device path (peer alias of the source
+    pool, done-flag waits, two kernels overlapped) forced onto one GPU, at a
+    reduced 2k-token size: prefix bit-exact, suffix within tolerance."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from bench_split import run_split_bench
+
+    r = run_split_bench(tokens=2048, iters=2, warmup=1, src_dev=0, dst_dev=0, force_two=force_two)
+    assert r["prefix_bit_exact"] is True and r["suffix_within_tolerance"] is True, r
+    assert r["suffix_reprefilled"] > 0 and r["prefix_blocks"] > 0
+    assert (r["ms"]["split_two_kernels"] is not None) == force_two

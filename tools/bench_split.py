@@ -58,10 +58,13 @@ def _fill(pool, seed):
 
 
 def run_split_bench(tokens: int = 8192, suffix=None, iters: int = 10, warmup: int = 3, src_dev: int = 0,
-                    dst_dev: int = 0) -> dict:
+                    dst_dev: int = 0, force_two: bool = False) -> dict:
+    """force_two: run the two-device code path (peer alias of the source pool,
+    done-flag waits, two-kernel overlap) even when src_dev == dst_dev, so a
+    1-GPU box exercises it."""
     shape = LLAMA2_13B
     n = tokens
-    two = src_dev != dst_dev
+    two = src_dev != dst_dev or force_two
     if two:
         _native.check(_native.lib().kvm_init(1), "kvm_init(enable_peer_access)")
     fpt = flops_per_token(shape, with_q=True)
@@ -207,7 +210,8 @@ def run_split_bench(tokens: int = 8192, suffix=None, iters: int = 10, warmup: in
     t_suffix = timeit(run_suffix_only) if plan.suffix else 0.0
     if two:
         alias.close()
-    where = f"src cuda:{src_dev} -> dst cuda:{dst_dev}" + (" (NVLink)" if two else " (same GPU)")
+    where = f"src cuda:{src_dev} -> dst cuda:{dst_dev}" + (" (NVLink)" if src_dev != dst_dev else
+                                                           " (same GPU, two-device code path)" if two else " (same GPU)")
     return {
         "config": "configs[2]: Llama-2-13B KV, 8k tokens, adaptive split", "devices": where, "tokens": n,
         "suffix_reprefilled": plan.suffix, "prefix_blocks": plan.prefix_blocks,
@@ -241,8 +245,9 @@ def main():
     ap.add_argument("--src-dev", type=int, default=0)
     ap.add_argument("--dst-dev", type=int, default=0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--force-two", action="store_true", help="two-device code path on one device (test)")
     a = ap.parse_args()
-    res = run_split_bench(a.tokens, a.suffix, a.iters, a.warmup, a.src_dev, a.dst_dev)
+    res = run_split_bench(a.tokens, a.suffix, a.iters, a.warmup, a.src_dev, a.dst_dev, a.force_two)
     if a.out:
         with open(a.out, "w") as f:
             json.dump(res, f)
