@@ -70,7 +70,9 @@ __device__ __forceinline__ void wait_layer(const Params& p, int layer) {
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     unsigned ns = 32;
-    while (ld_acquire_sys_u32(p.layer_flags + layer) < p.layer_value) {
+    // relaxed polls + one acquire fence when the layer is seen: an acquire per poll also
+    // orders this SM's other traffic and slows the copy running beside the waiting CTAs
+    while (ld_relaxed_sys_u32(p.layer_flags + layer) < p.layer_value) {
       __nanosleep(ns);
       if (ns < 512) ns <<= 1;
       uint64_t t;
@@ -80,6 +82,7 @@ __device__ __forceinline__ void wait_layer(const Params& p, int layer) {
         break;
       }
     }
+    fence_acq_rel_sys();
   }
   __syncthreads();
 }

@@ -535,16 +535,19 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // the kernel returns, so a lost peer write cannot wedge the GPU.
 __global__ void wait_flag_kernel(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* err) {
   if (threadIdx.x == 0) {
+    // relaxed polls (an acquire per poll would also order this SM's other traffic), one acquire
+    // fence once the value is seen; exponential backoff to 2 us
     unsigned ns = 32;
     const uint64_t t0 = globaltimer_ns();
-    while (ld_acquire_sys_u32(flag) < value) {
+    while (ld_relaxed_sys_u32(flag) < value) {
       __nanosleep(ns);
-      if (ns < 1024) ns <<= 1;
+      if (ns < 2048) ns <<= 1;
       if (timeout_ns && globaltimer_ns() - t0 > timeout_ns) {
         if (err) atomicExch(err, 1u);
         return;
       }
     }
+    fence_acq_rel_sys();
   }
 }
 
@@ -1173,6 +1176,21 @@ int kvm_wait_flag_timeout(const uint32_t* flag, uint32_t value, uint64_t timeout
   int sdev = -1;
   if (stream) KVM_CUDA_TRY(cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &sdev));
   DeviceGuard dg(sdev);   // a launch into another device's stream fails unless that device is current
+  {
+    // The spinning waiter must not pin its SM to a small shared-memory carveout: a copy kernel
+    // (128 KiB ring) or the re-prefill GEMM (223 KiB) launched beside it on the same GPU would then
+    // find one SM it cannot use until the waiter exits -- a persistent grid of one CTA per SM
+    // runs a second wave (measured: a 7B-4k bulk copy 0.653 -> 1.030 ms with a waiter beside it).
+    static std::atomic<uint64_t> carveout_set{0};
+    int dev = sdev;
+    if (dev < 0) cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(carveout_set.load() & bit)) {
+      KVM_CUDA_TRY(cudaFuncSetAttribute(wait_flag_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        (int)cudaSharedmemCarveoutMaxShared));
+      carveout_set.fetch_or(bit);
+    }
+  }
   wait_flag_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flag, value, timeout_ns, err_word);
   KVM_CUDA_TRY(cudaGetLastError());
   count_launch();
