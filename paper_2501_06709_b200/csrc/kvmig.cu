@@ -128,6 +128,7 @@ int sm_count(int device) {
 // kernels
 // ---------------------------------------------------------------------------
 constexpr int kTileBytes = 32 * 1024;   // work unit
+constexpr int kQueueChunk = 4;          // bulk engine's dynamic queue: tiles per request
 constexpr int kLdgThreads = 256;
 constexpr int kLdgVecPerThread = kTileBytes / 16 / kLdgThreads;  // 8
 
@@ -165,6 +166,7 @@ struct MigrateParamsT {
   int32_t n_moves;
   int32_t per_layer_flush;   // 1: flush at (move, layer) granularity
   int64_t total_tiles;
+  uint32_t* queue;           // bulk engine: [next tile, CTAs done] self-rewinding tile queue; NULL = static
   DevMove m[kMoves];
   int32_t blocks[kInline > 0 ? 2 * kInline : 1];
 };
@@ -446,6 +448,18 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
   const int64_t first = blockIdx.x;
   const int64_t stride = gridDim.x;
   const int64_t my_tiles = first < p.total_tiles ? (p.total_tiles - 1 - first) / stride + 1 : 0;
+  // Tile source.  Static: tiles first, first + stride, ...  Dynamic (p.queue): lane 0 takes chunks of
+  // kQueueChunk consecutive tiles from a global counter, requesting the next chunk one chunk ahead so
+  // the atomic's round trip hides behind the copies; a CTA slowed by whatever shares its SM (a flag
+  // waiter, a decode, NVLink back-pressure) then simply takes fewer tiles instead of setting the
+  // pace of the whole grid.
+  const bool dyn = p.queue != nullptr;
+  int64_t c_cur = 0, c_end = 0, c_next = 0;
+  if (dyn && lane == 0) {
+    c_cur = atomicAdd(p.queue, (uint32_t)kQueueChunk);
+    c_end = c_cur + kQueueChunk;
+    c_next = atomicAdd(p.queue, (uint32_t)kQueueChunk);
+  }
 
   int cur_ld = 0;
   int key_move = -1, key_layer = -1, key_n = 0;
@@ -453,10 +467,12 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
   __shared__ uint8_t* st_dst[kBulkStages];
   __shared__ int st_len[kBulkStages], st_move[kBulkStages], st_layer[kBulkStages];
 
-  for (int64_t i = 0; i < my_tiles + kBulkLag; ++i) {
+  int64_t n_loaded = 0;     // warp-uniform
+  bool exhausted = false;   // warp-uniform
+  for (int64_t i = 0;; ++i) {
     // ---- store side: tile j = i - lag ----
     const int64_t j = i - kBulkLag;
-    if (j >= 0) {
+    if (j >= 0 && j < n_loaded) {
       const int sj = (int)(j % kBulkStages);
       int mv = 0, ly = 0;
       if (lane == 0) { mv = st_move[sj]; ly = st_layer[sj]; }
@@ -482,21 +498,38 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
       }
       ++key_n;
     }
-    // ---- load side: tile i ----
-    if (i < my_tiles) {
+    // ---- load side: tile n_loaded (slot n_loaded % stages; n_loaded == i until the source runs dry) ----
+    if (!exhausted) {
+      long long t = -1;
       if (lane == 0) {
-        const int si = (int)(i % kBulkStages);
-        // slot si last held tile i - stages; its store must have finished reading smem.
-        bulk_wait_read<kBulkStages - kBulkLag>();
-        TileRef tr = decode_tile(p, first + i * stride, cur_ld);
-        st_dst[si] = tr.dst;
-        st_len[si] = tr.len;
-        st_move[si] = tr.move;
-        st_layer[si] = p.per_layer_flush ? tr.layer : 0;
-        mbar_expect_tx(full + si, (uint32_t)tr.len);
-        bulk_g2s<kEvictFirst>(smem + si * kTileBytes, tr.src, (uint32_t)tr.len, full + si, pol);
+        if (dyn) {
+          if (c_cur >= c_end) {
+            c_cur = c_next;
+            c_end = c_cur + kQueueChunk;
+            c_next = atomicAdd(p.queue, (uint32_t)kQueueChunk);
+          }
+          t = c_cur < p.total_tiles ? c_cur++ : -1;
+        } else {
+          t = n_loaded < my_tiles ? first + n_loaded * stride : -1;
+        }
+        if (t >= 0) {
+          const int si = (int)(n_loaded % kBulkStages);
+          // slot si last held tile n_loaded - stages; its store must have finished reading smem.
+          bulk_wait_read<kBulkStages - kBulkLag>();
+          TileRef tr = decode_tile(p, t, cur_ld);
+          st_dst[si] = tr.dst;
+          st_len[si] = tr.len;
+          st_move[si] = tr.move;
+          st_layer[si] = p.per_layer_flush ? tr.layer : 0;
+          mbar_expect_tx(full + si, (uint32_t)tr.len);
+          bulk_g2s<kEvictFirst>(smem + si * kTileBytes, tr.src, (uint32_t)tr.len, full + si, pol);
+        }
       }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t < 0) exhausted = true;
+      else ++n_loaded;
     }
+    if (exhausted && j + 1 >= n_loaded) break;   // every loaded tile has been stored
   }
   if (key_move >= 0) {
     int done = 0;
@@ -506,6 +539,15 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
     }
     done = __shfl_sync(0xffffffffu, done, 0);
     if (done) finalize_move<false>(p, p.m[key_move], lane, 32);
+  }
+  if (dyn && lane == 0) {
+    // Every CTA gets here only after its queue requests ran past the end; the last one out rewinds
+    // the queue for the next launch that uses this staging slot (ordered after this kernel).
+    __threadfence();
+    if (atomicAdd(p.queue + 1, 1u) == gridDim.x - 1) {
+      p.queue[0] = 0;
+      p.queue[1] = 0;
+    }
   }
 }
 
@@ -824,10 +866,23 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
   p.per_layer_flush = any_layer_flags ? 1 : 0;
   if (on_host && (rc = validate_batch_disjoint(moves, n))) return rc;
 
-  // A staging slot is needed only for host lists that are not inline and for
-  // completion counters; an untracked inline move is parameters only.
+  // The bulk engine's persistent grid (more tiles than CTAs) takes its tiles from a queue: two
+  // self-rewinding counters after the moves' completion counters in the staging slot.
+  // KVM_COPY_STATIC=1 keeps the static grid-stride partition (A/B).
+  static const bool static_copy = [] {
+    const char* e = getenv("KVM_COPY_STATIC");
+    return e && atoi(e) != 0;
+  }();
+  const int cap = (flags >> 8) & 0xff;
+  const bool shallow = std::is_same<P, SmallParams>::value && tiles <= ds.bulk_grid_small && !cap;
+  const int big_grid = cap ? std::min(ds.bulk_grid, cap * sm_count(device)) : ds.bulk_grid;
+  const bool dyn = (flags & KVM_F_ENGINE_BULK) && !shallow && tiles > big_grid && !static_copy;
+  if (dyn) ctrs += 2;
+
+  // A staging slot is needed only for host lists that are not inline, for
+  // completion counters and for the tile queue; an untracked inline move is parameters only.
   Slot* slot = nullptr;
-  if (host_bytes > 0 || any_track)
+  if (host_bytes > 0 || any_track || dyn)
     if ((rc = slot_acquire(ds, host_bytes, ctrs, &slot))) return rc;
   size_t off = 0, coff = 0;
   for (int i = 0; i < n; ++i) {
@@ -858,6 +913,7 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
       d.dst_blocks = mv.dst_blocks;
     }
   }
+  p.queue = dyn ? slot->ctr + coff : nullptr;
   if (off > 0) KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
   if ((rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream))) return rc;
   if (slot) {
