@@ -14,8 +14,6 @@ pool; 7B, 4k tokens = 2 GiB by default), inputs > L2, CUDA events, median of
   torch         pool[:, :, dst] = pool[:, :, src]  (advanced-index gather + put)
   vllm-swap_blocks  vLLM 0.22's block copy (_C_cache_ops.swap_blocks) per plane: how
                 vLLM moves KV blocks (one cudaMemcpyAsync per block)
-  memcpy-batch  cudaMemcpyBatchAsync: one call, one (src, dst, 128 KiB) entry per
-                (layer, K|V, block) piece -> copy engines
   memcpy-loop   cudaMemcpyAsync per piece (host-issued, 16 384 calls)
 
 Prints one JSON line; GB/s counts payload bytes (kv_bytes), "hbm_frac" the
@@ -41,11 +39,6 @@ from paper_2501_06709_b200.kvcache import SHAPES, KVPool  # noqa: E402
 
 WORKLOADS = {"7b-4k": ("llama2-7b", 4096), "13b-8k": ("llama2-13b", 8192), "70b-16k": ("llama3-70b-gqa", 16384),
              "7b-512": ("llama2-7b", 512)}
-
-
-class MemcpyAttributes(ctypes.Structure):   # cudaMemcpyAttributes (CUDA 12.8+)
-    _fields_ = [("srcAccessOrder", ctypes.c_int), ("srcLocType", ctypes.c_int), ("srcLocId", ctypes.c_int),
-                ("dstLocType", ctypes.c_int), ("dstLocId", ctypes.c_int), ("flags", ctypes.c_uint)]
 
 
 def main():
@@ -148,7 +141,6 @@ def main():
     fwd = (addrs(sb), addrs(db))
     bwd = (addrs(db), addrs(sb))
     cnt = fwd[0].size
-    sizes = (ctypes.c_size_t * cnt)(*([pb] * cnt))
     cudart = None
     for name in ("libcudart.so.12", "libcudart.so"):
         try:
@@ -159,18 +151,6 @@ def main():
     arrays = {}
     for key, (src, dst) in (("f", fwd), ("b", bwd)):
         arrays[key] = ((ctypes.c_void_p * cnt)(*dst.tolist()), (ctypes.c_void_p * cnt)(*src.tolist()))
-
-    attr = MemcpyAttributes(1, 1, 0, 1, 0, 0)   # stream order; device 0 -> device 0
-    attr_idx = (ctypes.c_size_t * 1)(0)
-    fail_idx = ctypes.c_size_t(0)
-
-    def batch_arm():
-        d, src = arrays["b" if flip[0] else "f"]
-        flip[0] = not flip[0]
-        rc = cudart.cudaMemcpyBatchAsync(d, src, sizes, ctypes.c_size_t(cnt), ctypes.byref(attr), attr_idx,
-                                         ctypes.c_size_t(1), ctypes.byref(fail_idx), sptr)
-        if rc != 0:
-            raise RuntimeError(f"cudaMemcpyBatchAsync -> {rc}")
 
     def loop_arm():
         d, src = arrays["b" if flip[0] else "f"]
@@ -183,7 +163,7 @@ def main():
     if vops is not None:
         arms.append(("vllm-swap_blocks", vllm_arm))
     if cudart is not None:
-        arms += [("memcpy-batch", batch_arm), ("memcpy-loop", loop_arm)]
+        arms.append(("memcpy-loop", loop_arm))
     for name, fn in arms:
         try:
             ms = timeit(fn)
