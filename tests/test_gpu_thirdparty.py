@@ -181,3 +181,142 @@ def test_flashinfer_decodes_a_migrated_cache_like_the_source():
     after = _flashinfer_decode(fi, pools[1], q, row, seq, torch.float16)
     torch.cuda.synchronize()
     assert torch.equal(before.view(torch.int16), after.view(torch.int16))
+
+
+# --- the byte path: kvm_migrate / kvm_compact == vLLM's own block copy --------------------------------------
+# vLLM moves KV blocks with _C_cache_ops.swap_blocks(src, dst, block_bytes, mapping): per cache tensor, block
+# mapping[i][0] of src -> block mapping[i][1] of dst.  The paper's prototype sits on vLLM, so
+# this is the published byte semantics of a block move; the pool planes below ARE vLLM's per-layer caches
+# ([NB][16][H][D] contiguous per (layer, K|V)), and the foreign-layout case hands kvm_migrate vLLM's own
+# FlashAttention tensors.  Expectation: whole pools byte-identical after the same mapping.
+
+def _vllm_ops():
+    try:
+        import vllm._custom_ops as vops
+        torch.ops._C_cache_ops.swap_blocks   # noqa: B018  (raises when vLLM's CUDA ops are not loadable)
+    except Exception as e:  # pragma: no cover - the image ships vLLM 0.22
+        pytest.skip(f"vLLM cache ops unavailable: {e!r}")
+    return vops
+
+
+def _rand_fill(t, seed):
+    g = torch.Generator(device=t.device).manual_seed(seed)
+    v = t.view(torch.int16)
+    v.copy_(torch.randint(-2 ** 15, 2 ** 15, v.shape, generator=g, device=t.device, dtype=torch.int16))
+
+
+def _planes(pool):
+    return [pool.tensor[l, kv] for l in range(pool.shape.layers) for kv in range(2)]
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+@pytest.mark.parametrize("host_blocks", [True, False])
+@pytest.mark.parametrize("n", [1, 19, 64])
+def test_migrate_equals_vllm_swap_blocks(engine, host_blocks, n):
+    """kvm_migrate(src pool -> dst pool) leaves the destination pool byte-identical to vLLM's swap_blocks
+    applied plane by plane with the same (src block, dst block) mapping, and the source untouched."""
+    import ctypes
+
+    from paper_2501_06709_b200 import _native
+    vops = _vllm_ops()
+    shape = ModelShape("v", layers=3, kv_heads=8, head_dim=128, q_heads=8, d_model=1024)   # 32 KiB pieces
+    nb = 96
+    src, dst = KVPool(shape, nb), KVPool(shape, nb)
+    _rand_fill(src.tensor, 11 + n)
+    _rand_fill(dst.tensor, 12 + n)
+    rng = np.random.default_rng(n)
+    sb = rng.permutation(nb)[:n].astype(np.int32)
+    dst.allocator.take(rng.permutation(nb)[:nb // 3])
+    db = dst.allocator.alloc(n)
+    expect = dst.tensor.clone()
+    src_before = src.tensor.clone()
+    mapping = torch.from_numpy(np.stack([sb, db], 1).astype(np.int64))
+    for ps, pd in zip(_planes(src), [expect[l, kv] for l in range(shape.layers) for kv in range(2)]):
+        vops.swap_blocks(ps, pd, shape.piece_bytes, mapping)
+    m = _native.Move()
+    m.src_pool, m.dst_pool, m.n_blocks = src.pool_id, dst.pool_id, n
+    keep = []
+    if host_blocks:
+        m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
+        flags = _native.KVM_F_BLOCKS_ON_HOST
+    else:
+        keep = [torch.from_numpy(sb).cuda(), torch.from_numpy(db).cuda()]
+        m.src_blocks, m.dst_blocks = keep[0].data_ptr(), keep[1].data_ptr()
+        flags = 0
+    flags |= _native.KVM_F_ENGINE_BULK if engine == "bulk" else 0
+    arr = (_native.Move * 1)(m)
+    _native.check(_native.lib().kvm_migrate(arr, 1, flags, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(dst.tensor.view(torch.int16), expect.view(torch.int16))
+    assert torch.equal(src.tensor.view(torch.int16), src_before.view(torch.int16))
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+def test_compact_equals_vllm_swap_blocks_in_place(engine):
+    """kvm_compact (src pool == dst pool, disjoint block sets) == vLLM swap_blocks with src == dst tensor."""
+    import ctypes
+
+    from paper_2501_06709_b200 import _native
+    vops = _vllm_ops()
+    shape = ModelShape("v", layers=4, kv_heads=4, head_dim=128, q_heads=4, d_model=512)     # 16 KiB pieces
+    nb = 128
+    pool = KVPool(shape, nb)
+    _rand_fill(pool.tensor, 3)
+    perm = np.random.default_rng(3).permutation(nb).astype(np.int32)
+    sb, db = perm[:45], perm[45:90]
+    expect = pool.tensor.clone()
+    mapping = torch.from_numpy(np.stack([sb, db], 1).astype(np.int64))
+    for l in range(shape.layers):
+        for kv in range(2):
+            vops.swap_blocks(expect[l, kv], expect[l, kv], shape.piece_bytes, mapping)
+    flags = _native.KVM_F_BLOCKS_ON_HOST | (_native.KVM_F_ENGINE_BULK if engine == "bulk" else 0)
+    _native.check(_native.lib().kvm_compact(pool.pool_id, sb.ctypes.data, db.ctypes.data, len(sb), None, flags,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(pool.tensor.view(torch.int16), expect.view(torch.int16))
+
+
+@pytest.mark.parametrize("layout", ["flash_attn", "flashinfer"])
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+def test_migrate_between_vllm_caches_equals_swap_blocks(layout, engine):
+    """Two vLLM-shaped per-layer cache sets (vLLM's own get_kv_cache_shape), registered in place: kvm_migrate
+    between them == vLLM swap_blocks on the same tensors' K and V blocks (FlashAttention layout: the K / V
+    halves are block arrays; FlashInfer: blocks interleave K|V, so the mapping moves 2b and 2b+1 of the
+    [NB*2][16][H][D] view)."""
+    import ctypes
+
+    from paper_2501_06709_b200 import _native
+    from paper_2501_06709_b200.foreign import StridedKVPool, vllm_cache_shape
+    vops = _vllm_ops()
+    L, nb, H, D = 3, 64, 8, 128
+    shp = vllm_cache_shape(layout, nb, 16, H, D)
+    srcs = [torch.empty(shp, dtype=torch.float16, device="cuda") for _ in range(L)]
+    dsts = [torch.empty(shp, dtype=torch.float16, device="cuda") for _ in range(L)]
+    for i, t in enumerate(srcs + dsts):
+        _rand_fill(t, 40 + i)
+    sp, dp = StridedKVPool.from_vllm(srcs, layout), StridedKVPool.from_vllm(dsts, layout)
+    rng = np.random.default_rng(9)
+    sb = rng.permutation(nb)[:23].astype(np.int32)
+    db = rng.permutation(nb)[:23].astype(np.int32)
+    expect = [t.clone() for t in dsts]
+    piece = 16 * H * D * 2
+    for s, e in zip(srcs, expect):
+        if layout == "flash_attn":
+            m = torch.from_numpy(np.stack([sb, db], 1).astype(np.int64))
+            for kv in range(2):
+                vops.swap_blocks(s[kv], e[kv], piece, m)
+        else:
+            m = torch.from_numpy(np.concatenate([np.stack([2 * sb + kv, 2 * db + kv], 1) for kv in range(2)])
+                                 .astype(np.int64))
+            vops.swap_blocks(s, e, piece, m)
+    mv = _native.Move()
+    mv.src_pool, mv.dst_pool, mv.n_blocks = sp.pool_id, dp.pool_id, len(sb)
+    mv.src_blocks, mv.dst_blocks = sb.ctypes.data, db.ctypes.data
+    flags = _native.KVM_F_BLOCKS_ON_HOST | (_native.KVM_F_ENGINE_BULK if engine == "bulk" else 0)
+    _native.check(_native.lib().kvm_migrate((_native.Move * 1)(mv), 1, flags,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    for got, e in zip(dsts, expect):
+        assert torch.equal(got.view(torch.int16), e.view(torch.int16))
+    sp.close()
+    dp.close()

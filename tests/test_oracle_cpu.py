@@ -248,3 +248,67 @@ def test_abi_struct_layout():
     assert ctypes.sizeof(_native.PoolDesc) == 24
     assert ctypes.sizeof(_native.Move) == 56
     assert _native.Move.src_blocks.offset == 16
+
+
+# --- the oracle pinned to third-party outputs (vLLM swap_blocks, flashinfer decode) -------------------------
+# tests/golden/thirdparty_vectors.json is written on a B200 by tests/golden/make_thirdparty_golden.py from the
+# libraries the paper's prototype ran its data plane in; inputs are regenerated here from seeds.
+_TP = os.path.join(ROOT, "tests", "golden", "thirdparty_vectors.json")
+
+
+def _tp_vectors():
+    import json
+    with open(_TP) as fh:
+        return json.load(fh)
+
+
+def test_oracle_migrate_equals_vllm_swap_blocks_vectors():
+    """oracle_migrate over whole pools == vLLM swap_blocks applied per (layer, K|V) plane (sha256 of the
+    destination pool; the source unchanged), incl. in-place compaction and NaN/inf bit patterns."""
+    import hashlib
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("mk", os.path.join(ROOT, "tests", "golden",
+                                                                    "make_thirdparty_golden.py"))
+    mk = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mk)
+    vec = _tp_vectors()
+    assert len(vec["swap_blocks"]) == len(mk.SWAP_CASES)
+    for case in vec["swap_blocks"]:
+        L, H, D = case["layers"], case["kv_heads"], case["head_dim"]
+        src, dst, sb, db = mk.swap_inputs(L, H, D, case["src_nb"], case["dst_nb"], case["n"], case["seed"],
+                                          case["in_place"])
+        src = src.view(np.int16).reshape(L, 2, case["src_nb"], 16, H, D)
+        sd = orc.desc(L, H, D, 16, case["src_nb"])
+        if case["in_place"]:
+            orc.migrate(src, sd, src, sd, sb, db)
+            got = src
+        else:
+            dst = dst.view(np.int16).reshape(L, 2, case["dst_nb"], 16, H, D)
+            before = hashlib.sha256(src.tobytes()).hexdigest()
+            orc.migrate(src, sd, dst, orc.desc(L, H, D, 16, case["dst_nb"]), sb, db)
+            got = dst
+            assert hashlib.sha256(src.tobytes()).hexdigest() == before == case["src_sha256"], case["name"]
+        assert hashlib.sha256(got.tobytes()).hexdigest() == case["dst_sha256"], case["name"]
+
+
+def test_oracle_decode_equals_flashinfer_vectors():
+    """oracle/attention_ref.reference_decode (fp32 torch on CPU) == flashinfer's paged decode output recorded
+    on a B200 for the same pool / page table / queries (fp16; atol 2e-3, rtol 2e-2 as the GPU test)."""
+    import importlib.util
+    from types import SimpleNamespace
+
+    import torch
+
+    from oracle.attention_ref import reference_decode
+    spec = importlib.util.spec_from_file_location("mk", os.path.join(ROOT, "tests", "golden",
+                                                                    "make_thirdparty_golden.py"))
+    mk = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mk)
+    for case in _tp_vectors()["decode"]:
+        H, Hq, lens = case["kv_heads"], case["q_heads"], case["seq_lens"]
+        k, v, tables, q = mk.decode_inputs(H, Hq, lens, case["seed"])
+        pool = SimpleNamespace(shape=SimpleNamespace(head_dim=128, kv_heads=H, block_tokens=16),
+                               tensor=torch.from_numpy(np.stack([k, v])[None]))
+        got = reference_decode(pool, torch.from_numpy(q)[None], [torch.from_numpy(t) for t in tables], lens)
+        want = torch.tensor([float.fromhex(x) for x in case["out_f32_hex"]]).view(len(lens), Hq, 128)
+        torch.testing.assert_close(got[0], want, atol=2e-3, rtol=2e-2, msg=case["name"])
