@@ -166,7 +166,8 @@ struct MigrateParamsT {
   int32_t n_moves;
   int32_t per_layer_flush;   // 1: flush at (move, layer) granularity
   int64_t total_tiles;
-  uint32_t* queue;           // bulk engine: [next tile, CTAs done] self-rewinding tile queue; NULL = static
+  unsigned long long* queue;        // bulk engine's tile queue (a monotonic counter); NULL = static
+  unsigned long long queue_base;    // its value when this launch starts (host-tracked per slot)
   DevMove m[kMoves];
   int32_t blocks[kInline > 0 ? 2 * kInline : 1];
 };
@@ -448,17 +449,22 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
   const int64_t first = blockIdx.x;
   const int64_t stride = gridDim.x;
   const int64_t my_tiles = first < p.total_tiles ? (p.total_tiles - 1 - first) / stride + 1 : 0;
-  // Tile source.  Static: tiles first, first + stride, ...  Dynamic (p.queue): lane 0 takes chunks of
-  // kQueueChunk consecutive tiles from a global counter, requesting the next chunk one chunk ahead so
-  // the atomic's round trip hides behind the copies; a CTA slowed by whatever shares its SM (a flag
-  // waiter, a decode, NVLink back-pressure) then simply takes fewer tiles instead of setting the
-  // pace of the whole grid.
+  // Tile source.  Static: tiles first, first + stride, ...  Dynamic (p.queue): every CTA starts on its
+  // own chunk of kQueueChunk consecutive tiles (no atomic before the first load), then lane 0 takes
+  // further chunks from a global counter, requesting the next one a chunk ahead so the atomic's round
+  // trip hides behind the copies; a CTA slowed by whatever shares its SM (a flag waiter, a decode,
+  // NVLink back-pressure) then simply takes fewer tiles instead of setting the pace of the whole grid.
+  // The counter is never rewound: each CTA ends holding exactly two requests past the last full chunk,
+  // so a launch advances it by kQueueChunk * (floor((tiles - grid * kQueueChunk) / kQueueChunk) +
+  // 2 * grid), which the host adds to the slot's base (launch_copy's caller requires tiles >=
+  // 2 * grid * kQueueChunk, so every CTA's first chunk is whole).
   const bool dyn = p.queue != nullptr;
+  const int64_t q0 = (int64_t)gridDim.x * kQueueChunk;
   int64_t c_cur = 0, c_end = 0, c_next = 0;
   if (dyn && lane == 0) {
-    c_cur = atomicAdd(p.queue, (uint32_t)kQueueChunk);
+    c_cur = (int64_t)blockIdx.x * kQueueChunk;
     c_end = c_cur + kQueueChunk;
-    c_next = atomicAdd(p.queue, (uint32_t)kQueueChunk);
+    c_next = q0 + (int64_t)(atomicAdd(p.queue, (unsigned long long)kQueueChunk) - p.queue_base);
   }
 
   int cur_ld = 0;
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
           if (c_cur >= c_end) {
             c_cur = c_next;
             c_end = c_cur + kQueueChunk;
-            c_next = atomicAdd(p.queue, (uint32_t)kQueueChunk);
+            c_next = q0 + (int64_t)(atomicAdd(p.queue, (unsigned long long)kQueueChunk) - p.queue_base);
           }
           t = c_cur < p.total_tiles ? c_cur++ : -1;
         } else {
@@ -539,15 +545,6 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
     }
     done = __shfl_sync(0xffffffffu, done, 0);
     if (done) finalize_move<false>(p, p.m[key_move], lane, 32);
-  }
-  if (dyn && lane == 0) {
-    // Every CTA gets here only after its queue requests ran past the end; the last one out rewinds
-    // the queue for the next launch that uses this staging slot (ordered after this kernel).
-    __threadfence();
-    if (atomicAdd(p.queue + 1, 1u) == gridDim.x - 1) {
-      p.queue[0] = 0;
-      p.queue[1] = 0;
-    }
   }
 }
 
@@ -600,8 +597,9 @@ struct Slot {
   void* host = nullptr;        // pinned
   uint8_t* dev = nullptr;      // device: block lists
   size_t cap = 0;
-  uint32_t* ctr = nullptr;     // device counters (zeroed once, self-resetting)
+  uint32_t* ctr = nullptr;     // device counters (zeroed once, self-resetting); words 0-1: tile queue
   size_t ctr_cap = 0;          // in uint32
+  unsigned long long queue_next = 0;   // the tile queue's value after the last launch queued on this slot
   cudaEvent_t ev = nullptr;
   bool pending = false;
 };
@@ -669,6 +667,7 @@ static int slot_acquire(DevState& ds, size_t bytes, size_t ctrs, Slot** out) {
     KVM_CUDA_TRY(cudaMalloc(&s.ctr, cap * sizeof(uint32_t)));
     KVM_CUDA_TRY(cudaMemset(s.ctr, 0, cap * sizeof(uint32_t)));
     s.ctr_cap = cap;
+    s.queue_next = 0;
   }
   *out = &s;
   return KVM_OK;
@@ -866,9 +865,11 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
   p.per_layer_flush = any_layer_flags ? 1 : 0;
   if (on_host && (rc = validate_batch_disjoint(moves, n))) return rc;
 
-  // The bulk engine's persistent grid (more tiles than CTAs) takes its tiles from a queue: two
-  // self-rewinding counters after the moves' completion counters in the staging slot.
-  // KVM_COPY_STATIC=1 keeps the static grid-stride partition (A/B).
+  // The bulk engine's persistent grid takes its tiles from a queue once there are at least two
+  // chunks per CTA (below that the queue's atomics cost more than the balance buys: measured on a
+  // 4-block 7B move, 11 -> 14 us): a monotonic 64-bit counter in words 0-1 of the staging slot's
+  // counters (the moves' completion counters follow it).  KVM_COPY_STATIC=1 keeps the static
+  // grid-stride partition (A/B).
   static const bool static_copy = [] {
     const char* e = getenv("KVM_COPY_STATIC");
     return e && atoi(e) != 0;
@@ -876,15 +877,17 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
   const int cap = (flags >> 8) & 0xff;
   const bool shallow = std::is_same<P, SmallParams>::value && tiles <= ds.bulk_grid_small && !cap;
   const int big_grid = cap ? std::min(ds.bulk_grid, cap * sm_count(device)) : ds.bulk_grid;
-  const bool dyn = (flags & KVM_F_ENGINE_BULK) && !shallow && tiles > big_grid && !static_copy;
-  if (dyn) ctrs += 2;
+  const bool dyn = (flags & KVM_F_ENGINE_BULK) && !shallow && tiles >= 2 * (int64_t)big_grid * kQueueChunk &&
+                   !static_copy;
+  constexpr size_t kQueueWords = 2;
+  ctrs += kQueueWords;
 
   // A staging slot is needed only for host lists that are not inline, for
   // completion counters and for the tile queue; an untracked inline move is parameters only.
   Slot* slot = nullptr;
   if (host_bytes > 0 || any_track || dyn)
     if ((rc = slot_acquire(ds, host_bytes, ctrs, &slot))) return rc;
-  size_t off = 0, coff = 0;
+  size_t off = 0, coff = kQueueWords;
   for (int i = 0; i < n; ++i) {
     DevMove& d = p.m[i];
     const kvm_move& mv = moves[i];
@@ -913,9 +916,15 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
       d.dst_blocks = mv.dst_blocks;
     }
   }
-  p.queue = dyn ? slot->ctr + coff : nullptr;
+  if (dyn) {
+    p.queue = reinterpret_cast<unsigned long long*>(slot->ctr);
+    p.queue_base = slot->queue_next;
+  }
   if (off > 0) KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
   if ((rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream))) return rc;
+  if (dyn)   // see migrate_bulk_kernel: the counter's advance is fixed by tiles and grid
+    slot->queue_next += (unsigned long long)kQueueChunk *
+                        (unsigned long long)((tiles - (int64_t)big_grid * kQueueChunk) / kQueueChunk + 2 * big_grid);
   if (slot) {
     KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
     slot->pending = true;
