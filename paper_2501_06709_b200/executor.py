@@ -153,6 +153,8 @@ class MigrationExecutor:
             # single process, several GPUs: kernels on the source device store straight
             # into the destination device's pool and block table (UVA peer access)
             _native.check(_native.lib().kvm_init(1), "kvm_init(enable_peer_access)")
+        for d in sorted(devices):   # created now: the first torch stream of a process costs ~0.5 s
+            self.stream(d)
 
     # -- streams ---------------------------------------------------------------
     def stream(self, device: int):
