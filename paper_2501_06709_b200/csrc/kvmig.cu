@@ -128,7 +128,7 @@ int sm_count(int device) {
 // kernels
 // ---------------------------------------------------------------------------
 constexpr int kTileBytes = 32 * 1024;   // work unit
-constexpr int kQueueChunk = 4;          // bulk engine's dynamic queue: tiles per request
+constexpr int kQueueChunk = 4;          // bulk engine's dynamic queue: largest request (tiles)
 constexpr int kLdgThreads = 256;
 constexpr int kLdgVecPerThread = kTileBytes / 16 / kLdgThreads;  // 8
 
@@ -166,8 +166,9 @@ struct MigrateParamsT {
   int32_t n_moves;
   int32_t per_layer_flush;   // 1: flush at (move, layer) granularity
   int64_t total_tiles;
-  unsigned long long* queue;        // bulk engine's tile queue (a monotonic counter); NULL = static
-  unsigned long long queue_base;    // its value when this launch starts (host-tracked per slot)
+  uint32_t* queue;           // bulk engine's tile queue (zero at launch); NULL = static partition
+  uint32_t* queue_other;     // the slot's other queue word, zeroed here for the slot's next launch
+  int32_t queue_chunk;       // largest request / first static chunk per CTA (tiles)
   DevMove m[kMoves];
   int32_t blocks[kInline > 0 ? 2 * kInline : 1];
 };
@@ -450,21 +451,29 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
   const int64_t stride = gridDim.x;
   const int64_t my_tiles = first < p.total_tiles ? (p.total_tiles - 1 - first) / stride + 1 : 0;
   // Tile source.  Static: tiles first, first + stride, ...  Dynamic (p.queue): every CTA starts on its
-  // own chunk of kQueueChunk consecutive tiles (no atomic before the first load), then lane 0 takes
+  // own chunk of queue_chunk consecutive tiles (no atomic before the first load), then lane 0 takes
   // further chunks from a global counter, requesting the next one a chunk ahead so the atomic's round
   // trip hides behind the copies; a CTA slowed by whatever shares its SM (a flag waiter, a decode,
   // NVLink back-pressure) then simply takes fewer tiles instead of setting the pace of the whole grid.
-  // The counter is never rewound: each CTA ends holding exactly two requests past the last full chunk,
-  // so a launch advances it by kQueueChunk * (floor((tiles - grid * kQueueChunk) / kQueueChunk) +
-  // 2 * grid), which the host adds to the slot's base (launch_copy's caller requires tiles >=
-  // 2 * grid * kQueueChunk, so every CTA's first chunk is whole).
+  // Requests are guided: about a quarter of the remaining tiles per CTA, at most queue_chunk, so the
+  // grid's CTAs finish within about a tile of each other.  The counter is the slot's word that the
+  // previous launch on this slot zeroed; this launch zeroes the other one for the next.
   const bool dyn = p.queue != nullptr;
-  const int64_t q0 = (int64_t)gridDim.x * kQueueChunk;
-  int64_t c_cur = 0, c_end = 0, c_next = 0;
+  const int64_t qc = dyn ? p.queue_chunk : 0;
+  const int64_t q0 = (int64_t)gridDim.x * qc;
+  const int64_t q_rem = p.total_tiles - q0;          // tiles handed out by the counter
+  int64_t c_cur = 0, c_end = 0, c_next = 0, n_next = 0;
+  auto request = [&](int64_t seen) {                 // lane 0: ask for the chunk after `seen`
+    int64_t want = (q_rem - seen) / (4 * (int64_t)gridDim.x);
+    want = want < 1 ? 1 : (want > qc ? qc : want);
+    n_next = want;
+    c_next = (int64_t)atomicAdd(p.queue, (uint32_t)want);
+  };
   if (dyn && lane == 0) {
-    c_cur = (int64_t)blockIdx.x * kQueueChunk;
-    c_end = c_cur + kQueueChunk;
-    c_next = q0 + (int64_t)(atomicAdd(p.queue, (unsigned long long)kQueueChunk) - p.queue_base);
+    if (blockIdx.x == 0) *p.queue_other = 0;
+    c_cur = (int64_t)blockIdx.x * qc;
+    c_end = c_cur + qc;
+    request(0);
   }
 
   int cur_ld = 0;
@@ -510,9 +519,10 @@ __global__ void __launch_bounds__(32) migrate_bulk_kernel(const __grid_constant_
       if (lane == 0) {
         if (dyn) {
           if (c_cur >= c_end) {
-            c_cur = c_next;
-            c_end = c_cur + kQueueChunk;
-            c_next = q0 + (int64_t)(atomicAdd(p.queue, (unsigned long long)kQueueChunk) - p.queue_base);
+            const int64_t v = c_next;
+            c_cur = q0 + v;
+            c_end = c_cur + n_next;
+            if (c_cur < p.total_tiles) request(v + n_next);
           }
           t = c_cur < p.total_tiles ? c_cur++ : -1;
         } else {
@@ -597,9 +607,9 @@ struct Slot {
   void* host = nullptr;        // pinned
   uint8_t* dev = nullptr;      // device: block lists
   size_t cap = 0;
-  uint32_t* ctr = nullptr;     // device counters (zeroed once, self-resetting); words 0-1: tile queue
+  uint32_t* ctr = nullptr;     // device counters (zeroed once, self-resetting); words 0-1: tile queues
   size_t ctr_cap = 0;          // in uint32
-  unsigned long long queue_next = 0;   // the tile queue's value after the last launch queued on this slot
+  int queue_word = 0;          // which of words 0-1 the next tile-queue launch on this slot counts on
   cudaEvent_t ev = nullptr;
   bool pending = false;
 };
@@ -667,7 +677,7 @@ static int slot_acquire(DevState& ds, size_t bytes, size_t ctrs, Slot** out) {
     KVM_CUDA_TRY(cudaMalloc(&s.ctr, cap * sizeof(uint32_t)));
     KVM_CUDA_TRY(cudaMemset(s.ctr, 0, cap * sizeof(uint32_t)));
     s.ctr_cap = cap;
-    s.queue_next = 0;
+    s.queue_word = 0;
   }
   *out = &s;
   return KVM_OK;
@@ -867,17 +877,23 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
 
   // The bulk engine's persistent grid takes its tiles from a queue once there are at least two
   // chunks per CTA (below that the queue's atomics cost more than the balance buys: measured on a
-  // 4-block 7B move, 11 -> 14 us): a monotonic 64-bit counter in words 0-1 of the staging slot's
-  // counters (the moves' completion counters follow it).  KVM_COPY_STATIC=1 keeps the static
-  // grid-stride partition (A/B).
+  // 4-block 7B move, 11 -> 14 us).  Its counter is word 0 or 1 of the staging slot's counters,
+  // alternating per use of the slot (each launch zeroes the other; uses of one slot are serialised
+  // by slot_acquire's event wait).  KVM_COPY_STATIC=1 keeps the static grid-stride partition and
+  // KVM_COPY_CHUNK=n sets the largest request (A/B).
   static const bool static_copy = [] {
     const char* e = getenv("KVM_COPY_STATIC");
     return e && atoi(e) != 0;
   }();
+  static const int chunk = [] {
+    const char* e = getenv("KVM_COPY_CHUNK");
+    const int c = e ? atoi(e) : kQueueChunk;
+    return c < 1 ? 1 : (c > 64 ? 64 : c);
+  }();
   const int cap = (flags >> 8) & 0xff;
   const bool shallow = std::is_same<P, SmallParams>::value && tiles <= ds.bulk_grid_small && !cap;
   const int big_grid = cap ? std::min(ds.bulk_grid, cap * sm_count(device)) : ds.bulk_grid;
-  const bool dyn = (flags & KVM_F_ENGINE_BULK) && !shallow && tiles >= 2 * (int64_t)big_grid * kQueueChunk &&
+  const bool dyn = (flags & KVM_F_ENGINE_BULK) && !shallow && tiles >= 2 * (int64_t)big_grid * chunk &&
                    !static_copy;
   constexpr size_t kQueueWords = 2;
   ctrs += kQueueWords;
@@ -917,14 +933,13 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
     }
   }
   if (dyn) {
-    p.queue = reinterpret_cast<unsigned long long*>(slot->ctr);
-    p.queue_base = slot->queue_next;
+    p.queue = slot->ctr + slot->queue_word;
+    p.queue_other = slot->ctr + (slot->queue_word ^ 1);
+    p.queue_chunk = chunk;
+    slot->queue_word ^= 1;
   }
   if (off > 0) KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
   if ((rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream))) return rc;
-  if (dyn)   // see migrate_bulk_kernel: the counter's advance is fixed by tiles and grid
-    slot->queue_next += (unsigned long long)kQueueChunk *
-                        (unsigned long long)((tiles - (int64_t)big_grid * kQueueChunk) / kQueueChunk + 2 * big_grid);
   if (slot) {
     KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
     slot->pending = true;
