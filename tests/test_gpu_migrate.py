@@ -570,3 +570,41 @@ def test_executor_validation_leaves_pools_tables_untouched():
         assert {ex.where(r).gpu for r in (1, 2, 3)} == {0}
     rep = ex.execute([PlannedMove(PendingMove(1, 0, 1, 0, 40), KV_TRANSFER)])
     assert rep.records[0].requests == [1] and ex.where(1).gpu == 1 and tables[1].has(1)
+
+
+@pytest.mark.parametrize("tracked", [True, False])
+def test_tile_queue_across_slot_reuse(tracked):
+    """The bulk engine's guided tile queue (>= 8 tiles per CTA) counts on one of two words of a staging
+    slot and zeroes the other for the slot's next launch.  40 back-to-back launches of varying size
+    (queue and static partitions mixed, every staging slot reused) on one stream: each launch copies
+    the request to fresh blocks, and the final blocks hold the original bytes, the table row and the
+    done flag are the last launch's."""
+    shape = ModelShape("q7b", layers=8, kv_heads=32, head_dim=128, q_heads=32, d_model=4096)   # 128 KiB pieces
+    nb = 400
+    pool = KVPool(shape, nb)
+    _fill(pool, 17)
+    table = BlockTable(2, 64)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rng = np.random.default_rng(3)
+    sizes = [40, 3, 64, 19, 1, 33, 64, 7] * 5          # 4 tiles x 16 planes per block: 64 .. 4096 tiles
+    cur = np.sort(rng.permutation(nb)[:sizes[0]]).astype(np.int32)
+    orig = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(cur).long().cuda()].clone()
+    keep = [orig]
+    for i, n in enumerate(sizes):
+        # move the first n blocks of the request to n fresh blocks (the rest stays), other blocks untouched
+        used = set(cur.tolist())
+        free = np.array([b for b in rng.permutation(nb) if b not in used][:n], dtype=np.int32)
+        src = cur[:n].copy()
+        m = _move(pool, pool, src, free, table.row_ptr(1) if tracked else 0, flag.data_ptr() if tracked else 0,
+                  value=i + 1)
+        keep += [src, free]
+        _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1,
+                                                _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK,
+                                                _stream()))
+        cur = np.concatenate([free, cur[n:]]).astype(np.int32)
+    torch.cuda.synchronize()
+    now = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(cur).long().cuda()]
+    assert torch.equal(now, orig)
+    if tracked:
+        assert int(flag.item()) == len(sizes)
+        assert np.array_equal(table.rows[table.slot(1), :sizes[-1]].cpu().numpy(), keep[-1])
