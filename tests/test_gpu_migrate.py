@@ -587,7 +587,7 @@ def test_tile_queue_across_slot_reuse(tracked):
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
     rng = np.random.default_rng(3)
     sizes = [40, 3, 64, 19, 1, 33, 64, 7] * 5          # 4 tiles x 16 planes per block: 64 .. 4096 tiles
-    cur = np.sort(rng.permutation(nb)[:sizes[0]]).astype(np.int32)
+    cur = np.sort(rng.permutation(nb)[:max(sizes)]).astype(np.int32)   # the request: 64 blocks
     orig = pool.tensor.view(torch.int16)[:, :, torch.from_numpy(cur).long().cuda()].clone()
     keep = [orig]
     for i, n in enumerate(sizes):
