@@ -234,6 +234,10 @@ def _kernel_extras(device: int) -> dict:
     except Exception as e:
         out["split_13b_8k"] = {"error": repr(e)[:300]}
     torch.cuda.empty_cache()
+    # the push over a remote link this box has: PCIe to / from pinned host memory (system-scope completion,
+    # as for a peer pool) vs the link's contiguous-copy roofline and vLLM swap_blocks (child process)
+    if device == 0:
+        out["remote_link_pcie"] = _tool_json("bench_host_link.py", ["--iters", "5"], timeout_s=300)
     return out
 
 
