@@ -89,11 +89,12 @@ class BlockAllocator:
             raise ConfigError("num_blocks must be > 0")
         self.num_blocks = num_blocks
         self._free = np.ones(num_blocks, dtype=bool)
+        self._n_free = num_blocks
         self._lo = 0    # every id below _lo is in use (lower bound of the lowest free id)
 
     @property
     def n_free(self) -> int:
-        return int(self._free.sum())
+        return self._n_free
 
     def alloc(self, n: int) -> np.ndarray:
         if n < 0:
@@ -111,6 +112,7 @@ class BlockAllocator:
             raise RequestTooLarge(f"pool has {self.n_free} free blocks, {n} requested")
         ids = np.concatenate(parts) if len(parts) > 1 else parts[0]
         self._free[ids] = False
+        self._n_free -= len(ids)
         self._lo = int(ids[-1]) + 1
         return ids.astype(np.int32)
 
@@ -122,6 +124,7 @@ class BlockAllocator:
         if not self._free[b].all():
             raise ValueError("block already in use")
         self._free[b] = False
+        self._n_free -= int(np.unique(b).size) if b.size > 1 else int(b.size)
 
     def free(self, blocks: Iterable[int]) -> None:
         b = np.asarray(list(blocks) if not isinstance(blocks, np.ndarray) else blocks, dtype=np.int64)
@@ -130,6 +133,7 @@ class BlockAllocator:
         if self._free[b].any():
             raise ValueError("double free")
         self._free[b] = True
+        self._n_free += int(np.unique(b).size) if b.size > 1 else int(b.size)
         if b.size:
             self._lo = min(self._lo, int(b.min()))
 

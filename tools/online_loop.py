@@ -188,6 +188,16 @@ def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_e
     peak, peak_gpus = dry_run_pool_blocks(fx, trace, models, bpt, topo, bounds, shapes, max_slots, split)
     pools, tables = {}, {}
     per_dev_bytes = {}
+    need = {}
+    for (pg, name), blocks in peak.items():   # fail before allocating when the pools cannot fit
+        sh = next(s for s in shapes.values() if s.name == name)
+        d = devices[pg % len(devices)]
+        need[d] = need.get(d, 0) + sh.pool_bytes(max(16, int(blocks * margin) + 64))
+    for d, b in need.items():
+        free = torch.cuda.mem_get_info(d)[0]
+        if b > free - (2 << 30):
+            raise SystemExit(f"online_loop: the pools of the logical GPUs on device {d} need {b / 2 ** 30:.1f} GiB, "
+                             f"{free / 2 ** 30:.1f} GiB free: use more --devices or fewer --max-slots")
     for g in range(peak_gpus):
         dev = devices[g % len(devices)]
         pools[g], tables[g] = {}, {}
