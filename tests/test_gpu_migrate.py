@@ -608,3 +608,59 @@ def test_tile_queue_across_slot_reuse(tracked):
     if tracked:
         assert int(flag.item()) == len(sizes)
         assert np.array_equal(table.rows[table.slot(1), :sizes[-1]].cpu().numpy(), keep[-1])
+
+
+@pytest.mark.parametrize("seed", range(max(1, int(os.environ.get("KVM_FUZZ_SEEDS", "100")) // 5)))
+def test_randomized_queue_sized_batches_vs_oracle(seed):
+    """Random batches large enough for the bulk engine's guided tile queue (>= 8 tiles per CTA, i.e.
+    >= 2 * 148 * 4 tiles) and around its threshold: 32-160 KiB pieces, 1-6 moves of mixed pools in one
+    launch, random block-list placement, per-move table row / done flag / layer flags or none; whole
+    destination pools byte-exact against the C oracle, flags and rows exact."""
+    rng = np.random.default_rng(5000 + seed)
+    sh = ModelShape(f"q{seed}", layers=int(rng.integers(2, 9)), kv_heads=int(rng.choice([8, 16, 32, 40])),
+                    head_dim=128, q_heads=8, d_model=1024)
+    tpb = 2 * sh.layers * ((sh.piece_bytes + 32767) // 32768)            # tiles per block
+    nb = int(min(480, max(64, (2 * 1184 // tpb) + 16)))
+    pools = [(KVPool(sh, nb), KVPool(sh, nb)) for _ in range(int(rng.integers(1, 3)))]
+    for s, d in pools:
+        _fill(s, int(rng.integers(1 << 30)))
+        _fill(d, int(rng.integers(1 << 30)))
+    host = bool(rng.integers(2))
+    table = BlockTable(8, nb)
+    ctrl = torch.zeros(8 + 8 * sh.layers, dtype=torch.int32, device="cuda")
+    moves, keep, checks, rows = [], [], [], []
+    for i in range(int(rng.integers(1, 7))):
+        src, dst = pools[int(rng.integers(len(pools)))]
+        free = np.flatnonzero(dst.allocator.free_mask())
+        n = int(rng.integers(0, min(len(free), nb) + 1))
+        sb = rng.permutation(nb)[:n].astype(np.int32)
+        db = dst.allocator.alloc(n)
+        kind = int(rng.integers(3))    # 0 untracked, 1 row + flag, 2 row + flag + layer flags
+        row = table.row_ptr(i) if kind else 0
+        flag = ctrl[i:].data_ptr() if kind else 0
+        lf = ctrl[8 + i * sh.layers:].data_ptr() if kind == 2 else 0
+        if host:
+            keep += [sb, db]
+            m = _move(src, dst, sb, db, row, flag, lf, value=i + 1)
+        else:
+            sbd, dbd = torch.from_numpy(sb).cuda(), torch.from_numpy(db).cuda()
+            keep += [sbd, dbd]
+            m = _move(src, dst, sbd.data_ptr(), dbd.data_ptr(), row, flag, lf, value=i + 1, n=n)
+        moves.append(m)
+        checks.append((src, dst, sb, db))
+        rows.append((i, kind, db))
+    expect = {}
+    for src, dst, sb, db in checks:
+        if id(dst) not in expect:
+            expect[id(dst)] = (dst, dst.tensor.view(torch.int16).cpu().numpy())
+        orc.migrate(src.tensor.view(torch.int16).cpu().numpy(), _desc(src), expect[id(dst)][1], _desc(dst), sb, db)
+    _run(moves, _native.KVM_F_ENGINE_BULK | (_native.KVM_F_BLOCKS_ON_HOST if host else 0))
+    for dst, exp in expect.values():
+        assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
+    c = ctrl.cpu().numpy()
+    for i, kind, db in rows:
+        if kind:
+            assert c[i] == i + 1
+            assert np.array_equal(table.rows[table.slot(i), :len(db)].cpu().numpy(), db)
+        if kind == 2:
+            assert (c[8 + i * sh.layers: 8 + (i + 1) * sh.layers] == i + 1).all()   # layer flags carry the value
