@@ -9,7 +9,11 @@ leg.  The product package (paper_2501_06709_b200) never imports this package.
   kvmig_oracle.c      the byte path (migrate / allocate / re-prefill) in C;
                       the reference moves no bytes, so the byte layout is frozen
                       by this repo and pinned by identity / known-answer
-                      properties (see the C header).
+                      properties and by recorded outputs of vLLM 0.22's
+                      swap_blocks (tests/golden/thirdparty_vectors.json); the
+                      re-prefill by HF transformers' Llama projections (see the
+                      C header and tests/test_oracle_cpu.py).
   kvmig_oracle.py     ctypes wrapper over liboracle_kvmig.so (built by Makefile).
-  attention_ref.py    fp32 torch paged-decode reference (checker of kvm_paged_decode).
+  attention_ref.py    fp32 torch paged-decode reference (checker of kvm_paged_decode),
+                      pinned by recorded flashinfer 0.6 decode outputs.
 """

@@ -19,6 +19,13 @@
  * Known answers: a migration is the identity on bytes (dst piece == src
  * piece, NaN payloads included), nothing outside the dst blocks changes, and
  * the dst block-table row equals the ascending-free-list allocation.
+ * Third-party pin: the data plane of the paper's prototype was vLLM
+ * (not vendored, no version pinned by the reference).  vLLM
+ * 0.22's block copy `_C_cache_ops.swap_blocks(src, dst, block_bytes, mapping)`
+ * applied per (layer, K|V) plane is the published semantics of a block move;
+ * oracle_migrate reproduces the sha256 of its recorded outputs
+ * (tests/golden/thirdparty_vectors.json, written on a B200 by
+ * tests/golden/make_thirdparty_golden.py; checked by tests/test_oracle_cpu.py).
  */
 #include <pthread.h>
 #include <stdint.h>
