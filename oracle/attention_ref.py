@@ -2,7 +2,9 @@
 decode attention (softmax(q.K^T * scale) . V per layer, request and query
 head, grouped-query heads sharing their KV head), gathering K/V through the
 block tables exactly as kvm_paged_decode addresses the pool.  Used by
-tests/test_gpu_decode.py as the checker; the product never imports it."""
+tests/test_gpu_decode.py as the checker; the product never imports it.
+Pinned by flashinfer 0.6's paged decode: tests/test_oracle_cpu.py reproduces
+its outputs recorded on a B200 (tests/golden/thirdparty_vectors.json)."""
 import math
 
 def reference_decode(pool, q, block_tables, seq_lens, layer0: int = 0, scale: float = None):
