@@ -995,7 +995,7 @@ def run_ring(args, ctx) -> int:
         line = {
             "metric": "kv_migration_GBps", "value": round(main["value"], 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(main["elapsed_ms"] / main["K"], 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
+            "higher_is_better": True, "scaling": "weak", "scaling_note": "N=1 is intra-GPU compaction bound by HBM (configs[1] needs two GPUs); N>1 is the ring push bound by NVLink (one link crossing per byte): compare roofline.frac per N, not value(N)/(N*value(1))", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
             "data": "synthetic (seeded random KV bits, NaN payloads included)",
             "config": {"workload": (f"{args.workload} ring push i->(i+1) mod {world} over NVLink (CUDA IPC)"
                                     if not shared else
@@ -1202,7 +1202,7 @@ def run_compact(args, ctx) -> int:
     line = {
         "metric": "kv_migration_GBps", "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(elapsed_ms / K, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
+        "higher_is_better": True, "scaling": "weak", "scaling_note": "N=1 is intra-GPU compaction bound by HBM (configs[1] needs two GPUs); N>1 is the ring push bound by NVLink (one link crossing per byte): compare roofline.frac per N, not value(N)/(N*value(1))", "vs_baseline": None, "dtype": "fp16 bytes (u16 copy)",
         "data": "synthetic (seeded random KV bits, NaN payloads included)",
         "config": {"workload": f"{args.workload} intra-GPU migration (compaction into fresh blocks of the same pool)",
                    "baseline_config": cfg_desc, "kv_bytes_per_rank_per_step": kv_bytes, "blocks": n,
