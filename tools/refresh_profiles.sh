@@ -1,5 +1,5 @@
 #!/usr/bin/env bash
-# Re-measure every number quoted in profiles/r1_results.md on one B200, into
+# Re-measure every number quoted in profiles/r1_results.md / r2_results.md on one B200, into
 # gpurun_out/refresh/ (copy what you want to keep into profiles/).  Run through
 #   gpurun --timeout 2400 -- 'bash tools/refresh_profiles.sh'
 # Each step is bounded by its own timeout so one failure does not stall the rest.
@@ -17,6 +17,7 @@ run bench 600 python bench.py
 run bench_reference 600 python bench.py --impl reference
 for w in 13b-8k 70b-16k; do run "bench_$w" 600 python bench.py --workload "$w" --no-cpu-baseline --no-extras; done
 run migrate_vs_library 600 python tools/bench_migrate_baselines.py
+run host_link 300 python tools/bench_host_link.py
 run concurrent 600 python tools/bench_concurrent.py
 for a in "" "--rows 4096" "--shape llama2-7b --rows 2048" "--kv-only" "--rows 1456" "--rows 1280"; do
   run "reprefill_${a// /_}" 300 python tools/bench_reprefill.py $a
