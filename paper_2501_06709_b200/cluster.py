@@ -188,6 +188,10 @@ class _Sizes(MutableMapping):
     def __contains__(self, rid) -> bool:
         return rid in self._c._snap().sizes
 
+    def as_dict(self) -> Dict[int, int]:
+        """The current sizes as a plain dict (read-only use; valid until the next mutation)."""
+        return self._c._snap().sizes
+
     def __repr__(self):
         return repr(self._c._snap().sizes)
 

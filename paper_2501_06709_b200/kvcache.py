@@ -101,6 +101,19 @@ class BlockAllocator:
             raise ValueError("n must be >= 0")
         if n == 0:
             return np.zeros(0, dtype=np.int32)
+        if n == 1:   # decode growth: one block at a time (argmax finds the first free id in a window)
+            i = self._lo
+            while i < self.num_blocks:
+                w = self._free[i:i + 512]
+                j = int(w.argmax())
+                if w[j]:
+                    b = i + j
+                    self._free[b] = False
+                    self._n_free -= 1
+                    self._lo = b + 1
+                    return np.array([b], dtype=np.int32)
+                i += len(w)
+            raise RequestTooLarge(f"pool has {self.n_free} free blocks, 1 requested")
         parts, got, i = [], 0, self._lo
         while got < n and i < self.num_blocks:   # scan windows upward from the lowest possibly-free id
             w = self._free[i:i + max(1024, 2 * (n - got))]

@@ -163,11 +163,19 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
     slot = 0
     while slot < horizon or running or buffered:
         growths, completions = {}, []
+        size_now: Dict[int, int] = {}   # _size_at(request, this slot), computed once per request and slot
+
+        def size_of(rid):
+            v = size_now.get(rid)
+            if v is None:
+                v = size_now[rid] = _size_at(recs[rid], slot, tps, bpt_of(rid))
+            return v
+
         for rid, rec in running.items():
             if _completion_slot(rec[1], rec[3], tps) <= slot:
                 completions.append(rid)
             else:
-                growths[rid] = _size_at(rec, slot, tps, bpt_of(rid))
+                growths[rid] = size_of(rid)
         for rid in by_slot.get(slot, []):
             _, _a, prompt, response = recs[rid]
             size = (prompt + response) * bpt_of(rid) if reserve_final else prompt * bpt_of(rid)
@@ -205,7 +213,7 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
                 executor.release(rid)
             for rid in running:
                 if rid in executor.loc:
-                    tok = _size_at(recs[rid], slot, tps, bpt_of(rid)) // bpt_of(rid)
+                    tok = size_of(rid) // bpt_of(rid)
                     if tok > executor.loc[rid].tokens:
                         executor.grow(rid, tok)
             for rid, size in arrivals:
@@ -241,7 +249,8 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
             waiting = set()
             for item in pending:
                 waiting.update(cluster.groups[item].members if item < 0 and item in cluster.groups else (item,))
-            rep = executor.reconcile(lambda rid: cluster.placement.get(cluster.item_of_request(rid)), skip=waiting)
+            placement, rgroup = cluster.placement, cluster.request_group   # item_of_request, model.py:248-250
+            rep = executor.reconcile(lambda rid: placement.get(rgroup.get(rid, rid)), skip=waiting)
             out.reconciled_moves += len(rep.records)
             out.reconciled_bytes += rep.bytes_moved
         for mv in plan.deferred:
@@ -249,7 +258,8 @@ def run_slots(records: Sequence[Tuple[int, int, int, int]], scheduler, cluster, 
         active = sum(1 for g in cluster.gpus.values() if g.residents)
         out.active_gpus.append(active)
         sizes = cluster.sizes
-        out.used_bytes.append(sum(min(_size_at(rec, slot, tps, bpt_of(rid)), cluster.capacity_bytes)
+        sizes = sizes.as_dict() if hasattr(sizes, "as_dict") else sizes
+        out.used_bytes.append(sum(min(size_of(rid), cluster.capacity_bytes)
                                   for rid, rec in running.items() if rid in sizes))
         out.capacity_bytes.append(active * cluster.capacity_bytes)
         out.logical_moves.append(n_moves)
