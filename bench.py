@@ -982,6 +982,10 @@ def run_ring(args, ctx) -> int:
             # the suffix (and the fused kernel pulling the prefix), child process, others wait on the CPU
             extras["split_13b_8k_2gpu"] = _tool_json("bench_split.py", ["--src-dev", "0", "--dst-dev", "1",
                                                                         "--iters", "5"], timeout_s=600)
+            # time to the first decode step after a 7B-4k migration GPU 0 -> GPU 1: sequential vs the decode
+            # of layer l starting when the copy released layer l's flag on GPU 1
+            extras["pipelined_decode_7b_4k_2gpu"] = _tool_json(
+                "bench_pipelined_decode.py", ["--src-dev", "0", "--dst-dev", "1", "--reps", "10"], timeout_s=300)
         if not shared and ctx["ndev"] >= 8 and world >= 8 and args.config5_slots > 0:
             # configs[4] at real shapes: the live loop (native scheduler -> planner -> executor) with one
             # logical GPU per B200, full Llama-2-7B KV, slot-limited; bytes fingerprint-checked.  A child
