@@ -238,6 +238,8 @@ def _kernel_extras(device: int) -> dict:
     # as for a peer pool) vs the link's contiguous-copy roofline and vLLM swap_blocks (child process)
     if device == 0:
         out["remote_link_pcie"] = _tool_json("bench_host_link.py", ["--iters", "5"], timeout_s=300)
+        # decode of resident requests beside an incoming migration / a re-prefill on every SM / on an SM budget
+        out["decode_interference"] = _tool_json("bench_interference.py", ["--steps", "30"], timeout_s=300)
     return out
 
 

@@ -151,6 +151,15 @@ typedef struct kvm_reprefill_args {
  * each layer's projection, as a model forward produces them); default: one
  * [rows][d_model] for every layer. */
 #define KVM_REPREFILL_X_PER_LAYER 0x4
+/* Run the re-prefill (or the split) on at most n SMs (bits 8-15 of flags;
+ * 0 = every SM).  The GEMM kernels are persistent and fill every SM they are
+ * given for the whole launch, so a decode step launched beside an uncapped
+ * re-prefill waits for it; capping leaves 148 - n SMs to decode.  This is the
+ * destination's compute budget of the reference's cost model
+ * (Boundaries.comp_budget = prefill rate x epoch x budget_fraction,
+ * migration.py:77-91) expressed as an SM share. */
+#define KVM_REPREFILL_MAX_SMS(n) (((n)&0xff) << 8)
+#define KVM_REPREFILL_SMS_MASK 0xff00
 
 /* Adaptive split migration in ONE kernel on the destination GPU (extension of
  * the reference's all-or-nothing choice, migration.py:155-169): the first

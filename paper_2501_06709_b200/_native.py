@@ -43,6 +43,10 @@ KVM_REPREFILL_X_PER_LAYER = 0x4
 def KVM_F_CTAS_PER_SM(n: int) -> int:
     return (n & 0xFF) << 8
 
+
+def KVM_REPREFILL_MAX_SMS(n: int) -> int:
+    return (n & 0xFF) << 8
+
 # Every symbol include/kvmig.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "kvm_version", "kvm_last_error", "kvm_device_count", "kvm_init", "kvm_can_access_peer",

@@ -1003,10 +1003,11 @@ static int take_ctr_slot(DevCtr& dc, cudaStream_t stream, int* slot) {
 static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model, int q_cols, int tok0,
                              int n_dst_blocks, const void* x, const void* w, void* q_out,
                              const int32_t* dst_blocks, bool pair = false, bool x_per_layer = false);
-// Launch on the pool's device (current device already set); grid = min(work, SMs).
-static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream);
-// CTA-pair kernel: grid = 2 x min(work, co-resident clusters).
-static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream);
+// Launch on the pool's device (current device already set); grid = min(work, SMs, max_sms).
+// max_sms > 0 (KVM_REPREFILL_MAX_SMS) leaves the other SMs to whatever else runs on the GPU.
+static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream, int max_sms);
+// CTA-pair kernel: grid = 2 x min(work, co-resident clusters, max_sms / 2).
+static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream, int max_sms);
 static DevCtr g_ctr[64];
 static std::mutex g_rp_mu;
 
@@ -1074,7 +1075,7 @@ static int build_gemm_params(Params& p, const Pool* pool, int rows, int d_model,
   return KVM_OK;
 }
 
-static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
+static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream, int max_sms) {
   std::lock_guard<std::mutex> lk(g_rp_mu);
   DevCtr& dc = g_ctr[dev];
   if (!dc.attr) {
@@ -1090,7 +1091,8 @@ static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
   p.ctr = dc.ctr + slot;
   int64_t work = p.total_tiles;
   if (copy) work = std::max<int64_t>(work, (p.c_units + 1) / 2);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sm_count(dev)));
+  const int sms = max_sms > 0 ? std::min(max_sms, sm_count(dev)) : sm_count(dev);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, sms));
   if (copy)
     reprefill_kernel<true><<<grid, THREADS, SMEM_BYTES, stream>>>(p);
   else
@@ -1101,7 +1103,7 @@ static int launch_gemm(Params& p, int dev, bool copy, cudaStream_t stream) {
   return KVM_OK;
 }
 
-static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
+static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream, int max_sms) {
   static bool attr[64] = {};
   static int clusters[64] = {};
   std::lock_guard<std::mutex> lk(g_rp_mu);
@@ -1130,7 +1132,8 @@ static int launch_pair(Params& p, int dev, bool copy, cudaStream_t stream) {
   p.ctr = dc.ctr + slot;
   int64_t work = p.total_tiles;
   if (copy) work = std::max<int64_t>(work, (p.c_units + 3) / 4);  // ~4 copy warps per cluster
-  const int grid = 2 * (int)std::max<int64_t>(1, std::min<int64_t>(work, clusters[dev]));
+  const int cl = max_sms > 0 ? std::max(1, std::min(clusters[dev], max_sms / 2)) : clusters[dev];
+  const int grid = 2 * (int)std::max<int64_t>(1, std::min<int64_t>(work, cl));
   if (copy)
     pair::reprefill_pair_kernel<true><<<grid, THREADS, pair::SMEM_BYTES_COPY, stream>>>(p);
   else
@@ -1189,7 +1192,7 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a->x || !a->w || !a->dst_blocks) return fail(KVM_ERR_INVALID, "NULL x/w/dst_blocks");
   if ((int64_t)(a->tok0 + a->rows) > (int64_t)a->n_dst_blocks * d.block_tokens)
     return fail(KVM_ERR_INVALID, "dst_blocks do not cover tok0 + rows tokens");
-  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER))
+  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER | KVM_REPREFILL_SMS_MASK))
     return fail(KVM_ERR_INVALID, "unknown flags");
   if ((a->flags & KVM_REPREFILL_ROPE) && (d.head_dim != 128 || !(a->rope_theta > 1.f)))
     return fail(KVM_ERR_CONFIG, "KVM_REPREFILL_ROPE needs head_dim 128 and rope_theta > 1");
@@ -1208,7 +1211,8 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* tab = nullptr;
   if ((a->flags & KVM_REPREFILL_ROPE) && (rc = rope_table(p, a->rope_theta, st, &tab))) return rc;
-  rc = pair_kernel ? launch_pair(p, pool->device, false, st) : launch_gemm(p, pool->device, false, st);
+  const int max_sms = (a->flags & KVM_REPREFILL_SMS_MASK) >> 8;
+  rc = pair_kernel ? launch_pair(p, pool->device, false, st, max_sms) : launch_gemm(p, pool->device, false, st, max_sms);
   if (tab) cudaFreeAsync(tab, st);
   return rc;
 }
@@ -1237,7 +1241,7 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
     return fail(KVM_ERR_CONFIG, "kv_heads*head_dim and q_cols must be multiples of 32");
   if (!a->dst_blocks || (a->prefix_blocks && !a->src_blocks) || (suffix && (!a->x || !a->w)))
     return fail(KVM_ERR_INVALID, "NULL pointer argument");
-  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER))
+  if (a->flags & ~(KVM_REPREFILL_SINGLE_CTA | KVM_REPREFILL_ROPE | KVM_REPREFILL_X_PER_LAYER | KVM_REPREFILL_SMS_MASK))
     return fail(KVM_ERR_INVALID, "unknown flags");
   if ((a->flags & KVM_REPREFILL_ROPE) && (d.head_dim != 128 || !(a->rope_theta > 1.f)))
     return fail(KVM_ERR_CONFIG, "KVM_REPREFILL_ROPE needs head_dim 128 and rope_theta > 1");
@@ -1262,7 +1266,9 @@ extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* tab = nullptr;
   if ((a->flags & KVM_REPREFILL_ROPE) && (rc = rope_table(p, a->rope_theta, st, &tab))) return rc;
-  rc = pair_kernel ? launch_pair(p, dst->device, p.c_units > 0, st) : launch_gemm(p, dst->device, p.c_units > 0, st);
+  const int max_sms = (a->flags & KVM_REPREFILL_SMS_MASK) >> 8;
+  rc = pair_kernel ? launch_pair(p, dst->device, p.c_units > 0, st, max_sms)
+                   : launch_gemm(p, dst->device, p.c_units > 0, st, max_sms);
   if (tab) cudaFreeAsync(tab, st);
   return rc;
 }

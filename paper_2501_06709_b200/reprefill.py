@@ -46,7 +46,7 @@ def synthetic_hidden(shape: ModelShape, rows: int, device: int, seed: int = 2):
 
 def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=None,
               done_flag: int = 0, done_value: int = 1, single_cta: bool = False,
-              rope_theta: Optional[float] = None) -> None:
+              rope_theta: Optional[float] = None, max_sms: int = 0) -> None:
     """Launch kvm_reprefill: K/V of tokens [tok0, tok0 + rows) into `dst_blocks`.
 
     x: bf16 [rows][d_model] (device) fed to every layer, or [layers][rows][d_model]
@@ -56,11 +56,14 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
     selects the single-CTA kernel instead of the default CTA-pair one.
     rope_theta: apply rotary position embedding (HF rotate_half, positions
     tok0 + t) to Q and K in the epilogue, so the pool holds post-RoPE K as a
-    Llama KV cache does (head_dim 128).
+    Llama KV cache does (head_dim 128).  max_sms > 0: run on at most that many
+    SMs (KVM_REPREFILL_MAX_SMS), leaving the rest of the GPU to decode.
     """
     import torch
 
     shape = pool.shape
+    if not 0 <= max_sms <= 255:
+        raise ValueError("max_sms must be in [0, 255] (0 = every SM)")
     if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise ConfigError("re-prefill operands must be bf16")
     if pool.dtype != torch.bfloat16:
@@ -88,7 +91,8 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
     a.dst_blocks = dst_blocks.data_ptr()
     a.done_flag, a.done_value = done_flag or None, done_value
     a.flags = (_native.KVM_REPREFILL_SINGLE_CTA if single_cta else 0) | (
-        _native.KVM_REPREFILL_ROPE if rope_theta else 0) | (_native.KVM_REPREFILL_X_PER_LAYER if per_layer else 0)
+        _native.KVM_REPREFILL_ROPE if rope_theta else 0) | (_native.KVM_REPREFILL_X_PER_LAYER if per_layer else 0) | \
+        _native.KVM_REPREFILL_MAX_SMS(max_sms)
     a.rope_theta = float(rope_theta or 0.0)
     s = stream if stream is not None else torch.cuda.current_stream(pool.device)
     _native.check(_native.lib().kvm_reprefill(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),
@@ -98,13 +102,20 @@ def reprefill(pool: KVPool, x, w, dst_blocks, tok0: int = 0, q_out=None, stream=
 class ReprefillEngine:
     """Executor plug-in for token_transfer moves: recompute a request's KV on
     the destination from its (synthetic, seeded) hidden states.  One set of
-    synthetic weights per (device, model shape)."""
+    synthetic weights per (device, model shape).
 
-    def __init__(self, shapes, devices, with_q: bool = False, seed: int = 3, rope_theta: Optional[float] = None):
+    max_sms: the destination's compute budget as an SM share (0 = every SM):
+    each re-prefill runs on at most that many SMs, so decode steps of the
+    destination's resident requests keep the others (see
+    tools/bench_interference.py)."""
+
+    def __init__(self, shapes, devices, with_q: bool = False, seed: int = 3, rope_theta: Optional[float] = None,
+                 max_sms: int = 0):
         shapes = [shapes] if isinstance(shapes, ModelShape) else list(shapes)
         self.shapes = {s.name: s for s in shapes}
         self.with_q = with_q
         self.rope_theta = rope_theta   # post-RoPE K in the pool (KVM_REPREFILL_ROPE)
+        self.max_sms = max_sms
         self.weights = {(d, s.name): synthetic_weights(s, d, with_q=with_q, seed=seed)
                         for d in set(devices) for s in shapes}
 
@@ -131,7 +142,7 @@ class ReprefillEngine:
             blocks = torch.from_numpy(np.ascontiguousarray(dst_blocks, dtype=np.int32)).to(f"cuda:{dev}",
                                                                                           non_blocking=False)
             reprefill(pool, x, self.weights[(dev, pool.shape.name)], blocks, tok0=0, stream=stream,
-                      rope_theta=self.rope_theta)
+                      rope_theta=self.rope_theta, max_sms=self.max_sms)
             # keep the temporaries alive until the stream has consumed them
             x.record_stream(stream)
             blocks.record_stream(stream)

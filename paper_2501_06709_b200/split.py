@@ -106,11 +106,12 @@ def flops_per_token(shape, with_q: bool = True) -> int:
 
 def split_migrate_fused(src: KVPool, dst: KVPool, src_blocks_dev, dst_blocks_dev, plan: SplitPlan, x_suffix, w,
                         *, stream=None, table_row: int = 0, done_flag: int = 0, done_value: int = 1,
-                        single_cta: bool = False, rope_theta: float = 0.0) -> None:
+                        single_cta: bool = False, rope_theta: float = 0.0, max_sms: int = 0) -> None:
     """One-launch split migration on the destination (kvm_split_migrate): warps
     idle in the re-prefill GEMM copy the prefix while the tensor cores
     recompute the suffix.  src must be registered on dst's device (same GPU, or
-    an IPC-imported peer pool: the prefix is then pulled over NVLink)."""
+    an IPC-imported peer pool: the prefix is then pulled over NVLink).
+    max_sms > 0: at most that many SMs (KVM_REPREFILL_MAX_SMS)."""
     import torch
 
     per_layer = x_suffix is not None and x_suffix.dim() == 3   # [layers][suffix][d_model]
@@ -127,7 +128,8 @@ def split_migrate_fused(src: KVPool, dst: KVPool, src_blocks_dev, dst_blocks_dev
     a.q_out = None
     a.dst_table_row, a.done_flag, a.done_value = table_row or None, done_flag or None, done_value
     a.flags = (_native.KVM_REPREFILL_SINGLE_CTA if single_cta else 0) | (   # GEMM engine (default: CTA pair)
-        _native.KVM_REPREFILL_ROPE if rope_theta else 0) | (_native.KVM_REPREFILL_X_PER_LAYER if per_layer else 0)
+        _native.KVM_REPREFILL_ROPE if rope_theta else 0) | (_native.KVM_REPREFILL_X_PER_LAYER if per_layer else 0) | \
+        _native.KVM_REPREFILL_MAX_SMS(max_sms)
     a.rope_theta = float(rope_theta or 0.0)
     s = stream if stream is not None else torch.cuda.current_stream(dst.device)
     _native.check(_native.lib().kvm_split_migrate(ctypes.byref(a), ctypes.c_void_p(s.cuda_stream)),

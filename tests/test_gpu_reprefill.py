@@ -340,3 +340,34 @@ def test_reprefill_randomized(seed):
         ref = _rope_ref(ref, torch.arange(tok0, tok0 + rows, device="cuda"), 10000.0,
                         shape.q_cols if with_q else 0, shape.kv_cols)
     _check(shape, pool, blocks, tok0, rows, ref, q, before)
+
+
+@pytest.mark.parametrize("single_cta", [False, True])
+@pytest.mark.parametrize("max_sms", [1, 2, 7, 40, 100, 255])
+def test_reprefill_sm_budget_bit_identical(max_sms, single_cta):
+    """KVM_REPREFILL_MAX_SMS(n): the re-prefill on at most n SMs writes exactly the bytes the uncapped
+    launch writes (every output tile is the same contraction whichever CTA computes it), and Q too."""
+    shape = ModelShape("b", layers=3, kv_heads=4, head_dim=128, q_heads=8, d_model=512)
+    rows, tok0 = 700, 9
+    nblk = (tok0 + rows + 15) // 16
+    w = synthetic_weights(shape, 0, with_q=True, seed=5)
+    x = synthetic_hidden(shape, rows, 0, seed=6)
+    blocks = torch.randperm(nblk + 4, generator=torch.Generator().manual_seed(2))[:nblk].to(torch.int32).cuda()
+    outs = []
+    for cap in (0, max_sms):
+        pool = KVPool(shape, nblk + 4, dtype=torch.bfloat16)
+        pool.tensor.zero_()
+        q = torch.zeros(shape.layers, rows, shape.q_cols, dtype=torch.bfloat16, device="cuda")
+        reprefill(pool, x, w, blocks, tok0=tok0, q_out=q, single_cta=single_cta, max_sms=cap, rope_theta=10000.0)
+        torch.cuda.synchronize()
+        outs.append((pool.tensor.view(torch.int16).clone(), q.view(torch.int16).clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_reprefill_sm_budget_rejects_out_of_range():
+    shape = ModelShape("b", layers=1, kv_heads=1, head_dim=128, q_heads=1, d_model=64)
+    pool = KVPool(shape, 4, dtype=torch.bfloat16)
+    w = synthetic_weights(shape, 0, with_q=False, seed=1)
+    x = synthetic_hidden(shape, 16, 0, seed=1)
+    with pytest.raises(ValueError):
+        reprefill(pool, x, w, torch.arange(1, dtype=torch.int32, device="cuda"), max_sms=256)

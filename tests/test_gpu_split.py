@@ -205,7 +205,7 @@ def test_split_migrated_cache_decodes_like_the_original(single_cta, per_layer):
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVM_FUZZ_SEEDS", "50"))))
 def test_fused_split_randomized(seed):
     """Random geometry, request length, split point (incl. all-transfer and
-    all-recompute), RoPE, GEMM engine and block scatter for kvm_split_migrate:
+    all-recompute), RoPE, GEMM engine, SM budget and block scatter for kvm_split_migrate:
     prefix blocks bit-exact, suffix token slots within tolerance, the table
     row rewritten, nothing else in the destination pool written."""
     from paper_2501_06709_b200.split import split_migrate_fused
@@ -230,8 +230,10 @@ def test_fused_split_randomized(seed):
     x = synthetic_hidden(shape, max(plan.suffix, 1), 0, seed=seed)[:plan.suffix].contiguous()
     w = synthetic_weights(shape, 0, with_q=True, seed=seed + 1)
     table = BlockTable(1, plan.total_blocks + 1)
+    single_cta = bool(rng.integers(2))
     split_migrate_fused(src, dst, sb, db, plan, x if plan.suffix else None, w, table_row=table.row_ptr(0),
-                        single_cta=bool(rng.integers(2)), rope_theta=10000.0 if rope else 0.0)
+                        single_cta=single_cta, rope_theta=10000.0 if rope else 0.0,
+                        max_sms=int(rng.choice([0, 0, 2, 9, 64])))   # SM budget (KVM_REPREFILL_MAX_SMS)
     torch.cuda.synchronize()
     got = dst.tensor.view(torch.int16)
     pre = plan.prefix_blocks
