@@ -312,3 +312,25 @@ def test_oracle_decode_equals_flashinfer_vectors():
         got = reference_decode(pool, torch.from_numpy(q)[None], [torch.from_numpy(t) for t in tables], lens)
         want = torch.tensor([float.fromhex(x) for x in case["out_f32_hex"]]).view(len(lens), Hq, 128)
         torch.testing.assert_close(got[0], want, atol=2e-3, rtol=2e-2, msg=case["name"])
+
+
+def test_python_flag_constants_mirror_the_header():
+    """Every KVM_F_* / KVM_REPREFILL_* / KVM_DECODE_* / KVM_ERR_* value the Python side passes through
+    the C ABI equals include/kvmig.h's #define, macros (KVM_F_CTAS_PER_SM, KVM_REPREFILL_MAX_SMS)
+    evaluated for a few arguments."""
+    from paper_2501_06709_b200 import _native
+    with open(os.path.join(ROOT, "include", "kvmig.h")) as fh:
+        hdr = fh.read()
+    plain = dict(re.findall(r"#define (KVM_(?:F|REPREFILL|DECODE|ERR)_[A-Z_0-9]+) \(?(-?(?:0x)?[0-9a-fA-F]+)\)?", hdr))
+    checked = 0
+    for name, val in plain.items():
+        if hasattr(_native, name) and not callable(getattr(_native, name)):
+            assert getattr(_native, name) == int(val, 0), name
+            checked += 1
+    assert checked >= 16
+    assert "#define KVM_F_CTAS_PER_SM(n) (((n)&0xff) << 8)" in hdr
+    assert "#define KVM_REPREFILL_MAX_SMS(n) (((n)&0xff) << 8)" in hdr
+    for n in (0, 1, 64, 148, 255):
+        assert _native.KVM_F_CTAS_PER_SM(n) == (n & 0xFF) << 8
+        assert _native.KVM_REPREFILL_MAX_SMS(n) == (n & 0xFF) << 8
+        assert _native.KVM_REPREFILL_MAX_SMS(n) & ~int(plain["KVM_REPREFILL_SMS_MASK"], 0) == 0
