@@ -148,6 +148,22 @@ class ReprefillEngine:
             blocks.record_stream(stream)
 
 
+def sm_budget(fraction: float, sm_count: int) -> int:
+    """The destination's compute budget as an SM share: the reference gives
+    re-prefill `budget_fraction` of the destination's prefill capacity per
+    epoch (Boundaries.comp_budget = prefill rate x epoch x fraction,
+    migration.py:77-91); a re-prefill confined to that fraction of the SMs
+    (KVM_REPREFILL_MAX_SMS) runs at about that fraction of the full rate while
+    decode keeps the rest of the GPU.  Returns the cap for
+    ReprefillEngine(max_sms=...) (0 = every SM, for fraction >= 1), at least 2
+    (one CTA pair)."""
+    if not fraction > 0:
+        raise ValueError("fraction must be > 0")
+    if fraction >= 1:
+        return 0
+    return max(2, min(255, int(round(fraction * sm_count))))
+
+
 def split_point(tokens: int, bytes_per_token: int, link_bytes_per_s: float,
                 flops_per_token: float, tensor_flops_per_s: float, block_tokens: int = 16) -> int:
     """Extension of the binary kv/token choice (migration.py:155-169): transfer

@@ -334,3 +334,13 @@ def test_python_flag_constants_mirror_the_header():
         assert _native.KVM_F_CTAS_PER_SM(n) == (n & 0xFF) << 8
         assert _native.KVM_REPREFILL_MAX_SMS(n) == (n & 0xFF) << 8
         assert _native.KVM_REPREFILL_MAX_SMS(n) & ~int(plain["KVM_REPREFILL_SMS_MASK"], 0) == 0
+
+
+def test_sm_budget_maps_the_comp_budget_fraction():
+    from paper_2501_06709_b200.reprefill import sm_budget
+    assert sm_budget(0.2, 148) == 30          # the reference's default budget_fraction (config.py:70)
+    assert sm_budget(1.0, 148) == 0 and sm_budget(3.0, 148) == 0     # every SM
+    assert sm_budget(0.001, 148) == 2         # at least one CTA pair
+    assert sm_budget(0.5, 1000) == 255        # the flag's 8-bit field
+    with pytest.raises(ValueError):
+        sm_budget(0.0, 148)

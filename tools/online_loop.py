@@ -38,7 +38,7 @@ from paper_2501_06709_b200.executor import MigrationExecutor  # noqa: E402
 from paper_2501_06709_b200.kvcache import BlockAllocator, BlockTable, KVPool  # noqa: E402
 from paper_2501_06709_b200.planner import Topology, load_boundaries, plan_hybrid  # noqa: E402
 from paper_2501_06709_b200.replay import FingerprintedExecutor, pool_blocks_for  # noqa: E402
-from paper_2501_06709_b200.reprefill import ReprefillEngine  # noqa: E402
+from paper_2501_06709_b200.reprefill import ReprefillEngine, sm_budget  # noqa: E402
 from paper_2501_06709_b200.workload import LengthDistribution, gen_poisson  # noqa: E402
 from replay_trace import FULL, MINI  # noqa: E402
 
@@ -176,7 +176,8 @@ def dry_run_pool_blocks(fx, trace, models, bpt, topo, bounds, shapes, max_slots,
 
 
 def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_every: int = 100,
-               seed=None, max_slots=None, split: bool = False, devices=None, margin: float = 1.02) -> dict:
+               seed=None, max_slots=None, split: bool = False, devices=None, margin: float = 1.02,
+               reprefill_sm_fraction: float = 1.0) -> dict:
     with open(fixture) as fh:
         fx = json.load(fh)
     cfg = fx["config"]
@@ -210,8 +211,11 @@ def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_e
             pools[g][name] = KVPool(sh, nb, device=dev, dtype=torch.bfloat16)
             tables[g][name] = BlockTable(512, nb, device=dev)
     used = sorted({s.name for per in pools.values() for s in (p.shape for p in per.values())})
+    # re-prefill on the budget fraction of the SMs (reprefill.sm_budget; 1.0 = every SM)
+    max_sms = sm_budget(reprefill_sm_fraction, torch.cuda.get_device_properties(0).multi_processor_count)
     rp = ReprefillEngine([s for s in shapes.values() if s.name in used], sorted({p.device for per in pools.values()
-                                                                               for p in per.values()}), with_q=False)
+                                                                               for p in per.values()}), with_q=False,
+                         max_sms=max_sms)
     inner = MigrationExecutor(pools, tables, engine=engine, reprefill=rp, timing=True)
     ex = FingerprintedExecutor(inner)
     clock = Clock()
@@ -253,7 +257,7 @@ def run_online(fixture: str, shape: str = "mini", engine: str = "bulk", verify_e
         "fixture": os.path.basename(fixture), "seed": seed, "shape": shape, "devices": len(devices),
         "logical_gpus": len(inner.pools), "device_of_gpu": {g: devices[g % len(devices)] for g in pools},
         "pool_gib_per_device": {d: round(b / 2 ** 30, 2) for d, b in per_dev_bytes.items()},
-        "slots": n, "requests": len(trace), "peak_gpus": max(out.active_gpus),
+        "slots": n, "requests": len(trace), "peak_gpus": max(out.active_gpus), "reprefill_max_sms": max_sms,
         "plan_rows": len(out.plan_rows), "executed_records": sum(len(r.records) for r in ex.reports),
         "bytes_moved": out.bytes_moved, "reconciled_moves": out.reconciled_moves,
         "splits": sum(1 for r in out.plan_rows if r[6] == "split_transfer"),
@@ -278,9 +282,12 @@ def main():
                     help="another trace seed (same config); decisions are then not checked against the fixture")
     ap.add_argument("--devices", type=int, default=None, help="spread logical GPUs over the first N devices")
     ap.add_argument("--out", default=None, help="also write the JSON result here (bench.py's subprocess run)")
+    ap.add_argument("--reprefill-sm-fraction", type=float, default=1.0,
+                    help="run token_transfer re-prefills on this fraction of the SMs (e.g. the run's budget_fraction)")
     a = ap.parse_args()
     res = run_online(a.fixture, a.shape, a.engine, a.verify_every, a.seed, a.max_slots, a.split,
-                     devices=None if a.devices is None else list(range(a.devices)))
+                     devices=None if a.devices is None else list(range(a.devices)),
+                     reprefill_sm_fraction=a.reprefill_sm_fraction)
     if a.out:
         with open(a.out, "w") as fh:
             json.dump(res, fh)
