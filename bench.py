@@ -577,7 +577,7 @@ class Ring:
         torch.cuda.synchronize()
         self.ctx["barrier"]()
 
-    def step(self, engine: str, host: bool, ev=None):
+    def step(self, engine: str, host: bool, ev=None, max_sms: int = 0):
         """Push this rank's request to send_to, then make the incoming one (from
         recv_from) a dependency of this rank's stream."""
         ri, shared = self.ctx["ri"], self.ctx["shared"]
@@ -585,7 +585,7 @@ class Ring:
         if ev is not None:
             ev[0].record(self.stream)
         self.link.push(ri.send_to, self.sb_np if host else self.sb_dev, self.seq, engine=engine,
-                       stream=self.stream)
+                       stream=self.stream, max_sms=max_sms)
         if ev is not None:
             ev[1].record(self.stream)
         if shared:
@@ -634,7 +634,7 @@ class Ring:
                   f"{sums[ri.recv_from]}, table row ok {row_ok}", file=sys.stderr)
         return self.ctx["all_ok"](ok)
 
-    def timed(self, engine: str, K: int, W: int, meter=None, clocks=None) -> dict:
+    def timed(self, engine: str, K: int, W: int, meter=None, clocks=None, max_sms: int = 0) -> dict:
         import torch
 
         from paper_2501_06709_b200 import _native
@@ -644,7 +644,7 @@ class Ring:
         self.reset()
         with torch.cuda.stream(self.stream):
             for _ in range(W):
-                self.step(engine, host=False)
+                self.step(engine, host=False, max_sms=max_sms)
         self.stream.synchronize()
         self.ctx["barrier"]()
         ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
@@ -659,7 +659,7 @@ class Ring:
         with torch.cuda.stream(self.stream):
             t0.record(self.stream)
             for i in range(K):
-                self.step(engine, host=False, ev=ev[i])
+                self.step(engine, host=False, ev=ev[i], max_sms=max_sms)
             t1.record(self.stream)
         self.stream.synchronize()
         torch.cuda.synchronize()
@@ -909,6 +909,15 @@ def run_ring(args, ctx) -> int:
         ring.close()
         return 1
     bit_exact = gates[engine]
+    # how many SMs the link-bound push needs: the chosen engine on 32 and 64 SMs (KVM_F_MAX_SMS) beside
+    # the whole GPU (the timed run below uses the whole GPU); one SM's bulk pipeline moves ~37 GB/s
+    # (tools/bench_copy_sms.py), so ~21 SMs' worth saturates 0.77 TB/s
+    sm_ab = {}
+    for cap in (32, 64, 0):
+        r = ring.timed(engine, K=5, W=2, max_sms=cap)
+        sm_ab[str(cap or "all")] = {"push_ms_mean": round(r["push_ms_mean"], 4),
+                                    "GBps_per_gpu": round(ring.kv_bytes / (r["push_ms_mean"] / 1e3) / 1e9, 1),
+                                    "all_landed": r["all_landed"]}
     meter = NvlinkMeter(dev)
     clocks = ClockSampler(dev)
     main = ring.timed(engine, args.steps, args.warmup, meter=meter, clocks=clocks)
@@ -1009,6 +1018,7 @@ def run_ring(args, ctx) -> int:
                                     f"{ctx['ndev']} GPU (CUDA IPC test mode, no NVLink hop)"),
                        "baseline_config": cfg_desc, "kv_bytes_per_rank_per_step": kv_bytes, "blocks": n,
                        "pool_blocks": nb, "engine": engine, "engine_ab": ab or None,
+                       "push_sm_budget_ab": sm_ab or None,
                        "l2": "inputs larger than L2 (%.1f GiB per step per rank)" % (kv_bytes / 2 ** 30),
                        "parallelism": f"{world} ranks, one process per GPU" +
                                       (f" ({ctx['ndev']} physical GPU, shared)" if shared else ""),

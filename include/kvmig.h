@@ -80,6 +80,12 @@ extern "C" {
  * it can share SMs with a concurrently running persistent kernel (e.g. the
  * re-prefill GEMM of a split move on the same GPU). */
 #define KVM_F_CTAS_PER_SM(n) (((n)&0xff) << 8)
+/* Run the copy on at most n SMs' worth of CTAs (bits 16..23; 0 = the whole
+ * GPU).  A push whose bound is a link (NVLink ~0.77 TB/s, PCIe ~56 GB/s) needs
+ * far fewer SMs than the HBM-bound compaction; the rest stay with serving.
+ * Bulk engine: at most n CTAs, one per SM (its 128 KiB staging ring admits
+ * one CTA per SM); LDG engine: n x its per-SM occupancy CTAs. */
+#define KVM_F_MAX_SMS(n) (((n)&0xff) << 16)
 
 /* Pool geometry. */
 typedef struct kvm_pool_desc {

@@ -44,6 +44,10 @@ def KVM_F_CTAS_PER_SM(n: int) -> int:
     return (n & 0xFF) << 8
 
 
+def KVM_F_MAX_SMS(n: int) -> int:
+    return (n & 0xFF) << 16
+
+
 def KVM_REPREFILL_MAX_SMS(n: int) -> int:
     return (n & 0xFF) << 8
 

@@ -758,17 +758,27 @@ static int validate_batch_disjoint(const kvm_move* moves, int n) {
   return rc;
 }
 
+// The bulk engine's persistent grid for `flags`: KVM_F_CTAS_PER_SM and KVM_F_MAX_SMS caps applied.
+static int bulk_grid_for(const DevState& ds, int flags, int nsm) {
+  const int cap = (flags >> 8) & 0xff;
+  const int max_sms = (flags >> 16) & 0xff;
+  int g = cap ? std::min(ds.bulk_grid, cap * nsm) : ds.bulk_grid;
+  if (max_sms) g = std::min(g, max_sms);
+  return std::max(g, 1);
+}
+
 template <class P>
 static int launch_copy(const P& p, int64_t tiles, bool any_empty, int flags, int device, const DevState& ds,
                        cudaStream_t stream) {
   constexpr bool kSmall = std::is_same<P, SmallParams>::value;
   if (tiles > 0) {
     const int cap = (flags >> 8) & 0xff;
+    const int max_sms = (flags >> 16) & 0xff;
     const int nsm = sm_count(device);
     // A move that fits in one tile per CTA of the 2-stage kernel (3 CTAs/SM)
     // gets it: more SMs' worth of bulk units for a latency-bound copy.  Larger
     // moves keep the 4-stage pipeline (1 CTA/SM), which streams better.
-    const bool shallow = kSmall && tiles <= ds.bulk_grid_small && !cap;
+    const bool shallow = kSmall && tiles <= ds.bulk_grid_small && !cap && !max_sms;
     if ((flags & KVM_F_ENGINE_BULK) && shallow) {
       const int grid = (int)tiles;
       const int smem = bulk_smem_bytes(kBulkStagesSmall);
@@ -777,14 +787,16 @@ static int launch_copy(const P& p, int64_t tiles, bool any_empty, int flags, int
       else
         migrate_bulk_kernel<false, P, kBulkStagesSmall><<<grid, 32, smem, stream>>>(p);
     } else if (flags & KVM_F_ENGINE_BULK) {
-      const int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.bulk_grid, cap * nsm) : ds.bulk_grid);
+      const int grid = (int)std::min<int64_t>(tiles, bulk_grid_for(ds, flags, nsm));
       const int smem = bulk_smem_bytes(kBulkStages);
       if (flags & KVM_F_L2_EVICT_FIRST)
         migrate_bulk_kernel<true, P, kBulkStages><<<grid, 32, smem, stream>>>(p);
       else
         migrate_bulk_kernel<false, P, kBulkStages><<<grid, 32, smem, stream>>>(p);
     } else {
-      const int grid = (int)std::min<int64_t>(tiles, cap ? std::min(ds.ldg_grid, cap * nsm) : ds.ldg_grid);
+      int lg = cap ? std::min(ds.ldg_grid, cap * nsm) : ds.ldg_grid;
+      if (max_sms) lg = std::min(lg, std::max(1, max_sms * (ds.ldg_grid / nsm)));
+      const int grid = (int)std::min<int64_t>(tiles, lg);
       if (flags & KVM_F_L2_EVICT_FIRST)
         migrate_ldg_kernel<true, P><<<grid, kLdgThreads, 0, stream>>>(p);
       else
@@ -891,8 +903,9 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
     return c < 1 ? 1 : (c > 64 ? 64 : c);
   }();
   const int cap = (flags >> 8) & 0xff;
-  const bool shallow = std::is_same<P, SmallParams>::value && tiles <= ds.bulk_grid_small && !cap;
-  const int big_grid = cap ? std::min(ds.bulk_grid, cap * sm_count(device)) : ds.bulk_grid;
+  const bool shallow = std::is_same<P, SmallParams>::value && tiles <= ds.bulk_grid_small && !cap &&
+                       !((flags >> 16) & 0xff);
+  const int big_grid = bulk_grid_for(ds, flags, sm_count(device));
   const bool dyn = (flags & KVM_F_ENGINE_BULK) && !shallow && tiles >= 2 * (int64_t)big_grid * chunk &&
                    !static_copy;
   constexpr size_t kQueueWords = 2;
@@ -1195,7 +1208,7 @@ int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream) {
   if (n_moves == 0) return KVM_OK;
   if (!moves) return fail(KVM_ERR_INVALID, "moves is NULL");
   if (flags & ~(KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK | KVM_F_L2_EVICT_FIRST | KVM_F_SYS_SCOPE |
-                KVM_F_CTAS_PER_SM(0xff)))
+                KVM_F_CTAS_PER_SM(0xff) | KVM_F_MAX_SMS(0xff)))
     return fail(KVM_ERR_INVALID, "unknown flags");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < n_moves; i += KVM_MAX_MOVES) {

@@ -101,10 +101,11 @@ class PeerLink:
         return p
 
     def push(self, dst_rank: int, src_blocks, seq: int, engine: str = "bulk", stream=None,
-             layer_flags: int = 0) -> None:
+             layer_flags: int = 0, max_sms: int = 0) -> None:
         """Migrate the request held in `src_blocks` (host int32 array -> host
         block lists, or an int32 CUDA tensor) into `dst_rank`'s advertised
-        receive blocks; asynchronous on `stream`."""
+        receive blocks; asynchronous on `stream`.  max_sms > 0: the push runs
+        on at most that many SMs (KVM_F_MAX_SMS; the link, not the SMs, bounds it)."""
         import torch
 
         from .executor import ENGINES
@@ -115,7 +116,7 @@ class PeerLink:
         n = len(hb)
         m = self._native.Move()
         m.src_pool, m.dst_pool, m.n_blocks, m.done_value = self.pool.pool_id, mapped.pool_id, n, int(seq)
-        flags = ENGINES[engine]
+        flags = ENGINES[engine] | self._native.KVM_F_MAX_SMS(max_sms)
         if isinstance(src_blocks, np.ndarray):
             sb = np.ascontiguousarray(src_blocks, dtype=np.int32)
             if len(sb) != n:

@@ -117,7 +117,7 @@ class MigrationExecutor:
 
     def __init__(self, pools: Dict[int, KVPool], tables: Optional[Dict[int, BlockTable]] = None,
                  engine: str = "bulk", reprefill: Optional[Callable] = None, timing: bool = False,
-                 split_kernels: str = "auto"):
+                 split_kernels: str = "auto", copy_sms: int = 0):
         import torch
 
         if split_kernels not in ("auto", "fused", "two"):
@@ -142,7 +142,11 @@ class MigrationExecutor:
                 self.tables[g] = {m: t for m in self.pools[g]}
         models = {m for per in self.pools.values() for m in per}
         self.default_model = next(iter(models)) if len(models) == 1 else None
-        self.engine_flag = ENGINES[engine]
+        if not 0 <= copy_sms <= 255:
+            raise ConfigError("copy_sms must be in [0, 255] (0 = the whole GPU)")
+        # copy_sms > 0: every kvm_migrate / kvm_compact of this executor runs on at most that many SMs
+        # (KVM_F_MAX_SMS): a push bound by a link needs far fewer SMs than the HBM-bound compaction
+        self.engine_flag = ENGINES[engine] | _native.KVM_F_MAX_SMS(copy_sms)
         self.reprefill = reprefill
         self.loc: Dict[int, Residency] = {}
         self._streams: Dict[int, "torch.cuda.Stream"] = {}

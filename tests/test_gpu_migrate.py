@@ -664,3 +664,46 @@ def test_randomized_queue_sized_batches_vs_oracle(seed):
             assert np.array_equal(table.rows[table.slot(i), :len(db)].cpu().numpy(), db)
         if kind == 2:
             assert (c[8 + i * sh.layers: 8 + (i + 1) * sh.layers] == i + 1).all()   # layer flags carry the value
+
+
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+@pytest.mark.parametrize("max_sms", [1, 3, 16, 148, 255])
+def test_copy_sm_budget_bit_exact(engine, max_sms):
+    """KVM_F_MAX_SMS(n): the copy on at most n SMs' worth of CTAs (down to one CTA, where the bulk
+    engine's tile queue takes over from the second chunk) is byte-exact against the oracle over the
+    whole destination pool, table row and flag included; the executor's copy_sms applies it."""
+    shape = ModelShape("cap", layers=4, kv_heads=8, head_dim=128, q_heads=8, d_model=1024)   # 32 KiB pieces
+    nb = 160
+    src, dst = KVPool(shape, nb), KVPool(shape, nb)
+    _fill(src, 21)
+    _fill(dst, 22)
+    rng = np.random.default_rng(max_sms)
+    sb = rng.permutation(nb)[:120].astype(np.int32)
+    dst.allocator.take(rng.permutation(nb)[:30])
+    db = dst.allocator.alloc(120)
+    exp = dst.tensor.view(torch.int16).cpu().numpy()
+    orc.migrate(src.tensor.view(torch.int16).cpu().numpy(), _desc(src), exp, _desc(dst), sb, db)
+    table = BlockTable(2, 128)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    m = _move(src, dst, sb, db, table.row_ptr(3), flag.data_ptr(), value=7)
+    _run([m], _native.KVM_F_BLOCKS_ON_HOST | ENGINES[engine] | _native.KVM_F_MAX_SMS(max_sms))
+    assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
+    assert int(flag.item()) == 7
+    assert np.array_equal(table.rows[table.slot(3), :120].cpu().numpy(), db)
+
+
+def test_executor_copy_sms():
+    from paper_2501_06709_b200.executor import MigrationExecutor
+    from paper_2501_06709_b200.planner import KV_TRANSFER, PendingMove, PlannedMove
+
+    pools = {0: KVPool(SMALL, 64), 1: KVPool(SMALL, 64)}
+    for i, p in pools.items():
+        _fill(p, 30 + i)
+    ex = MigrationExecutor(pools, {0: BlockTable(4, 32), 1: BlockTable(4, 32)}, copy_sms=2)
+    ex.admit(9, 0, 300)
+    before = pools[0].tensor.view(torch.int16)[:, :, torch.from_numpy(ex.where(9).blocks).long().cuda()].clone()
+    ex.execute([PlannedMove(PendingMove(9, 0, 1, 0, 300), KV_TRANSFER)])
+    after = pools[1].tensor.view(torch.int16)[:, :, torch.from_numpy(ex.where(9).blocks).long().cuda()]
+    assert ex.where(9).gpu == 1 and torch.equal(before, after)
+    with pytest.raises(ConfigError):
+        MigrationExecutor(pools, copy_sms=256)

@@ -67,11 +67,15 @@ def main():
     sb = torch.arange(mig_n, dtype=torch.int32, device="cuda")
     db = torch.arange(8, mig_n + 8, dtype=torch.int32, device="cuda")
 
-    def migrate():
-        m = _native.Move()
-        m.src_pool, m.dst_pool, m.n_blocks = src.pool_id, dst.pool_id, mig_n
-        m.src_blocks, m.dst_blocks = sb.data_ptr(), db.data_ptr()
-        _native.check(lib.kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_ENGINE_BULK, ctypes.c_void_p(bg.cuda_stream)))
+    def migrate_on(max_sms):
+        def migrate():
+            m = _native.Move()
+            m.src_pool, m.dst_pool, m.n_blocks = src.pool_id, dst.pool_id, mig_n
+            m.src_blocks, m.dst_blocks = sb.data_ptr(), db.data_ptr()
+            _native.check(lib.kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_ENGINE_BULK | _native.KVM_F_MAX_SMS(max_sms),
+                                          ctypes.c_void_p(bg.cuda_stream)))
+        return migrate
+    migrate = migrate_on(0)
 
     # background 2: the 13B re-prefill of a 1 360-token suffix
     rows = 1360
@@ -144,10 +148,12 @@ def main():
     res = {"decode": f"8 x 7B requests x {seq} tokens, 32 layers, one paged-decode launch per step, high-priority "
                      f"stream", "steps": a.steps, "arms": {}}
     dec_alone = decode_alone_ms()
-    alone_bg = {"incoming_migrate_7b_4k": bg_time(migrate), "reprefill_all_sms": bg_time(rp(0))}
+    alone_bg = {"incoming_migrate_7b_4k": bg_time(migrate), "incoming_migrate_7b_4k_32_sms": bg_time(migrate_on(32)),
+                "reprefill_all_sms": bg_time(rp(0))}
     for cap in (112, 96, 64):
         alone_bg[f"reprefill_{cap}_sms"] = bg_time(rp(cap))
-    arms = [("alone", None), ("incoming_migrate_7b_4k", migrate), ("reprefill_all_sms", rp(0)),
+    arms = [("alone", None), ("incoming_migrate_7b_4k", migrate), ("incoming_migrate_7b_4k_32_sms", migrate_on(32)),
+            ("reprefill_all_sms", rp(0)),
             ("reprefill_112_sms", rp(112)), ("reprefill_96_sms", rp(96)), ("reprefill_64_sms", rp(64))]
     for name, fn in arms:
         res["arms"][name] = run_arm(fn, alone_bg.get(name))
