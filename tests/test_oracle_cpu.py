@@ -330,8 +330,10 @@ def test_python_flag_constants_mirror_the_header():
     assert checked >= 16
     assert "#define KVM_F_CTAS_PER_SM(n) (((n)&0xff) << 8)" in hdr
     assert "#define KVM_REPREFILL_MAX_SMS(n) (((n)&0xff) << 8)" in hdr
+    assert "#define KVM_F_MAX_SMS(n) (((n)&0xff) << 16)" in hdr
     for n in (0, 1, 64, 148, 255):
         assert _native.KVM_F_CTAS_PER_SM(n) == (n & 0xFF) << 8
+        assert _native.KVM_F_MAX_SMS(n) == (n & 0xFF) << 16
         assert _native.KVM_REPREFILL_MAX_SMS(n) == (n & 0xFF) << 8
         assert _native.KVM_REPREFILL_MAX_SMS(n) & ~int(plain["KVM_REPREFILL_SMS_MASK"], 0) == 0
 
