@@ -949,10 +949,10 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
     p.queue = slot->ctr + slot->queue_word;
     p.queue_other = slot->ctr + (slot->queue_word ^ 1);
     p.queue_chunk = chunk;
-    slot->queue_word ^= 1;
   }
   if (off > 0) KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
   if ((rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream))) return rc;
+  if (dyn) slot->queue_word ^= 1;   // only a launched kernel zeroes the other word for the next use
   if (slot) {
     KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
     slot->pending = true;
