@@ -769,7 +769,7 @@ static int bulk_grid_for(const DevState& ds, int flags, int nsm) {
 
 template <class P>
 static int launch_copy(const P& p, int64_t tiles, bool any_empty, int flags, int device, const DevState& ds,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, bool* copy_launched) {
   constexpr bool kSmall = std::is_same<P, SmallParams>::value;
   if (tiles > 0) {
     const int cap = (flags >> 8) & 0xff;
@@ -804,6 +804,7 @@ static int launch_copy(const P& p, int64_t tiles, bool any_empty, int flags, int
     }
     KVM_CUDA_TRY(cudaGetLastError());
     count_launch();
+    *copy_launched = true;
   }
   if (any_empty) {
     finalize_empty_kernel<P><<<1, 32, 0, stream>>>(p);
@@ -951,8 +952,10 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
     p.queue_chunk = chunk;
   }
   if (off > 0) KVM_CUDA_TRY(cudaMemcpyAsync(slot->dev, slot->host, off, cudaMemcpyHostToDevice, stream));
-  if ((rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream))) return rc;
-  if (dyn) slot->queue_word ^= 1;   // only a launched kernel zeroes the other word for the next use
+  bool copied = false;
+  rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream, &copied);
+  if (dyn && copied) slot->queue_word ^= 1;   // only a launched copy kernel zeroes the other word
+  if (rc) return rc;
   if (slot) {
     KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
     slot->pending = true;
