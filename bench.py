@@ -240,6 +240,8 @@ def _kernel_extras(device: int) -> dict:
         out["remote_link_pcie"] = _tool_json("bench_host_link.py", ["--iters", "5"], timeout_s=300)
         # decode of resident requests beside an incoming migration / a re-prefill on every SM / on an SM budget
         out["decode_interference"] = _tool_json("bench_interference.py", ["--steps", "30"], timeout_s=300)
+        # copy throughput against the SM budget (KVM_F_MAX_SMS): per-SM rate, SMs to saturate HBM / PCIe
+        out["copy_sm_budget"] = _tool_json("bench_copy_sms.py", [], timeout_s=300)
     return out
 
 

@@ -955,12 +955,12 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
   bool copied = false;
   rc = launch_copy(p, tiles, any_empty, flags, device, ds, stream, &copied);
   if (dyn && copied) slot->queue_word ^= 1;   // only a launched copy kernel zeroes the other word
-  if (rc) return rc;
-  if (slot) {
-    KVM_CUDA_TRY(cudaEventRecord(slot->ev, stream));
-    slot->pending = true;
+  if (slot) {   // whatever was queued (staging copy, kernels) holds the slot until this event, error or not
+    const cudaError_t e = cudaEventRecord(slot->ev, stream);
+    slot->pending = e == cudaSuccess;
+    if (!rc && e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(slot)");
   }
-  return KVM_OK;
+  return rc;
 }
 
 static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t stream) {
