@@ -18,6 +18,20 @@ def _nvml():
     return pynvml
 
 
+def _handle(nv, device: int):
+    """The NVML handle of CUDA device `device`, matched by PCI address: NVML
+    enumerates every GPU of the host in bus order while CUDA numbers only the
+    visible ones (CUDA_VISIBLE_DEVICES), so the indices need not agree."""
+    try:
+        import torch
+
+        pr = torch.cuda.get_device_properties(device)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        return nv.nvmlDeviceGetHandleByPciBusId(bus)
+    except Exception:
+        return nv.nvmlDeviceGetHandleByIndex(device)
+
+
 class ClockSampler:
     """NVML sampling of the SM clock and the clock-event (throttle) reasons
     every 5 ms while the context is open."""
@@ -31,7 +45,7 @@ class ClockSampler:
         try:
             nv = _nvml()
             self._nv = nv
-            self._h = nv.nvmlDeviceGetHandleByIndex(device)
+            self._h = _handle(nv, device)
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
         except Exception:
             self._nv = None
@@ -104,7 +118,7 @@ class NvlinkMeter:
         try:
             nv = _nvml()
             self._nv = nv
-            self._h = nv.nvmlDeviceGetHandleByIndex(device)
+            self._h = _handle(nv, device)
         except Exception as e:
             self._nv, self.error = None, f"NVML unavailable: {e!r}"[:200]
             return
@@ -240,7 +254,7 @@ class EnergyMeter:
         try:
             nv = _nvml()
             self._nv = nv
-            self._h = nv.nvmlDeviceGetHandleByIndex(device)
+            self._h = _handle(nv, device)
             self.limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1e3
             nv.nvmlDeviceGetTotalEnergyConsumption(self._h)
         except Exception as e:
