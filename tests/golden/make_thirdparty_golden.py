@@ -21,6 +21,12 @@ Vectors
                 Output: sha256 of the whole destination pool (and of the source,
                 which must not change).  Cases cover src != dst pools and the
                 in-place compaction (src pool == dst pool, disjoint block sets).
+  placement     vLLM 0.22 `_C_cache_ops.reshape_and_cache_flash(key, value,
+                key_cache, value_cache, slot_mapping, "auto", ...)`: token t of a
+                re-prefilled suffix lands in slot (tok0 + t) of the request's
+                block list; bf16 K = V = X from numpy, output sha256 of the
+                key cache.  The CPU test reproduces it with the C oracle's
+                re-prefill under identity projections (K = X exactly).
   decode        flashinfer 0.6 BatchDecodeWithPagedKVCacheWrapper (NHD layout)
                 over one layer's K/V planes of such a pool, fp16, GQA ratios
                 1/4/8, ragged lengths: output as float32 hex per element.
@@ -46,6 +52,13 @@ SWAP_CASES = [   # (name, layers, kv_heads, head_dim, src_nb, dst_nb, n_moved, s
     ("all_blocks", 2, 2, 64, 12, 12, 12, 4, False),
     ("compact_in_place", 3, 2, 32, 48, 48, 20, 5, True),
     ("llama_piece", 2, 8, 128, 32, 40, 17, 6, False),
+]
+
+PLACEMENT_CASES = [  # (name, kv_heads, rows, tok0, seed)
+    ("one_row", 2, 1, 0, 21),
+    ("ragged", 4, 77, 5, 22),
+    ("deep_offset", 1, 300, 4000, 23),
+    ("block_aligned", 8, 128, 16, 24),
 ]
 
 DECODE_CASES = [  # (name, kv_heads, q_heads, seq_lens, seed)
@@ -86,6 +99,17 @@ def decode_inputs(kv_heads, q_heads, seq_lens, seed, head_dim=128):
     return k, v, tables, q
 
 
+def placement_inputs(kv_heads, rows, tok0, seed, head_dim=128):
+    """bf16 bits of X [rows][kv_heads * head_dim] and the request's block list."""
+    rng = np.random.default_rng(seed)
+    f = rng.standard_normal((rows, kv_heads * head_dim)).astype(np.float32)
+    x = (f.view(np.uint32) >> 16).astype(np.uint16)           # bf16 by truncation: exact bf16 values
+    nblk = (tok0 + rows + 15) // 16
+    nb = nblk + 3
+    blocks = rng.permutation(nb)[:nblk].astype(np.int32)
+    return x, blocks, nb
+
+
 def sha(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -108,6 +132,25 @@ def gen_swap():
                     "n": n, "seed": seed, "in_place": in_place,
                     "dst_sha256": sha(res),
                     "src_sha256": sha(s_t.cpu().numpy().view(np.uint16)) if not in_place else None})
+    return out
+
+
+def gen_placement():
+    import vllm._custom_ops as vops
+    out = []
+    for name, H, rows, tok0, seed in PLACEMENT_CASES:
+        x, blocks, nb = placement_inputs(H, rows, tok0, seed)
+        xt = torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16).view(rows, H, 128).contiguous()
+        kc = torch.zeros(nb, 16, H, 128, dtype=torch.bfloat16, device="cuda")
+        vc = torch.zeros_like(kc)
+        pos = np.arange(tok0, tok0 + rows)
+        slots = torch.from_numpy((blocks[pos // 16].astype(np.int64) * 16 + pos % 16)).cuda()
+        one = torch.ones((), dtype=torch.float32, device="cuda")
+        vops.reshape_and_cache_flash(xt, xt, kc, vc, slots, "auto", one, one)
+        torch.cuda.synchronize()
+        out.append({"name": name, "kv_heads": H, "rows": rows, "tok0": tok0, "seed": seed,
+                    "key_cache_sha256": sha(kc.view(torch.int16).cpu().numpy()),
+                    "value_cache_sha256": sha(vc.view(torch.int16).cpu().numpy())})
     return out
 
 
@@ -139,7 +182,7 @@ def main():
     res = {"generator": "tests/golden/make_thirdparty_golden.py",
            "libraries": {"vllm": vllm.__version__, "flashinfer": flashinfer.__version__,
                          "torch": torch.__version__, "device": torch.cuda.get_device_name(0)},
-           "swap_blocks": gen_swap(), "decode": gen_decode()}
+           "swap_blocks": gen_swap(), "placement": gen_placement(), "decode": gen_decode()}
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as fh:
         json.dump(res, fh, indent=1)

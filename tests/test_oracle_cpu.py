@@ -346,3 +346,28 @@ def test_sm_budget_maps_the_comp_budget_fraction():
     assert sm_budget(0.5, 1000) == 255        # the flag's 8-bit field
     with pytest.raises(ValueError):
         sm_budget(0.0, 148)
+
+
+def test_oracle_reprefill_placement_equals_vllm_reshape_and_cache_vectors():
+    """The C oracle's re-prefill places token t of the suffix in slot (tok0 + t) of the request's blocks
+    exactly as vLLM's reshape_and_cache_flash does (recorded on a B200): with identity K / V projections
+    (K = V = X, exact in fp32 accumulation) the oracle's K and V planes hash like vLLM's key / value caches."""
+    import hashlib
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("mk", os.path.join(ROOT, "tests", "golden",
+                                                                    "make_thirdparty_golden.py"))
+    mk = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mk)
+    cases = _tp_vectors()["placement"]
+    assert len(cases) == len(mk.PLACEMENT_CASES)
+    for case in cases:
+        H, rows, tok0 = case["kv_heads"], case["rows"], case["tok0"]
+        x, blocks, nb = mk.placement_inputs(H, rows, tok0, case["seed"])
+        kvd = H * 128
+        eye = np.zeros((kvd, kvd), dtype=np.uint16)
+        eye[np.arange(kvd), np.arange(kvd)] = 0x3F80                       # bf16 1.0
+        w = np.ascontiguousarray(np.concatenate([eye, eye])[None])          # [1][2 kvd][kvd]: K = V = X
+        pool = np.zeros((1, 2, nb, 16, H, 128), dtype=np.uint16)
+        orc.reprefill(orc.desc(1, H, 128, 16, nb), pool, blocks, np.ascontiguousarray(x), w, rows, kvd, 0, tok0)
+        assert hashlib.sha256(pool[0, 0].tobytes()).hexdigest() == case["key_cache_sha256"], case["name"]
+        assert hashlib.sha256(pool[0, 1].tobytes()).hexdigest() == case["value_cache_sha256"], case["name"]
