@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(kLdgThreads)
 }
 
 // ------------------------- bulk-copy (TMA unit) engine ---------------------
-constexpr int kBulkStages = 4;        // batch launches (1 CTA/SM)
+#ifndef KVM_BULK_STAGES
+#define KVM_BULK_STAGES 4
+#endif
+constexpr int kBulkStages = KVM_BULK_STAGES;   // batch launches (1 CTA/SM); stages / 2 tiles loading
 constexpr int kBulkStagesSmall = 2;   // one-move launches: 3 CTAs/SM, one tile each
 constexpr int bulk_smem_bytes(int stages) { return stages * kTileBytes + 64; }
 
