@@ -320,3 +320,61 @@ def test_migrate_between_vllm_caches_equals_swap_blocks(layout, engine):
         assert torch.equal(got.view(torch.int16), e.view(torch.int16))
     sp.close()
     dp.close()
+
+
+@pytest.mark.parametrize("layout", ["native", "flash_attn", "flashinfer"])
+@pytest.mark.parametrize("engine", ["ldg", "bulk"])
+def test_fp8_kv_caches_migrate_like_vllm_swap_blocks(layout, engine):
+    """vLLM's fp8 KV caches (kv_cache_dtype="fp8": one byte per element, stored as uint8 / float8_e4m3fn)
+    are bytes to the copy path: a pool with elem_bytes = 1 (native layout, or vLLM's own per-layer caches
+    registered in place) migrates byte-identically to vLLM swap_blocks with the same mapping."""
+    import ctypes
+
+    from paper_2501_06709_b200 import _native
+    from paper_2501_06709_b200.foreign import StridedKVPool, vllm_cache_shape
+    vops = _vllm_ops()
+    L, nb, H, D = 3, 48, 8, 128
+    shape = ModelShape("fp8", layers=L, kv_heads=H, head_dim=D, q_heads=H, d_model=H * D, elem_bytes=1)
+    piece = shape.piece_bytes                                   # 16 KiB
+    rng = np.random.default_rng(4)
+    sb = rng.permutation(nb)[:19].astype(np.int32)
+    db = rng.permutation(nb)[:19].astype(np.int32)
+
+    def rand_u8(shp, seed):
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        return torch.randint(0, 256, shp, generator=g, device="cuda", dtype=torch.uint8)
+
+    if layout == "native":
+        src = KVPool(shape, nb, tensor=rand_u8((L, 2, nb, 16, H, D), 1).view(torch.float8_e4m3fn))
+        dst = KVPool(shape, nb, tensor=rand_u8((L, 2, nb, 16, H, D), 2).view(torch.float8_e4m3fn))
+        expect = dst.tensor.view(torch.uint8).clone()
+        m = torch.from_numpy(np.stack([sb, db], 1).astype(np.int64))
+        for l in range(L):
+            for kv in range(2):
+                vops.swap_blocks(src.tensor.view(torch.uint8)[l, kv], expect[l, kv], piece, m)
+        got = lambda: dst.tensor.view(torch.uint8)           # noqa: E731
+    else:
+        shp = vllm_cache_shape(layout, nb, 16, H, D)
+        srcs = [rand_u8(shp, 10 + l) for l in range(L)]
+        dsts = [rand_u8(shp, 20 + l) for l in range(L)]
+        src, dst = StridedKVPool.from_vllm(srcs, layout), StridedKVPool.from_vllm(dsts, layout)
+        exp_l = [t.clone() for t in dsts]
+        for s_, e in zip(srcs, exp_l):
+            if layout == "flash_attn":
+                m = torch.from_numpy(np.stack([sb, db], 1).astype(np.int64))
+                for kv in range(2):
+                    vops.swap_blocks(s_[kv], e[kv], piece, m)
+            else:
+                m = torch.from_numpy(np.concatenate([np.stack([2 * sb + kv, 2 * db + kv], 1) for kv in range(2)])
+                                     .astype(np.int64))
+                vops.swap_blocks(s_, e, piece, m)
+        expect = torch.stack(exp_l)
+        got = lambda: torch.stack(dsts)                       # noqa: E731
+    mv = _native.Move()
+    mv.src_pool, mv.dst_pool, mv.n_blocks = src.pool_id, dst.pool_id, len(sb)
+    mv.src_blocks, mv.dst_blocks = sb.ctypes.data, db.ctypes.data
+    flags = _native.KVM_F_BLOCKS_ON_HOST | (_native.KVM_F_ENGINE_BULK if engine == "bulk" else 0)
+    _native.check(_native.lib().kvm_migrate((_native.Move * 1)(mv), 1, flags,
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(got(), expect)
