@@ -30,6 +30,24 @@ def test_reference_arm_contract():
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
 
 
+def test_reference_arm_under_torchrun_two_ranks():
+    """The driver launches the reference arm like ours at N > 1 (torch.distributed.run, 2 ranks):
+    rank 0 alone runs it and prints the one line, the other rank exits 0 without work."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--impl", "reference", "--gpus", "2", "--workload", "7b-512", "--steps", "3",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0 and BASE_KEYS <= set(d)
+
+
 def test_self_launch_runs_n_ranks_cpu():
     """`python bench.py --gpus 2` without torchrun re-launches itself under
     torch.distributed.run with 2 ranks (gloo here, no GPU): rank 0 prints the
