@@ -290,7 +290,8 @@ def test_randomized_batches_vs_oracle(seed):
         if key not in expect:
             expect[key] = (dst, dst.tensor.view(torch.int16).cpu().numpy())
         orc.migrate(src.tensor.view(torch.int16).cpu().numpy(), _desc(src), expect[key][1], _desc(dst), sb, db)
-    _run(moves, engine | (_native.KVM_F_BLOCKS_ON_HOST if host else 0))
+    cap = int(rng.choice([0, 0, 0, 1, 5, 37]))   # copy SM budget (KVM_F_MAX_SMS), drawn last
+    _run(moves, engine | (_native.KVM_F_BLOCKS_ON_HOST if host else 0) | _native.KVM_F_MAX_SMS(cap))
     for dst, exp in expect.values():
         assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
     assert flags[:len(moves)].cpu().tolist() == list(range(1, len(moves) + 1))
@@ -654,7 +655,8 @@ def test_randomized_queue_sized_batches_vs_oracle(seed):
         if id(dst) not in expect:
             expect[id(dst)] = (dst, dst.tensor.view(torch.int16).cpu().numpy())
         orc.migrate(src.tensor.view(torch.int16).cpu().numpy(), _desc(src), expect[id(dst)][1], _desc(dst), sb, db)
-    _run(moves, _native.KVM_F_ENGINE_BULK | (_native.KVM_F_BLOCKS_ON_HOST if host else 0))
+    cap = int(rng.choice([0, 0, 2, 16, 64]))     # copy SM budget (KVM_F_MAX_SMS), drawn last
+    _run(moves, _native.KVM_F_ENGINE_BULK | (_native.KVM_F_BLOCKS_ON_HOST if host else 0) | _native.KVM_F_MAX_SMS(cap))
     for dst, exp in expect.values():
         assert np.array_equal(dst.tensor.view(torch.int16).cpu().numpy(), exp)
     c = ctrl.cpu().numpy()
