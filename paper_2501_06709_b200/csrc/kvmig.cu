@@ -636,7 +636,9 @@ static int dev_init(int device, DevState& ds) {
   int occ = 0;
   KVM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, migrate_ldg_kernel<false, BatchParams>,
                                                              kLdgThreads, 0));
-  ds.ldg_grid = sm_count(device) * std::max(occ, 1);
+  // 3 CTAs/SM, not the occupancy limit (4): with 4 the register-path copy thrashes HBM (7B-4k
+  // compaction 2 937 vs 3 077 GB/s; 7B-16k 2 680 vs 3 125; profiles/r2_session3/ldg_occupancy.json)
+  ds.ldg_grid = sm_count(device) * std::min(std::max(occ, 1), 3);
   const int big = bulk_smem_bytes(kBulkStages), small = bulk_smem_bytes(kBulkStagesSmall);
   const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
   KVM_CUDA_TRY(cudaFuncSetAttribute(migrate_bulk_kernel<false, BatchParams, kBulkStages>, attr, big));

@@ -3,7 +3,7 @@
 
     python tools/bench_copy_sms.py [--out f.json]
 
-Arms, bulk engine, 7B KV: a 7B-4k compaction inside one pool (HBM: 2 bytes
+Arms, bulk engine (or --engine ldg: n x 4 CTAs of 256 threads), 7B KV: a 7B-4k compaction inside one pool (HBM: 2 bytes
 of traffic per payload byte) and a 1 024-token push into pinned host memory
 (PCIe: the only link a one-GPU box has), each with the copy capped at
 1 .. 148 SMs.  The per-SM rate of the HBM arm at small budgets is what one
@@ -32,7 +32,9 @@ SMS = (1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 0)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--engine", choices=["bulk", "ldg"], default="bulk")
     a = ap.parse_args()
+    eng = _native.KVM_F_ENGINE_BULK if a.engine == "bulk" else 0
     lib = _native.lib()
     st = torch.cuda.Stream()
     sp = ctypes.c_void_p(st.cuda_stream)
@@ -55,10 +57,10 @@ def main():
         m = _native.Move()
         m.src_pool, m.dst_pool, m.n_blocks = src.pool_id, dst.pool_id, len(sb)
         m.src_blocks, m.dst_blocks = sb.ctypes.data, db.ctypes.data
-        flags = _native.KVM_F_BLOCKS_ON_HOST | _native.KVM_F_ENGINE_BULK | _native.KVM_F_MAX_SMS(cap)
+        flags = _native.KVM_F_BLOCKS_ON_HOST | eng | _native.KVM_F_MAX_SMS(cap)
         return lambda: _native.check(lib.kvm_migrate(ctypes.byref(m), 1, flags, sp))
 
-    res = {"engine": "bulk", "hbm_compaction_7b_4k": {}, "pcie_push_7b_1k": {}}
+    res = {"engine": a.engine, "hbm_compaction_7b_4k": {}, "pcie_push_7b_1k": {}}
     n = 256
     pool = KVPool(sh, 2 * n + 8)
     pool.tensor.view(torch.int16).random_(-2 ** 15, 2 ** 15 - 1)
