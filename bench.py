@@ -26,7 +26,12 @@ the same metric through the public API with host block lists (pinned staging
 row every step.  At N > 1 the same ring done the library way (NCCL
 batch_isend_irecv of the gathered request) is timed in the same run
 (`library`), and the 70B-GQA 16k-token ring (configs[3]) is measured beside
-the headline (`extra_workloads`).
+the headline (`extra_workloads`), with the push on 32 / 64 SMs
+(`config.push_sm_budget_ab`) and, on rank 0, GPU 0 -> 1 split and
+time-to-first-decode extras.  At N = 1 the line's `kernels` object adds the
+re-prefill (vs cuBLAS, with energy per launch), decode, the configs[2] split,
+the one-block move latency, the push over PCIe to pinned host memory, decode
+beside a migration / re-prefill, and the copy SM-budget sweep.
 
 --impl reference: the reference has no data path (it deletes executed moves,
 sim.py:221-223), so its CPU implementation of the path is the oracle port
