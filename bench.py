@@ -1240,7 +1240,8 @@ def run_compact(args, ctx) -> int:
         "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": 2 * n * 4, "d2h_bytes_per_step": n * 4,
                 "latency_ms_p50": round(1e3 * statistics.median(e2e_lat), 4),
                 "latency_definition": "one synchronous call through the API: issue -> result row on the host",
-                "path": "MigrationExecutor.compact(stream_ordered) -> kvm_compact(host block lists) -> "
+                "path": "MigrationExecutor.compact(stream_ordered) -> kvm_compact(host block lists: <= 256 blocks "
+                        "travel H2D inside the kernel's parameter block, more are staged by a pinned copy) -> "
                         "table row D2H -> host waits for the row (next step issued meanwhile)"},
         "library": lib_line,
         "gpu_launches": int(launches),

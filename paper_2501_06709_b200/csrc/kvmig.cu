@@ -172,7 +172,7 @@ struct MigrateParamsT {
   DevMove m[kMoves];
   int32_t blocks[kInline > 0 ? 2 * kInline : 1];
 };
-constexpr int kSmallInline = 128;
+constexpr int kSmallInline = 256;   // a 7B-4k request (256 blocks) rides in the parameters
 using BatchParams = MigrateParamsT<KVM_MAX_MOVES, 0>;
 using SmallParams = MigrateParamsT<1, kSmallInline>;
 

@@ -337,10 +337,10 @@ def test_compact_stream_ordered_back_to_back():
 
 
 @pytest.mark.parametrize("engine", ["ldg", "bulk"])
-@pytest.mark.parametrize("n", [1, 127, 128, 129, 300])
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 255, 256, 257, 300])
 @pytest.mark.parametrize("consumers", ["none", "device", "host_flag", "sys_scope"])
 def test_single_move_launch_class(engine, n, consumers):
-    """One-move launches use the small parameter block: host lists of <= 128
+    """One-move launches use the small parameter block: host lists of <= 256
     blocks ride inline (no staging copy), larger ones are staged; moves with no
     table row / flags skip completion accounting; completion stores are .gpu
     scope when every written pointer is this GPU's memory, .sys for a flag in
