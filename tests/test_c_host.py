@@ -39,3 +39,15 @@ def test_c_host_migration(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert "migration: 5 blocks" in out.stdout and "foreign layout: 3 blocks" in out.stdout
     assert "MISMATCH" not in out.stdout and out.stdout.count("bit-exact") == 2
+
+
+@pytest.mark.gpu
+def test_c_host_one_block_latency(tmp_path):
+    """--latency: a tracked one-block 7B move issued from C lands (event to event) in tens of microseconds
+    and reports its host issue time; the JSON line is what DESIGN.md quotes for a C/C++ host."""
+    import json
+    exe = _build(tmp_path)
+    out = subprocess.run([exe, "--latency"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    d = json.loads(out.stdout.strip().splitlines()[-1])["one_block_7b_move"]
+    assert d["bytes"] == 8 << 20 and 0 < d["host_issue_us_p50"] < d["issue_to_landed_us_p50"] < 200

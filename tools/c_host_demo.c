@@ -7,14 +7,17 @@
  *       -L paper_2501_06709_b200/_lib -lkvmig -Wl,-rpath,$PWD/paper_2501_06709_b200/_lib -o c_host_demo
  *   ./c_host_demo            # scheduler (CPU) + migration (GPU, if any)
  *   ./c_host_demo --cpu-only
+ *   ./c_host_demo --latency  # one-block 7B move issued from C: issue-to-landed and host issue (JSON)
  *
  * Exit status 0 on success.  This is what a C/C++/Go/Java host binds (the
  * reference itself is Python; INTEGRATION.md shows its ctypes stub).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include "kvmig.h"
 
@@ -22,7 +25,13 @@
 extern int cudaMalloc(void** p, size_t n);
 extern int cudaFree(void* p);
 extern int cudaMemcpy(void* dst, const void* src, size_t n, int kind);
+extern int cudaMemset(void* p, int v, size_t n);
 extern int cudaDeviceSynchronize(void);
+extern int cudaStreamCreate(void** s);
+extern int cudaEventCreate(void** e);
+extern int cudaEventRecord(void* e, void* s);
+extern int cudaEventSynchronize(void* e);
+extern int cudaEventElapsedTime(float* ms, void* a, void* b);
 #define H2D 1
 #define D2H 2
 
@@ -164,7 +173,68 @@ static int foreign_demo(void) {
   return bad;
 }
 
+static int cmp_f(const void* a, const void* b) {
+  float x = *(const float*)a, y = *(const float*)b;
+  return (x > y) - (x < y);
+}
+
+/* --latency: the one-block (8 MiB, Llama-2-7B) move a C/C++ host issues -- host block lists, the
+ * destination table row rewritten and the done flag released -- timed from a CUDA event recorded
+ * on the idle stream right before kvm_migrate to one right after it (host issue + kernel), and the
+ * host time of the call itself; medians over 300 calls after 50 warm-ups. */
+static int latency_demo(void) {
+  kvm_pool_desc d = {32, 32, 128, 16, 64, 2};
+  int64_t bytes = 0;
+  check(kvm_pool_bytes(&d, &bytes), "kvm_pool_bytes");
+  void *a = NULL, *b = NULL, *ctl = NULL, *st = NULL, *e0 = NULL, *e1 = NULL;
+  if (cudaMalloc(&a, (size_t)bytes) || cudaMalloc(&b, (size_t)bytes) || cudaMalloc(&ctl, 4096)) return 1;
+  cudaMemset(ctl, 0, 4096);
+  cudaStreamCreate(&st);
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int pa = check(kvm_pool_register(0, a, &d), "register"), pb = check(kvm_pool_register(0, b, &d), "register");
+  int32_t sb[] = {3}, db[] = {9};
+  enum { N = 350, W = 50 };
+  float lat[N], host[N];
+  for (int i = 0; i < N; ++i) {
+    kvm_move m;
+    memset(&m, 0, sizeof(m));
+    m.src_pool = pa;
+    m.dst_pool = pb;
+    m.n_blocks = 1;
+    m.src_blocks = sb;
+    m.dst_blocks = db;
+    m.dst_table_row = (int32_t*)((char*)ctl + 256);
+    m.done_flag = (uint32_t*)ctl;
+    m.done_value = (uint32_t)(i + 1);
+    cudaDeviceSynchronize();
+    struct timespec t0, t1;
+    cudaEventRecord(e0, st);
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    check(kvm_migrate(&m, 1, KVM_F_BLOCKS_ON_HOST | KVM_F_ENGINE_BULK, st), "kvm_migrate");
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    lat[i] = ms * 1000.0f;
+    host[i] = (float)((t1.tv_sec - t0.tv_sec) * 1e6 + (t1.tv_nsec - t0.tv_nsec) / 1e3);
+  }
+  qsort(lat + W, N - W, sizeof(float), cmp_f);
+  qsort(host + W, N - W, sizeof(float), cmp_f);
+  printf("{\"one_block_7b_move\": {\"bytes\": %lld, \"issue_to_landed_us_p50\": %.2f, \"host_issue_us_p50\": %.2f, "
+         "\"host\": \"C (tools/c_host_demo.c --latency)\"}}\n",
+         (long long)(bytes / d.num_blocks), lat[W + (N - W) / 2], host[W + (N - W) / 2]);
+  kvm_pool_unregister(pa);
+  kvm_pool_unregister(pb);
+  cudaFree(a);
+  cudaFree(b);
+  cudaFree(ctl);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && strcmp(argv[1], "--latency") == 0) return latency_demo();
   int cpu_only = argc > 1 && strcmp(argv[1], "--cpu-only") == 0;
   printf("libkvmig ABI %d\n", kvm_version());
   int rc = scheduler_demo();
