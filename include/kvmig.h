@@ -26,6 +26,10 @@
  *     ValueError, KVM_ERR_NOT_FOUND -> NotPlaced, KVM_ERR_CUDA -> KvmCudaError
  *     (a KvPackError subclass).
  *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *     kvm_migrate / kvm_compact / kvm_reprefill / kvm_split_migrate on a stream
+ *     that is being captured into a CUDA graph return KVM_ERR_UNSUPPORTED: their
+ *     launches take per-launch staging and counter state that the host orders
+ *     between launches, which a graph replay would bypass.
  *   - The library never allocates or frees pool memory: pools are borrowed
  *     device allocations (e.g. torch tensors) registered by pointer.
  *   - KV layout (frozen, vLLM-style layer-major):

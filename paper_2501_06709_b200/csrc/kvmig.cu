@@ -976,6 +976,15 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
   return rc;
 }
 
+int reject_capture(cudaStream_t stream, const char* what) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  KVM_CUDA_TRY(cudaStreamIsCapturing(stream, &st));
+  if (st != cudaStreamCaptureStatusNone)
+    return fail(KVM_ERR_UNSUPPORTED, std::string(what) + " cannot be captured into a CUDA graph (its launches "
+                                     "take per-launch staging / counter state the host orders)");
+  return KVM_OK;
+}
+
 static int migrate_batch(const kvm_move* moves, int n, int flags, cudaStream_t stream) {
   const Pool* sp0 = get_pool(moves[0].src_pool);
   if (!sp0) return KVM_ERR_NOT_FOUND;
@@ -1227,6 +1236,7 @@ int kvm_migrate(const kvm_move* moves, int n_moves, int flags, void* stream) {
                 KVM_F_CTAS_PER_SM(0xff) | KVM_F_MAX_SMS(0xff)))
     return fail(KVM_ERR_INVALID, "unknown flags");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int rc = reject_capture(s, "kvm_migrate")) return rc;
   for (int i = 0; i < n_moves; i += KVM_MAX_MOVES) {
     int rc = migrate_batch(moves + i, std::min(KVM_MAX_MOVES, n_moves - i), flags, s);
     if (rc) return rc;

@@ -13,6 +13,10 @@ namespace kvm {
 // Thread-local last-error text + code helpers (defined in kvmig.cu).
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
+// KVM_ERR_UNSUPPORTED if `stream` is being captured into a CUDA graph: the copy and re-prefill launches
+// take per-launch host state (staging slots, counter slots, the tile queue's word) that a graph replay
+// would reuse without the host's ordering.  Defined in kvmig.cu.
+int reject_capture(cudaStream_t stream, const char* what);
 
 #define KVM_CUDA_TRY(expr)                                   \
   do {                                                       \

@@ -1179,6 +1179,7 @@ static bool is_sm100(int dev) {
 
 extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
   if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
+  if (int rc = reject_capture(static_cast<cudaStream_t>(stream), "kvm_reprefill")) return rc;
   const Pool* pool = get_pool(a->dst_pool);
   if (!pool) return KVM_ERR_NOT_FOUND;
   const kvm_pool_desc& d = pool->desc;
@@ -1219,6 +1220,7 @@ extern "C" int kvm_reprefill(const kvm_reprefill_args* a, void* stream) {
 
 extern "C" int kvm_split_migrate(const kvm_split_args* a, void* stream) {
   if (!a) return fail(KVM_ERR_INVALID, "args is NULL");
+  if (int rc = reject_capture(static_cast<cudaStream_t>(stream), "kvm_split_migrate")) return rc;
   const Pool* dst = get_pool(a->dst_pool);
   const Pool* src = dst ? get_pool(a->src_pool) : nullptr;
   if (!dst || !src) return KVM_ERR_NOT_FOUND;

@@ -709,3 +709,33 @@ def test_executor_copy_sms():
     assert ex.where(9).gpu == 1 and torch.equal(before, after)
     with pytest.raises(ConfigError):
         MigrationExecutor(pools, copy_sms=256)
+
+
+def test_graph_capture_is_rejected_not_corrupted():
+    """kvm_migrate (and the re-prefill entry points) refuse a stream under CUDA-graph capture with
+    KVM_ERR_UNSUPPORTED instead of baking per-launch staging / queue state into a graph whose replays
+    would race the host's bookkeeping; the same move runs normally afterwards."""
+    from paper_2501_06709_b200.errors import KvmUnsupported
+    from paper_2501_06709_b200.reprefill import reprefill, synthetic_hidden, synthetic_weights
+
+    src, dst = KVPool(SMALL, 16), KVPool(SMALL, 16)
+    _fill(src, 1)
+    sb, db = np.arange(4, dtype=np.int32), np.arange(8, 12, dtype=np.int32)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(KvmUnsupported):
+        with torch.cuda.graph(g, stream=s):
+            m = _move(src, dst, sb, db)
+            _native.check(_native.lib().kvm_migrate(ctypes.byref(m), 1, _native.KVM_F_BLOCKS_ON_HOST,
+                                                    ctypes.c_void_p(s.cuda_stream)))
+    shape = ModelShape("g", layers=1, kv_heads=1, head_dim=128, q_heads=1, d_model=64)
+    pool = KVPool(shape, 4, dtype=torch.bfloat16)
+    x, w = synthetic_hidden(shape, 16, 0, seed=1), synthetic_weights(shape, 0, with_q=False, seed=2)
+    blocks = torch.arange(1, dtype=torch.int32, device="cuda")
+    g2 = torch.cuda.CUDAGraph()
+    with pytest.raises(KvmUnsupported):
+        with torch.cuda.graph(g2, stream=s):
+            reprefill(pool, x, w, blocks, stream=s)
+    torch.cuda.synchronize()
+    _run([_move(src, dst, sb, db)], _native.KVM_F_BLOCKS_ON_HOST)
+    assert torch.equal(dst.tensor[:, :, 8:12].view(torch.int16), src.tensor[:, :, 0:4].view(torch.int16))
