@@ -905,7 +905,7 @@ static int migrate_batch_t(P& p, const kvm_move* moves, int n, int flags, cudaSt
   // chunks per CTA (below that the queue's atomics cost more than the balance buys: measured on a
   // 4-block 7B move, 11 -> 14 us).  Its counter is word 0 or 1 of the staging slot's counters,
   // alternating per use of the slot (each launch zeroes the other; uses of one slot are serialised
-  // by slot_acquire's event wait).  KVM_COPY_STATIC=1 keeps the static grid-stride partition and
+  // by slot_acquire's event wait or by their common stream).  KVM_COPY_STATIC=1 keeps the static grid-stride partition and
   // KVM_COPY_CHUNK=n sets the largest request (A/B).
   static const bool static_copy = [] {
     const char* e = getenv("KVM_COPY_STATIC");
