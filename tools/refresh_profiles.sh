@@ -18,6 +18,11 @@ run bench_reference 600 python bench.py --impl reference
 for w in 13b-8k 70b-16k; do run "bench_$w" 600 python bench.py --workload "$w" --no-cpu-baseline --no-extras; done
 run migrate_vs_library 600 python tools/bench_migrate_baselines.py
 run host_link 300 python tools/bench_host_link.py
+run interference 300 python tools/bench_interference.py
+run copy_sms_bulk 300 python tools/bench_copy_sms.py
+run copy_sms_ldg 300 python tools/bench_copy_sms.py --engine ldg
+run launch_gap 300 python tools/bench_launch_gap.py
+run reprefill_rounds 300 python tools/bench_reprefill_rounds.py
 run concurrent 600 python tools/bench_concurrent.py
 for a in "" "--rows 4096" "--shape llama2-7b --rows 2048" "--kv-only" "--rows 1456" "--rows 1280"; do
   run "reprefill_${a// /_}" 300 python tools/bench_reprefill.py $a
