@@ -657,7 +657,6 @@ class Ring:
                 self.step(engine, host=False, max_sms=max_sms)
         self.stream.synchronize()
         self.ctx["barrier"]()
-        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = _native.launch_count()
         torch.cuda.synchronize()
@@ -666,10 +665,11 @@ class Ring:
             meter.start()
         if clocks is not None:
             clocks.__enter__()
+        # throughput: K steps back to back (no per-launch events in the region, as at N = 1)
         with torch.cuda.stream(self.stream):
             t0.record(self.stream)
             for i in range(K):
-                self.step(engine, host=False, ev=ev[i], max_sms=max_sms)
+                self.step(engine, host=False, max_sms=max_sms)
             t1.record(self.stream)
         self.stream.synchronize()
         torch.cuda.synchronize()
@@ -677,9 +677,18 @@ class Ring:
             clocks.__exit__()
         if meter is not None:
             meter.stop()
+        launches = _native.launch_count() - launches0
+        self.ctx["barrier"]()
+        # latency: the same step with an event pair around the push and one after the wait, after the region
+        KL = min(K, 30)
+        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(KL)]
+        with torch.cuda.stream(self.stream):
+            for i in range(KL):
+                self.step(engine, host=False, ev=ev[i], max_sms=max_sms)
+        self.stream.synchronize()
+        torch.cuda.synchronize()
         self.ctx["barrier"]()
         arrived = self.ctx["all_ok"](self.landed())
-        launches = _native.launch_count() - launches0
         elapsed = allreduce_max(t0.elapsed_time(t1), dev)
         push = [a.elapsed_time(b) for a, b, _ in ev]
         stepms = [a.elapsed_time(c) for a, _, c in ev]
@@ -1036,7 +1045,8 @@ def run_ring(args, ctx) -> int:
             "latency_ms": {"p50": round(main["push_p50"], 4), "p99": round(main["push_p99"], 4),
                            "definition": "per step on each rank: event before the push launch -> event after the "
                                          "push kernel, whose last CTA release-stores the done flag into the "
-                                         "destination (system scope) after the block-table row; max over ranks",
+                                         "destination (system scope) after the block-table row; max over ranks; "
+                                         "up to 30 steps timed one by one after the throughput region",
                            "step_p50": round(main["step_p50"], 4), "step_p99": round(main["step_p99"], 4),
                            "step_definition": "push + wait until the incoming move's done flag is visible here "
                                               "(ld.acquire.sys)"},
